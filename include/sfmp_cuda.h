@@ -1,0 +1,177 @@
+/*
+ * sfmp_cuda.h -- C ABI of the B200-native (sm_100a) SFMP mixed-precision GEMM.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   sfmp::gemv(const PackedModel&, const Vector&, GemvStats*)   lutgemm.hpp:57
+ * (definition lutgemm.cpp:95-135), together with the packed-model ingest it
+ * depends on (deserialize layout.cpp:210-279, compute_block_offsets
+ * layout.cpp:301-314) and the dequant oracle it is validated against
+ * (dequantize_model layout.cpp:316-332).  Paths are relative to
+ * /root/reference/proj.  Plain C: pointers, sizes and integer status codes;
+ * no torch or C++ types cross this boundary.  A header-only C++ shim that
+ * restores the reference's exception types is in include/sfmp/cuda.hpp.
+ *
+ * Semantics
+ *  - Weights are ingested as the exact SFMPPKD1 bytes.  The
+ *    block payload region is uploaded verbatim; no re-quantisation.
+ *  - sfmp_gemm computes, for every token t < M,
+ *        y[t] = gemv(model, x[t])          (M>1 loops the GEMV)
+ *    i.e. y = x * dequantize_model(model)^T with x and y in the ORIGINAL
+ *    column/row order: the col_perm gather (reorder_activation_in,
+ *    reorder.cpp:103-111) and row_perm scatter (reorder_activation_out,
+ *    reorder.cpp:113-121) happen inside the kernels.
+ *  - Results are deterministic and independent of grid size and stream
+ *    (no floating-point atomics; fixed-order split-K).
+ *  - Everything is stream-ordered on the caller's stream.  Calls on distinct
+ *    streams are safe when each passes its own workspace (or workspace=NULL
+ *    is used from one stream at a time).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns SFMP_ERR_CUDA.
+ */
+#ifndef SFMP_CUDA_H
+#define SFMP_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFMP_CUDA_ABI_VERSION 1
+
+/* Status codes, 1:1 with the reference exception kinds (errors.hpp:9-36). */
+typedef enum sfmp_status {
+    SFMP_OK = 0,
+    SFMP_ERR_SHAPE = 1,               /* sfmp::ShapeError   (e.g. x.len != cols, lutgemm.cpp:96) */
+    SFMP_ERR_CONFIG = 2,              /* sfmp::ConfigError  (e.g. reps < 1, lutgemm.cpp:138)     */
+    SFMP_ERR_FORMAT_BAD_MAGIC = 3,    /* FormatError{bad_magic}   layout.cpp:216-217             */
+    SFMP_ERR_FORMAT_BAD_VERSION = 4,  /* FormatError{bad_version} layout.cpp:220-222             */
+    SFMP_ERR_FORMAT_TRUNCATED = 5,    /* FormatError{truncated}   layout.cpp:154-159             */
+    SFMP_ERR_FORMAT_INVARIANT = 6,    /* FormatError{invariant}   layout.cpp:88-124, :229-275    */
+    SFMP_ERR_FORMAT_IO = 7,           /* FormatError{io}          layout.cpp:281-299             */
+    SFMP_ERR_CUDA = 8,                /* CUDA runtime / launch failure, or no sm_100 device      */
+    SFMP_ERR_NCCL = 9,                /* collective failure (sharded path)                        */
+    SFMP_ERR_INVALID_ARGUMENT = 10,   /* NULL pointer / bad enum                                  */
+    SFMP_ERR_NOMEM = 11,              /* host or device allocation failed                         */
+    SFMP_ERR_UNSUPPORTED = 12         /* valid request this build does not implement             */
+} sfmp_status;
+
+/* Activation element type.  Accumulation is always f32; y is always f32. */
+typedef enum sfmp_dtype { SFMP_F32 = 0, SFMP_F16 = 1, SFMP_BF16 = 2 } sfmp_dtype;
+
+/* Kernel selection (SFMP_PATH_AUTO picks by M: decode GEMV for M<=16,
+ * tcgen05 GEMM for larger M). Forcing a path is for tests and benches. */
+typedef enum sfmp_path {
+    SFMP_PATH_AUTO = 0,
+    SFMP_PATH_GEMV = 1,     /* K1: decode GEMV, M <= 16, HBM-bound            */
+    SFMP_PATH_GEMM = 2,     /* K2: tcgen05/TMEM prefill GEMM                   */
+    SFMP_PATH_GENERIC = 3   /* any m_b/n_b/M; simple CUDA-core kernel          */
+} sfmp_path;
+
+/* Opaque device-resident model (owns payload, offsets, perms, bit map). */
+typedef struct sfmp_dev_model sfmp_dev_model;
+
+/* Header / geometry summary (PackedModel fields, layout.hpp:36-53). */
+typedef struct sfmp_model_info {
+    uint64_t rows, cols;           /* m (output features), n (input features)            */
+    uint32_t m_b, n_b;             /* block_rows, group_size                              */
+    int32_t floor_bits, ceil_bits; /* candidate bit-widths                                */
+    int32_t mode;                  /* ReorderMode: 0 none, 1 row, 2 col, 3 rowcol        */
+    uint64_t block_count;          /* K = (m/m_b)(n/n_b)                                  */
+    uint64_t blocks_high;          /* blocks at ceil_bits (when ceil != floor)            */
+    double avg_code_bits;          /* sum_k bits_k / K                                    */
+    uint64_t payload_bytes;        /* bytes of the block region (scales+zeros+planes)     */
+    uint64_t device_bytes;         /* device memory held by the model                     */
+    uint32_t shard, num_shards;    /* (0,1) for an unsharded model                        */
+    uint64_t out_rows;             /* length of one output row of y written by sfmp_gemm  */
+    uint64_t global_rows;          /* rows of the whole (unsharded) matrix                */
+} sfmp_model_info;
+
+/* A PackedModel (layout.hpp:36-53) given field by field.  plane_ptrs holds
+ * sum_k block_bits[k] pointers in block order, planes least-significant
+ * first, each m_b*n_b/8 bytes (PackedBlock::planes, layout.hpp:22-27). */
+typedef struct sfmp_model_parts {
+    uint64_t rows, cols;
+    uint32_t m_b, n_b;
+    int32_t floor_bits, ceil_bits, mode;
+    const uint32_t* row_perm;           /* rows entries, NULL unless mode has row */
+    const uint32_t* col_perm;           /* cols entries, NULL unless mode has col */
+    const uint8_t* block_bits;          /* K entries                               */
+    const uint16_t* const* scales;      /* K pointers, m_b fp16 payloads each      */
+    const uint16_t* const* zeros;       /* K pointers, m_b fp16 payloads each      */
+    const uint8_t* const* plane_ptrs;   /* sum(block_bits) pointers                */
+} sfmp_model_parts;
+
+/* ---- library ---------------------------------------------------------- */
+int sfmp_abi_version(void);
+const char* sfmp_status_string(sfmp_status s);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* sfmp_last_error(void);
+/* Number of usable sm_100 devices (0 on a host without a B200). */
+int sfmp_device_count(void);
+
+/* ---- host-only ingest (no device needed) -------------------------------- */
+/* Full SFMPPKD1 validation (deserialize + PackedModel::validate). */
+sfmp_status sfmp_parse_header(const uint8_t* bytes, size_t len, sfmp_model_info* info);
+/* compute_block_offsets (layout.cpp:301-314): absolute byte offset of each
+ * block in the serialized stream. */
+sfmp_status sfmp_block_offsets(const uint8_t* bytes, size_t len, uint64_t* offsets,
+                               uint64_t count);
+
+/* ---- model lifetime ------------------------------------------------------ */
+/* Ingest SFMPPKD1 bytes (read_packed_file/deserialize equivalent) onto `device`. */
+sfmp_status sfmp_model_create(const uint8_t* bytes, size_t len, int device,
+                              sfmp_dev_model** out);
+/* Ingest an in-memory PackedModel (already validated by its owner). */
+sfmp_status sfmp_model_create_from_parts(const sfmp_model_parts* parts, int device,
+                                         sfmp_dev_model** out);
+/* Ingest only the block rows owned by `shard` of `num_shards` under the snake
+ * (boustrophedon) block-row partition.  The shard's
+ * sfmp_gemm writes y_local[M][out_rows] in shard-local reordered row order;
+ * sfmp_unpermute_gathered() turns the all-gathered shards into y. */
+/* Host-only shard plan: gather_map[num_shards*shard_rows] maps (shard g,
+ * local row i) to the ORIGINAL output row (0xFFFFFFFF for padding);
+ * *shard_rows receives the per-shard row count (padded to the largest). Pass
+ * gather_map=NULL to query *shard_rows only. */
+sfmp_status sfmp_shard_plan(const uint8_t* bytes, size_t len, uint32_t num_shards,
+                            uint32_t* gather_map, uint64_t* shard_rows);
+sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device,
+                                    uint32_t shard, uint32_t num_shards, sfmp_dev_model** out);
+sfmp_status sfmp_model_destroy(sfmp_dev_model* model);
+sfmp_status sfmp_model_get_info(const sfmp_dev_model* model, sfmp_model_info* info);
+
+/* ---- compute (device pointers, stream-ordered) ------------------------- */
+/* Bytes of scratch sfmp_gemm needs for this M (0 if none). */
+sfmp_status sfmp_workspace_size(const sfmp_dev_model* model, int64_t M, sfmp_path path,
+                                size_t* bytes);
+/* y[M][out_rows] (f32) = x[M][cols] (dtype) . W^T.  workspace may be NULL
+ * (the model's own scratch is used; then calls must not overlap). */
+sfmp_status sfmp_gemm(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M,
+                      float* y, void* workspace, size_t workspace_bytes, void* stream);
+sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype,
+                         int64_t M, float* y, void* workspace, size_t workspace_bytes,
+                         sfmp_path path, void* stream);
+/* Host-buffer convenience with the reference's calling convention: x and y
+ * are HOST arrays; copies, kernel and synchronisation happen inside. */
+sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M,
+                           float* y_host, void* stream);
+
+/* K3 (debug/parity): dense f32 W[rows][cols] in ORIGINAL order, bit-exact
+ * with dequantize_model (layout.cpp:316-332; quantizer.cpp:50-55). */
+sfmp_status sfmp_dequantize(const sfmp_dev_model* model, float* w, void* stream);
+/* Integer codes [rows][cols] in REORDERED (stored) order, bit-exact with
+ * unpack_block (layout.cpp:67-86). */
+sfmp_status sfmp_unpack_codes(const sfmp_dev_model* model, uint8_t* codes, void* stream);
+
+/* ---- sharded output assembly (multi-GPU) ---------------------- */
+/* gathered: [num_shards][M][shard_rows] f32 as produced by an all-gather of
+ * each shard's y_local.  Writes y[M][rows] in ORIGINAL row order.  `model`
+ * may be any shard of the same matrix (all shards carry the global map). */
+sfmp_status sfmp_unpermute_gathered(const sfmp_dev_model* model, const float* gathered,
+                                    int64_t M, float* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFMP_CUDA_H */

@@ -1,0 +1,298 @@
+"""B200-native SFMP mixed-precision GEMM -- Python host mirror of the reference API.
+
+The product is ``libsfmp_b200.so`` (C ABI in ``include/sfmp_cuda.h``; CUDA
+kernels for sm_100a in ``csrc/``).  This module binds it with ctypes and
+mirrors the reference's operator interface for the hot path
+(``/root/reference/proj``):
+
+* ``PackedModel`` bytes (SFMPPKD1, ``layout.cpp:179-279``) -> ``DeviceModel``
+* ``gemv(model, x)``                       -> ``lutgemm.hpp:57`` / ``lutgemm.cpp:95-135``
+* ``DeviceModel.dequantize()``             -> ``dequantize_model`` (``layout.cpp:316-332``)
+* ``DeviceModel.unpack_codes()``           -> ``unpack_block`` (``layout.cpp:67-86``)
+* ``compute_block_offsets(bytes)``         -> ``layout.cpp:301-314``
+* ``ShapeError`` / ``ConfigError`` / ``FormatError(kind)`` -> ``errors.hpp:9-36``
+
+PyTorch is plumbing only (device memory and streams).  There is no CPU
+fallback: without the built library or an sm_100 device the compute entry
+points raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsfmp_b200.so")
+
+# status codes (include/sfmp_cuda.h)
+OK, E_SHAPE, E_CONFIG, E_MAGIC, E_VERSION, E_TRUNC, E_INVARIANT, E_IO, E_CUDA, E_NCCL, E_ARG, \
+    E_NOMEM, E_UNSUPPORTED = range(13)
+F32, F16, BF16 = 0, 1, 2
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_GENERIC = 0, 1, 2, 3
+
+EXPORTED_SYMBOLS = (
+    "sfmp_abi_version", "sfmp_status_string", "sfmp_last_error", "sfmp_device_count",
+    "sfmp_parse_header", "sfmp_block_offsets", "sfmp_model_create",
+    "sfmp_model_create_from_parts", "sfmp_model_create_shard", "sfmp_model_destroy",
+    "sfmp_model_get_info", "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
+    "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered", "sfmp_shard_plan",
+)
+
+
+class SfmpError(RuntimeError):
+    code = -1
+
+
+class ShapeError(SfmpError, ValueError):
+    """sfmp::ShapeError (errors.hpp:9-12)."""
+
+
+class ConfigError(SfmpError, ValueError):
+    """sfmp::ConfigError (errors.hpp:14-17)."""
+
+
+class FormatError(SfmpError):
+    """sfmp::FormatError with .kind in {bad_magic, bad_version, truncated, invariant, io}."""
+
+    def __init__(self, kind: str, msg: str):
+        super().__init__(f"{kind}: {msg}")
+        self.kind = kind
+
+
+class CudaError(SfmpError):
+    pass
+
+
+class UnsupportedError(SfmpError):
+    pass
+
+
+_FORMAT_KINDS = {E_MAGIC: "bad_magic", E_VERSION: "bad_version", E_TRUNC: "truncated",
+                 E_INVARIANT: "invariant", E_IO: "io"}
+
+
+class ModelInfo(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("m_b", C.c_uint32),
+                ("n_b", C.c_uint32), ("floor_bits", C.c_int32), ("ceil_bits", C.c_int32),
+                ("mode", C.c_int32), ("block_count", C.c_uint64), ("blocks_high", C.c_uint64),
+                ("avg_code_bits", C.c_double), ("payload_bytes", C.c_uint64),
+                ("device_bytes", C.c_uint64), ("shard", C.c_uint32), ("num_shards", C.c_uint32),
+                ("out_rows", C.c_uint64), ("global_rows", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile libsfmp_b200.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    if force:
+        subprocess.run(["make", "-s", "-C", HERE, "clean"], check=True)
+    subprocess.run(["make", "-s", "-j8", "-C", HERE], check=True)
+    return LIB_PATH
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run paper_2602_01027_b200.build() "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, sz, i64 = C.c_void_p, C.c_size_t, C.c_int64
+    L.sfmp_abi_version.restype = C.c_int
+    L.sfmp_status_string.restype = C.c_char_p
+    L.sfmp_status_string.argtypes = [C.c_int]
+    L.sfmp_last_error.restype = C.c_char_p
+    L.sfmp_device_count.restype = C.c_int
+    L.sfmp_parse_header.argtypes = [vp, sz, C.POINTER(ModelInfo)]
+    L.sfmp_block_offsets.argtypes = [vp, sz, vp, C.c_uint64]
+    L.sfmp_model_create.argtypes = [vp, sz, C.c_int, C.POINTER(vp)]
+    L.sfmp_model_create_shard.argtypes = [vp, sz, C.c_int, C.c_uint32, C.c_uint32, C.POINTER(vp)]
+    L.sfmp_model_destroy.argtypes = [vp]
+    L.sfmp_model_get_info.argtypes = [vp, C.POINTER(ModelInfo)]
+    L.sfmp_workspace_size.argtypes = [vp, i64, C.c_int, C.POINTER(sz)]
+    L.sfmp_gemm.argtypes = [vp, vp, C.c_int, i64, vp, vp, sz, vp]
+    L.sfmp_gemm_ex.argtypes = [vp, vp, C.c_int, i64, vp, vp, sz, C.c_int, vp]
+    L.sfmp_gemm_host.argtypes = [vp, vp, i64, vp, vp]
+    L.sfmp_dequantize.argtypes = [vp, vp, vp]
+    L.sfmp_unpack_codes.argtypes = [vp, vp, vp]
+    L.sfmp_unpermute_gathered.argtypes = [vp, vp, i64, vp, vp]
+    L.sfmp_shard_plan.argtypes = [vp, sz, C.c_uint32, vp, C.POINTER(C.c_uint64)]
+    for name in ("sfmp_parse_header", "sfmp_block_offsets", "sfmp_model_create",
+                 "sfmp_model_create_shard", "sfmp_model_destroy", "sfmp_model_get_info",
+                 "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
+                 "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered",
+                 "sfmp_shard_plan"):
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    msg = lib().sfmp_last_error().decode(errors="replace")
+    if status == E_SHAPE:
+        raise ShapeError(msg)
+    if status == E_CONFIG:
+        raise ConfigError(msg)
+    if status in _FORMAT_KINDS:
+        raise FormatError(_FORMAT_KINDS[status], msg)
+    if status == E_CUDA:
+        raise CudaError(msg)
+    if status == E_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    e = SfmpError(f"{lib().sfmp_status_string(status).decode()}: {msg}")
+    e.code = status
+    raise e
+
+
+def device_count() -> int:
+    return int(lib().sfmp_device_count())
+
+
+def parse_header(data: bytes) -> dict:
+    """Validate an SFMPPKD1 stream on the host (deserialize + validate)."""
+    info = ModelInfo()
+    check(lib().sfmp_parse_header(data, len(data), C.byref(info)))
+    return info.as_dict()
+
+
+def compute_block_offsets(data: bytes) -> np.ndarray:
+    """compute_block_offsets (layout.cpp:301-314)."""
+    K = parse_header(data)["block_count"]
+    out = np.zeros(K, np.uint64)
+    check(lib().sfmp_block_offsets(data, len(data), out.ctypes.data, K))
+    return out
+
+
+def shard_plan(data: bytes, num_shards: int):
+    """Snake block-row partition: (gather_map[num_shards, shard_rows], shard_rows)."""
+    sr = C.c_uint64(0)
+    check(lib().sfmp_shard_plan(data, len(data), num_shards, None, C.byref(sr)))
+    gmap = np.zeros(num_shards * sr.value, np.uint32)
+    check(lib().sfmp_shard_plan(data, len(data), num_shards, gmap.ctypes.data, C.byref(sr)))
+    return gmap.reshape(num_shards, sr.value), int(sr.value)
+
+
+def _dtype_code(t) -> int:
+    import torch
+    return {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}[t.dtype]
+
+
+def _stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class DeviceModel:
+    """A packed model resident on one B200 (sfmp_model_create)."""
+
+    def __init__(self, data: bytes, device: int = 0, shard: int | None = None,
+                 num_shards: int = 1):
+        self._h = C.c_void_p()
+        self._data_len = len(data)
+        if shard is None:
+            check(lib().sfmp_model_create(data, len(data), device, C.byref(self._h)))
+        else:
+            check(lib().sfmp_model_create_shard(data, len(data), device, shard, num_shards,
+                                                C.byref(self._h)))
+        info = ModelInfo()
+        check(lib().sfmp_model_get_info(self._h, C.byref(info)))
+        self.info = info.as_dict()
+        self.device = device
+        self.rows, self.cols = self.info["rows"], self.info["cols"]
+        self.out_rows = self.info["out_rows"]
+        self._ws = {}
+
+    def close(self):
+        if self._h:
+            lib().sfmp_model_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def workspace_bytes(self, M: int, path: int = PATH_AUTO) -> int:
+        n = C.c_size_t(0)
+        check(lib().sfmp_workspace_size(self._h, M, path, C.byref(n)))
+        return int(n.value)
+
+    def workspace(self, M: int, path: int = PATH_AUTO):
+        import torch
+        nbytes = self.workspace_bytes(M, path)
+        key = (path, nbytes)
+        if nbytes and key not in self._ws:
+            self._ws[key] = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws.get(key)
+
+    def gemm(self, x, out=None, path: int = PATH_AUTO, workspace=None, stream=None):
+        """y[M, out_rows] (f32) = x[M, cols] . W^T, x/y torch CUDA tensors, original order."""
+        import torch
+        if x.dim() == 1:
+            x = x.unsqueeze(0)
+        if x.shape[-1] != self.cols:
+            raise ShapeError("gemv: x.len != model cols")
+        x = x.contiguous()
+        M = x.shape[0]
+        if out is None:
+            out = torch.empty(M, self.out_rows, dtype=torch.float32, device=x.device)
+        ws = workspace if workspace is not None else self.workspace(M, path)
+        check(lib().sfmp_gemm_ex(self._h, C.c_void_p(x.data_ptr()), _dtype_code(x), M,
+                                 C.c_void_p(out.data_ptr()),
+                                 C.c_void_p(ws.data_ptr()) if ws is not None else None,
+                                 ws.numel() if ws is not None else 0, path, _stream_ptr(stream)))
+        return out
+
+    def gemm_host(self, x: np.ndarray) -> np.ndarray:
+        """Reference calling convention: host f32 in, host f32 out (copies inside)."""
+        x = np.ascontiguousarray(np.atleast_2d(x), np.float32)
+        if x.shape[-1] != self.cols:
+            raise ShapeError("gemv: x.len != model cols")
+        y = np.empty((x.shape[0], self.out_rows), np.float32)
+        check(lib().sfmp_gemm_host(self._h, x.ctypes.data, x.shape[0], y.ctypes.data, None))
+        return y
+
+    def dequantize(self, stream=None):
+        import torch
+        w = torch.empty(self.out_rows, self.cols, dtype=torch.float32,
+                        device=f"cuda:{self.device}")
+        check(lib().sfmp_dequantize(self._h, C.c_void_p(w.data_ptr()), _stream_ptr(stream)))
+        return w
+
+    def unpack_codes(self, stream=None):
+        import torch
+        c = torch.empty(self.rows, self.cols, dtype=torch.uint8, device=f"cuda:{self.device}")
+        check(lib().sfmp_unpack_codes(self._h, C.c_void_p(c.data_ptr()), _stream_ptr(stream)))
+        return c
+
+    def unpermute_gathered(self, gathered, M: int, out=None, stream=None):
+        """[num_shards, M, shard_rows] all-gathered shard outputs -> y[M, rows] original order."""
+        import torch
+        if out is None:
+            out = torch.empty(M, self.info["global_rows"], dtype=torch.float32,
+                              device=gathered.device)
+        check(lib().sfmp_unpermute_gathered(self._h, C.c_void_p(gathered.data_ptr()), M,
+                                            C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+
+def gemv(model: DeviceModel, x, stream=None):
+    """sfmp::gemv (lutgemm.hpp:57): one token (or M tokens looped)."""
+    y = model.gemm(x, stream=stream)
+    return y[0] if x.dim() == 1 else y

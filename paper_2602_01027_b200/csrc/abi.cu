@@ -1,0 +1,673 @@
+// abi.cu -- the extern "C" boundary (include/sfmp_cuda.h): SFMPPKD1 ingest,
+// device model lifetime, kernel dispatch.  Host code only.
+//
+// Ingest restates deserialize (layout.cpp:210-279) + PackedModel::validate
+// (layout.cpp:88-124) + compute_block_offsets (layout.cpp:301-314) with the
+// same error kinds (errors.hpp:20-36).  Paths relative to /root/reference/proj.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/sfmp_cuda.h"
+#include "sfmp_internal.h"
+
+using sfmpk::DevModel;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sfmp_status fail(sfmp_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+sfmp_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(SFMP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define SFMP_CUDA_TRY(expr)                                 \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Host ingest of SFMPPKD1
+// ---------------------------------------------------------------------------
+struct Parsed {
+    uint64_t rows = 0, cols = 0;
+    uint32_t m_b = 0, n_b = 0;
+    int floor_bits = 0, ceil_bits = 0, mode = 0;
+    const uint32_t* row_perm = nullptr;  // unaligned pointers into the stream
+    const uint32_t* col_perm = nullptr;
+    uint64_t K = 0;
+    const uint8_t* bits = nullptr;
+    std::vector<uint64_t> off;  // absolute offsets
+    uint64_t payload_begin = 0, payload_end = 0;
+};
+
+template <class T>
+T rd(const uint8_t* p) {
+    T v;
+    std::memcpy(&v, p, sizeof(T));
+    return v;
+}
+
+sfmp_status check_perm(const uint8_t* p, uint64_t n, const char* what) {
+    std::vector<uint8_t> seen(n, 0);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t v = rd<uint32_t>(p + 4 * i);
+        if (v >= n || seen[v])
+            return fail(SFMP_ERR_FORMAT_INVARIANT,
+                        std::string(what) + ": permutation is not a bijection on 0..n-1");
+        seen[v] = 1;
+    }
+    return SFMP_OK;
+}
+
+sfmp_status parse(const uint8_t* b, size_t len, Parsed& m) {
+    if (!b && len) return fail(SFMP_ERR_INVALID_ARGUMENT, "null byte buffer");
+    size_t pos = 0;
+    auto need = [&](uint64_t n, const char* what) -> sfmp_status {
+        if (n > len - pos)
+            return fail(SFMP_ERR_FORMAT_TRUNCATED, std::string("truncated while reading ") + what);
+        return SFMP_OK;
+    };
+    sfmp_status s;
+    if ((s = need(8, "magic"))) return s;
+    if (std::memcmp(b, "SFMPPKD1", 8) != 0) return fail(SFMP_ERR_FORMAT_BAD_MAGIC, "not an SFMPPKD1 file");
+    pos = 8;
+    if ((s = need(2, "version"))) return s;
+    const uint16_t ver = rd<uint16_t>(b + pos);
+    pos += 2;
+    if (ver != 1)
+        return fail(SFMP_ERR_FORMAT_BAD_VERSION, "unsupported packed model version " + std::to_string(ver));
+    if ((s = need(28, "header"))) return s;
+    m.rows = rd<uint64_t>(b + pos);
+    m.cols = rd<uint64_t>(b + pos + 8);
+    m.m_b = rd<uint32_t>(b + pos + 16);
+    m.n_b = rd<uint32_t>(b + pos + 20);
+    m.floor_bits = b[pos + 24];
+    m.ceil_bits = b[pos + 25];
+    const uint8_t mode = b[pos + 26];
+    pos += 28;
+    if (mode > 3) return fail(SFMP_ERR_FORMAT_INVARIANT, "unknown reorder mode byte");
+    m.mode = mode;
+    if (m.rows < 1 || m.cols < 1 || m.m_b < 1 || m.n_b < 1 || m.rows % m.m_b || m.cols % m.n_b ||
+        m.n_b % 8)
+        return fail(SFMP_ERR_FORMAT_INVARIANT, "bad shape/block header fields");
+    if (mode & 1) {
+        if (m.rows > (len - pos) / 4) return fail(SFMP_ERR_FORMAT_TRUNCATED, "truncated while reading row permutation");
+        m.row_perm = reinterpret_cast<const uint32_t*>(b + pos);
+        if ((s = check_perm(b + pos, m.rows, "row permutation"))) return s;
+        pos += m.rows * 4;
+    }
+    if (mode & 2) {
+        if (m.cols > (len - pos) / 4) return fail(SFMP_ERR_FORMAT_TRUNCATED, "truncated while reading col permutation");
+        m.col_perm = reinterpret_cast<const uint32_t*>(b + pos);
+        if ((s = check_perm(b + pos, m.cols, "col permutation"))) return s;
+        pos += m.cols * 4;
+    }
+    if ((s = need(8, "block count"))) return s;
+    m.K = rd<uint64_t>(b + pos);
+    pos += 8;
+    if (m.K != (m.rows / m.m_b) * (m.cols / m.n_b))
+        return fail(SFMP_ERR_FORMAT_INVARIANT, "block count does not match shape/block dims");
+    if ((s = need(m.K, "block bit map"))) return s;
+    m.bits = b + pos;
+    pos += m.K;
+    m.payload_begin = pos;
+    m.off.resize(m.K);
+    const uint64_t plane = static_cast<uint64_t>(m.m_b) * m.n_b / 8;
+    for (uint64_t k = 0; k < m.K; ++k) {
+        m.off[k] = pos;
+        const uint64_t n = 4ull * m.m_b + static_cast<uint64_t>(m.bits[k]) * plane;
+        if (n > len - pos) return fail(SFMP_ERR_FORMAT_TRUNCATED, "truncated while reading block payload");
+        pos += n;
+    }
+    if (pos != len) return fail(SFMP_ERR_FORMAT_INVARIANT, "trailing bytes after model");
+    m.payload_end = pos;
+    if (m.floor_bits < 1 || m.ceil_bits < m.floor_bits || m.ceil_bits - m.floor_bits > 1 || m.ceil_bits > 8)
+        return fail(SFMP_ERR_FORMAT_INVARIANT, "packed model: bad candidate bit-widths");
+    for (uint64_t k = 0; k < m.K; ++k)
+        if (m.bits[k] != m.floor_bits && m.bits[k] != m.ceil_bits)
+            return fail(SFMP_ERR_FORMAT_INVARIANT, "packed model: block bit-width outside candidate set");
+    return SFMP_OK;
+}
+
+void fill_info(const Parsed& p, sfmp_model_info* info) {
+    std::memset(info, 0, sizeof(*info));
+    info->rows = p.rows;
+    info->cols = p.cols;
+    info->m_b = p.m_b;
+    info->n_b = p.n_b;
+    info->floor_bits = p.floor_bits;
+    info->ceil_bits = p.ceil_bits;
+    info->mode = p.mode;
+    info->block_count = p.K;
+    uint64_t sum = 0, high = 0;
+    for (uint64_t k = 0; k < p.K; ++k) {
+        sum += p.bits[k];
+        if (p.ceil_bits != p.floor_bits && p.bits[k] == p.ceil_bits) ++high;
+    }
+    info->blocks_high = high;
+    info->avg_code_bits = p.K ? static_cast<double>(sum) / p.K : 0.0;
+    info->payload_bytes = p.payload_end - p.payload_begin;
+    info->num_shards = 1;
+    info->out_rows = p.rows;
+    info->global_rows = p.rows;
+}
+
+template <class T>
+sfmp_status dev_upload(DevModel& d, T** dst, const void* src, size_t bytes) {
+    void* ptr = nullptr;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(&ptr, bytes);
+    if (e != cudaSuccess) return fail(SFMP_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    d.allocs.push_back(ptr);
+    d.device_bytes += bytes;
+    if (src) {
+        e = cudaMemcpy(ptr, src, bytes, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy H2D");
+    } else {
+        e = cudaMemset(ptr, 0, bytes);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
+    }
+    *dst = static_cast<T*>(ptr);
+    return SFMP_OK;
+}
+
+void free_model(DevModel* d) {
+    if (!d) return;
+    {
+        DeviceGuard g(d->device);
+        for (void* p : d->allocs) cudaFree(p);
+    }
+    delete d;
+}
+
+// Decode-GEMV schedule: balance units over CTAs by bytes.
+sfmp_status build_gemv_schedule(DevModel& d) {
+    d.gemv_ok = (d.m_b % 128 == 0) && (d.n_b % 128 == 0) && d.cols < (1ull << 31) &&
+                d.rows < (1ull << 31);
+    if (!d.gemv_ok) return SFMP_OK;
+    sfmpk::GemvSchedule& g = d.gemv;
+    g.tile_rows = 128;
+    g.row_tiles = static_cast<int>(d.rows / 128);
+    g.block_cols = static_cast<int>(d.cols / d.n_b);
+    const int RT = g.row_tiles, BC = g.block_cols;
+    const int64_t units = static_cast<int64_t>(RT) * BC;
+    const int tiles_per_brow = static_cast<int>(d.m_b / 128);
+    std::vector<double> prefix(units + 1, 0.0);
+    const double nb8 = d.n_b / 8.0;
+    for (int64_t u = 0; u < units; ++u) {
+        const int rt = static_cast<int>(u / BC), bc = static_cast<int>(u % BC);
+        const uint64_t k = static_cast<uint64_t>(rt / tiles_per_brow) * BC + bc;
+        prefix[u + 1] = prefix[u] + 512.0 + d.h_bits[k] * 128.0 * nb8 + 1024.0;
+    }
+    const int G = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(d.num_sms) * sfmpk::gemv_ctas_per_sm()));
+    g.grid = G;
+    std::vector<int> begin(G + 1, 0);
+    begin[G] = static_cast<int>(units);
+    int64_t u = 0;
+    for (int c = 1; c < G; ++c) {
+        const double target = prefix[units] * c / G;
+        while (u < units && prefix[u] < target) ++u;
+        int64_t lo = begin[c - 1] + 1, hi = units - (G - c);
+        begin[c] = static_cast<int>(std::min(std::max<int64_t>(u, lo), hi));
+        u = begin[c];
+    }
+    std::vector<int> owner(units);
+    for (int c = 0; c < G; ++c)
+        for (int v = begin[c]; v < begin[c + 1]; ++v) owner[v] = c;
+    std::vector<int> nseg(RT), slot(RT), first(RT);
+    int slots = 0;
+    for (int rt = 0; rt < RT; ++rt) {
+        const int f = owner[static_cast<int64_t>(rt) * BC], l = owner[static_cast<int64_t>(rt) * BC + BC - 1];
+        first[rt] = f;
+        nseg[rt] = l - f + 1;
+        slot[rt] = slots;
+        if (nseg[rt] > 1) slots += nseg[rt];
+    }
+    g.total_slots = slots;
+    sfmp_status s;
+    if ((s = dev_upload(d, &g.d_cta_begin, begin.data(), begin.size() * sizeof(int)))) return s;
+    if ((s = dev_upload(d, &g.d_rt_nseg, nseg.data(), nseg.size() * sizeof(int)))) return s;
+    if ((s = dev_upload(d, &g.d_rt_slot, slot.data(), slot.size() * sizeof(int)))) return s;
+    if ((s = dev_upload(d, &g.d_rt_first, first.data(), first.size() * sizeof(int)))) return s;
+    if ((s = dev_upload<unsigned>(d, &g.d_counters, nullptr, RT * sizeof(unsigned)))) return s;
+    return SFMP_OK;
+}
+
+// Build a device model from a parsed stream, restricted to `brows` block rows
+// (in the given order).  out_map: local reordered row -> column of y.
+sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
+                        const std::vector<uint64_t>& brows, const std::vector<uint32_t>& out_map,
+                        uint64_t out_rows, DevModel** out) {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(SFMP_ERR_CUDA, "no CUDA device available (no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(SFMP_ERR_INVALID_ARGUMENT, "bad device ordinal");
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (prop.major != 10)
+        return fail(SFMP_ERR_CUDA, "device is not sm_100 (B200); this build targets sm_100a only");
+    DeviceGuard guard(device);
+    std::unique_ptr<DevModel, void (*)(DevModel*)> d(new DevModel(), free_model);
+    d->device = device;
+    d->num_sms = prop.multiProcessorCount;
+    d->m_b = p.m_b;
+    d->n_b = p.n_b;
+    d->cols = p.cols;
+    d->floor_bits = p.floor_bits;
+    d->ceil_bits = p.ceil_bits;
+    d->mode = p.mode;
+    d->global_rows = p.rows;
+    const uint64_t BC = p.cols / p.n_b;
+    d->rows = brows.size() * p.m_b;
+    d->K = brows.size() * BC;
+    d->out_rows = out_rows;
+    // Gather the selected block rows (each a contiguous span) into one buffer.
+    std::vector<uint8_t> payload;
+    uint64_t total = 0;
+    for (uint64_t br : brows) {
+        const uint64_t a = p.off[br * BC], z = (br + 1) * BC < p.K ? p.off[(br + 1) * BC] : p.payload_end;
+        total += z - a;
+    }
+    payload.reserve(total);
+    d->h_bits.reserve(d->K);
+    d->h_off.reserve(d->K);
+    uint64_t sum = 0;
+    for (uint64_t br : brows) {
+        const uint64_t a = p.off[br * BC], z = (br + 1) * BC < p.K ? p.off[(br + 1) * BC] : p.payload_end;
+        for (uint64_t bc = 0; bc < BC; ++bc) {
+            d->h_off.push_back(payload.size() + (p.off[br * BC + bc] - a));
+            d->h_bits.push_back(p.bits[br * BC + bc]);
+            sum += p.bits[br * BC + bc];
+            if (p.ceil_bits != p.floor_bits && p.bits[br * BC + bc] == p.ceil_bits) ++d->blocks_high;
+        }
+        payload.insert(payload.end(), bytes + a, bytes + z);
+    }
+    d->avg_bits = d->K ? static_cast<double>(sum) / d->K : 0.0;
+    d->payload_bytes = payload.size();
+    sfmp_status s;
+    if ((s = dev_upload(*d, &d->d_payload, payload.data(), payload.size()))) return s;
+    if ((s = dev_upload(*d, &d->d_off, d->h_off.data(), d->h_off.size() * 8))) return s;
+    if ((s = dev_upload(*d, &d->d_bits, d->h_bits.data(), d->h_bits.size()))) return s;
+    std::vector<uint32_t> cp(p.cols);
+    if (p.col_perm) std::memcpy(cp.data(), p.col_perm, p.cols * 4);
+    else std::iota(cp.begin(), cp.end(), 0u);
+    if ((s = dev_upload(*d, &d->d_col_perm, cp.data(), cp.size() * 4))) return s;
+    if ((s = dev_upload(*d, &d->d_out_map, out_map.data(), out_map.size() * 4))) return s;
+    if ((s = build_gemv_schedule(*d))) return s;
+    d->gemm_ok = sfmpk::gemm_supported(*d);
+    const size_t ws = d->gemv_ok ? sfmpk::gemv_workspace_bytes(*d, 16) : 0;
+    if (ws) {
+        if ((s = dev_upload<float>(*d, &d->d_ws, nullptr, ws))) return s;
+        d->ws_bytes = ws;
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "upload sync");
+    *out = d.release();
+    return SFMP_OK;
+}
+
+std::vector<uint32_t> row_order(const Parsed& p) {
+    std::vector<uint32_t> r(p.rows);
+    if (p.row_perm) std::memcpy(r.data(), p.row_perm, p.rows * 4);
+    else std::iota(r.begin(), r.end(), 0u);
+    return r;
+}
+
+// Snake (boustrophedon) block-row owner.
+uint32_t snake_owner(uint64_t br, uint32_t G) {
+    const uint64_t round = br / G, pos = br % G;
+    return static_cast<uint32_t>((round & 1) ? G - 1 - pos : pos);
+}
+
+// Snake block-row partition + global gather map.
+sfmp_status shard_plan(const Parsed& p, uint32_t G, std::vector<std::vector<uint64_t>>& owned,
+                       std::vector<uint32_t>& gmap, uint64_t& SR) {
+    if (G < 1) return fail(SFMP_ERR_CONFIG, "num_shards must be >= 1");
+    const uint64_t GR = p.rows / p.m_b;
+    if (GR < G) return fail(SFMP_ERR_SHAPE, "fewer block rows than shards (repack with a smaller m_b)");
+    owned.assign(G, {});
+    for (uint64_t br = 0; br < GR; ++br) owned[snake_owner(br, G)].push_back(br);
+    size_t maxb = 0;
+    for (auto& v : owned) maxb = std::max(maxb, v.size());
+    SR = maxb * p.m_b;
+    const std::vector<uint32_t> rp = row_order(p);
+    gmap.assign(G * SR, 0xFFFFFFFFu);
+    for (uint32_t g = 0; g < G; ++g)
+        for (size_t i = 0; i < owned[g].size(); ++i)
+            for (uint32_t r = 0; r < p.m_b; ++r) gmap[g * SR + i * p.m_b + r] = rp[owned[g][i] * p.m_b + r];
+    return SFMP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sfmp_abi_version(void) { return SFMP_CUDA_ABI_VERSION; }
+
+const char* sfmp_status_string(sfmp_status s) {
+    switch (s) {
+        case SFMP_OK: return "ok";
+        case SFMP_ERR_SHAPE: return "shape";
+        case SFMP_ERR_CONFIG: return "config";
+        case SFMP_ERR_FORMAT_BAD_MAGIC: return "bad_magic";
+        case SFMP_ERR_FORMAT_BAD_VERSION: return "bad_version";
+        case SFMP_ERR_FORMAT_TRUNCATED: return "truncated";
+        case SFMP_ERR_FORMAT_INVARIANT: return "invariant";
+        case SFMP_ERR_FORMAT_IO: return "io";
+        case SFMP_ERR_CUDA: return "cuda";
+        case SFMP_ERR_NCCL: return "nccl";
+        case SFMP_ERR_INVALID_ARGUMENT: return "invalid_argument";
+        case SFMP_ERR_NOMEM: return "nomem";
+        case SFMP_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown";
+}
+
+const char* sfmp_last_error(void) { return g_last_error.c_str(); }
+
+int sfmp_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int ok = 0;
+    for (int i = 0; i < n; ++i) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10) ++ok;
+    }
+    return ok;
+}
+
+sfmp_status sfmp_parse_header(const uint8_t* bytes, size_t len, sfmp_model_info* info) {
+    if (!info) return fail(SFMP_ERR_INVALID_ARGUMENT, "null info");
+    Parsed p;
+    sfmp_status s = parse(bytes, len, p);
+    if (s) return s;
+    fill_info(p, info);
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_block_offsets(const uint8_t* bytes, size_t len, uint64_t* offsets, uint64_t count) {
+    if (!offsets && count) return fail(SFMP_ERR_INVALID_ARGUMENT, "null offsets");
+    Parsed p;
+    sfmp_status s = parse(bytes, len, p);
+    if (s) return s;
+    if (count != p.K) return fail(SFMP_ERR_SHAPE, "offset buffer length != block count");
+    std::memcpy(offsets, p.off.data(), p.K * 8);
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_model_create(const uint8_t* bytes, size_t len, int device, sfmp_dev_model** out) {
+    if (!out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    Parsed p;
+    sfmp_status s = parse(bytes, len, p);
+    if (s) return s;
+    std::vector<uint64_t> brows(p.rows / p.m_b);
+    std::iota(brows.begin(), brows.end(), 0ull);
+    DevModel* d = nullptr;
+    s = build_model(bytes, p, device, brows, row_order(p), p.rows, &d);
+    if (s) return s;
+    *out = reinterpret_cast<sfmp_dev_model*>(d);
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_model_create_from_parts(const sfmp_model_parts* pt, int device, sfmp_dev_model** out) {
+    if (!pt || !out || !pt->block_bits || !pt->scales || !pt->zeros || !pt->plane_ptrs)
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "null parts");
+    if (pt->m_b < 1 || pt->n_b < 1 || pt->rows % pt->m_b || pt->cols % pt->n_b || pt->n_b % 8 ||
+        pt->mode < 0 || pt->mode > 3)
+        return fail(SFMP_ERR_FORMAT_INVARIANT, "packed model: bad geometry");
+    if (((pt->mode & 1) && !pt->row_perm) || ((pt->mode & 2) && !pt->col_perm))
+        return fail(SFMP_ERR_FORMAT_INVARIANT, "packed model: permutation missing for mode");
+    // Serialise (layout.cpp:179-208) then ingest through the same validated path.
+    const uint64_t K = (pt->rows / pt->m_b) * (pt->cols / pt->n_b);
+    const uint64_t pb = static_cast<uint64_t>(pt->m_b) * pt->n_b / 8;
+    std::vector<uint8_t> b;
+    auto put = [&](const void* src, size_t n) {
+        const uint8_t* s = static_cast<const uint8_t*>(src);
+        b.insert(b.end(), s, s + n);
+    };
+    const uint16_t ver = 1;
+    const uint8_t hdr[4] = {static_cast<uint8_t>(pt->floor_bits), static_cast<uint8_t>(pt->ceil_bits),
+                            static_cast<uint8_t>(pt->mode), 0};
+    put("SFMPPKD1", 8);
+    put(&ver, 2);
+    put(&pt->rows, 8);
+    put(&pt->cols, 8);
+    put(&pt->m_b, 4);
+    put(&pt->n_b, 4);
+    put(hdr, 4);
+    if (pt->mode & 1) put(pt->row_perm, pt->rows * 4);
+    if (pt->mode & 2) put(pt->col_perm, pt->cols * 4);
+    put(&K, 8);
+    put(pt->block_bits, K);
+    uint64_t pi = 0;
+    for (uint64_t k = 0; k < K; ++k) {
+        if (!pt->scales[k] || !pt->zeros[k]) return fail(SFMP_ERR_INVALID_ARGUMENT, "null block scales/zeros");
+        put(pt->scales[k], pt->m_b * 2ull);
+        put(pt->zeros[k], pt->m_b * 2ull);
+        for (int i = 0; i < pt->block_bits[k]; ++i, ++pi) {
+            if (!pt->plane_ptrs[pi]) return fail(SFMP_ERR_INVALID_ARGUMENT, "null plane pointer");
+            put(pt->plane_ptrs[pi], pb);
+        }
+    }
+    return sfmp_model_create(b.data(), b.size(), device, out);
+}
+
+sfmp_status sfmp_shard_plan(const uint8_t* bytes, size_t len, uint32_t num_shards, uint32_t* gather_map,
+                            uint64_t* shard_rows) {
+    if (!shard_rows) return fail(SFMP_ERR_INVALID_ARGUMENT, "null shard_rows");
+    Parsed p;
+    sfmp_status s = parse(bytes, len, p);
+    if (s) return s;
+    std::vector<std::vector<uint64_t>> owned;
+    std::vector<uint32_t> gmap;
+    uint64_t SR = 0;
+    if ((s = shard_plan(p, num_shards, owned, gmap, SR))) return s;
+    *shard_rows = SR;
+    if (gather_map) std::memcpy(gather_map, gmap.data(), gmap.size() * 4);
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device, uint32_t shard,
+                                    uint32_t num_shards, sfmp_dev_model** out) {
+    if (!out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    if (num_shards < 1 || shard >= num_shards) return fail(SFMP_ERR_CONFIG, "bad shard index/count");
+    Parsed p;
+    sfmp_status s = parse(bytes, len, p);
+    if (s) return s;
+    std::vector<std::vector<uint64_t>> owned;
+    std::vector<uint32_t> gmap;
+    uint64_t SR = 0;
+    if ((s = shard_plan(p, num_shards, owned, gmap, SR))) return s;
+    std::vector<uint32_t> local(owned[shard].size() * p.m_b);
+    std::iota(local.begin(), local.end(), 0u);
+    DevModel* d = nullptr;
+    s = build_model(bytes, p, device, owned[shard], local, SR, &d);
+    if (s) return s;
+    d->shard = shard;
+    d->num_shards = num_shards;
+    d->shard_rows = SR;
+    {
+        DeviceGuard guard(device);
+        s = dev_upload(*d, &d->d_gather_map, gmap.data(), gmap.size() * 4);
+    }
+    if (s) {
+        free_model(d);
+        return s;
+    }
+    *out = reinterpret_cast<sfmp_dev_model*>(d);
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_model_destroy(sfmp_dev_model* model) {
+    free_model(reinterpret_cast<DevModel*>(model));
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_model_get_info(const sfmp_dev_model* model, sfmp_model_info* info) {
+    if (!model || !info) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    std::memset(info, 0, sizeof(*info));
+    info->rows = d.rows;
+    info->cols = d.cols;
+    info->m_b = d.m_b;
+    info->n_b = d.n_b;
+    info->floor_bits = d.floor_bits;
+    info->ceil_bits = d.ceil_bits;
+    info->mode = d.mode;
+    info->block_count = d.K;
+    info->blocks_high = d.blocks_high;
+    info->avg_code_bits = d.avg_bits;
+    info->payload_bytes = d.payload_bytes;
+    info->device_bytes = d.device_bytes;
+    info->shard = d.shard;
+    info->num_shards = d.num_shards;
+    info->out_rows = d.out_rows;
+    info->global_rows = d.global_rows;
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_workspace_size(const sfmp_dev_model* model, int64_t M, sfmp_path path, size_t* bytes) {
+    if (!model || !bytes) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    size_t b = 0;
+    const bool gemm = (path == SFMP_PATH_GEMM) || (path == SFMP_PATH_AUTO && M > 16 && d.gemm_ok);
+    if (gemm) b = sfmpk::gemm_workspace_bytes(d, M);
+    else if (path != SFMP_PATH_GENERIC && d.gemv_ok) b = sfmpk::gemv_workspace_bytes(d, 16);
+    *bytes = b;
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M,
+                         float* y, void* workspace, size_t workspace_bytes, sfmp_path path,
+                         void* stream) {
+    if (!model) return fail(SFMP_ERR_INVALID_ARGUMENT, "null model");
+    if (M < 0) return fail(SFMP_ERR_SHAPE, "negative M");
+    if (M == 0) return SFMP_OK;
+    if (!x || !y) return fail(SFMP_ERR_INVALID_ARGUMENT, "null x/y");
+    if (dtype != SFMP_F32 && dtype != SFMP_F16 && dtype != SFMP_BF16)
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "bad dtype");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    DeviceGuard guard(d.device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (path == SFMP_PATH_AUTO) path = (M > 16 && d.gemm_ok) ? SFMP_PATH_GEMM : (d.gemv_ok ? SFMP_PATH_GEMV : SFMP_PATH_GENERIC);
+    cudaError_t e = cudaSuccess;
+    const size_t esz = dtype == SFMP_F32 ? 4 : 2;
+    switch (path) {
+        case SFMP_PATH_GEMV: {
+            if (!d.gemv_ok) return fail(SFMP_ERR_UNSUPPORTED, "decode GEMV needs m_b%128==0 and n_b%128==0");
+            float* ws = static_cast<float*>(workspace);
+            const size_t need = sfmpk::gemv_workspace_bytes(d, 16);
+            if (!ws) ws = d.d_ws;
+            else if (workspace_bytes < need) return fail(SFMP_ERR_CONFIG, "workspace too small");
+            for (int64_t t0 = 0; t0 < M && e == cudaSuccess; t0 += 16) {
+                const int mt = static_cast<int>(std::min<int64_t>(16, M - t0));
+                e = sfmpk::launch_gemv(d, static_cast<const uint8_t*>(x) + t0 * d.cols * esz, dtype, mt,
+                                       y + t0 * d.out_rows, ws, st);
+            }
+            break;
+        }
+        case SFMP_PATH_GEMM: {
+            if (!d.gemm_ok) return fail(SFMP_ERR_UNSUPPORTED, "tcgen05 GEMM unsupported for this geometry");
+            const size_t need = sfmpk::gemm_workspace_bytes(d, M);
+            if (need && (!workspace || workspace_bytes < need))
+                return fail(SFMP_ERR_CONFIG, "GEMM path needs a workspace (sfmp_workspace_size)");
+            e = sfmpk::launch_gemm(d, x, dtype, M, y, workspace, st);
+            break;
+        }
+        case SFMP_PATH_GENERIC: e = sfmpk::launch_generic(d, x, dtype, M, y, st); break;
+        default: return fail(SFMP_ERR_INVALID_ARGUMENT, "bad path");
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_gemm(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M, float* y,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+    return sfmp_gemm_ex(model, x, dtype, M, y, workspace, workspace_bytes, SFMP_PATH_AUTO, stream);
+}
+
+sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M, float* y_host,
+                           void* stream) {
+    if (!model || (!x_host && M) || (!y_host && M)) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    if (M == 0) return SFMP_OK;
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    DeviceGuard guard(d.device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    float *dx = nullptr, *dy = nullptr;
+    void* ws = nullptr;
+    size_t wsb = 0;
+    sfmp_status s = sfmp_workspace_size(model, M, SFMP_PATH_AUTO, &wsb);
+    if (s) return s;
+    SFMP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dx), M * d.cols * 4, st));
+    SFMP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dy), M * d.out_rows * 4, st));
+    if (wsb) SFMP_CUDA_TRY(cudaMallocAsync(&ws, wsb, st));
+    SFMP_CUDA_TRY(cudaMemcpyAsync(dx, x_host, M * d.cols * 4, cudaMemcpyHostToDevice, st));
+    s = sfmp_gemm(model, dx, SFMP_F32, M, dy, ws, wsb, stream);
+    if (s == SFMP_OK)
+        SFMP_CUDA_TRY(cudaMemcpyAsync(y_host, dy, M * d.out_rows * 4, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(dx, st);
+    cudaFreeAsync(dy, st);
+    if (ws) cudaFreeAsync(ws, st);
+    SFMP_CUDA_TRY(cudaStreamSynchronize(st));
+    return s;
+}
+
+sfmp_status sfmp_dequantize(const sfmp_dev_model* model, float* w, void* stream) {
+    if (!model || !w) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    DeviceGuard guard(d.device);
+    cudaError_t e = sfmpk::launch_dequant(d, nullptr, w, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "dequant launch");
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_unpack_codes(const sfmp_dev_model* model, uint8_t* codes, void* stream) {
+    if (!model || !codes) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    DeviceGuard guard(d.device);
+    cudaError_t e = sfmpk::launch_unpack(d, codes, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "unpack launch");
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_unpermute_gathered(const sfmp_dev_model* model, const float* gathered, int64_t M, float* y,
+                                    void* stream) {
+    if (!model || (M && (!gathered || !y))) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    if (d.num_shards < 2 || !d.d_gather_map) return fail(SFMP_ERR_CONFIG, "model is not a shard");
+    DeviceGuard guard(d.device);
+    cudaError_t e = sfmpk::launch_unpermute_gathered(d, gathered, M, y, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "unpermute launch");
+    return SFMP_OK;
+}
+
+}  // extern "C"

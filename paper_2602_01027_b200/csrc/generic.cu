@@ -1,0 +1,186 @@
+// generic.cu -- geometry-agnostic kernels: the generic GEMM (any m_b, n_b, M),
+// K3 dequant/unpack (bit-exact parity entry points) and the sharded-output
+// un-permutation.  Paths relative to /root/reference/proj.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "sfmp_internal.h"
+
+namespace sfmpk {
+
+namespace {
+
+template <sfmp_dtype DT>
+__device__ __forceinline__ float ldx(const void* x, size_t i) {
+    if constexpr (DT == SFMP_F32) return __ldg(static_cast<const float*>(x) + i);
+    else if constexpr (DT == SFMP_F16)
+        return __half2float(__ldg(static_cast<const __half*>(x) + i));
+    else
+        return __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(x) + i));
+}
+
+__device__ __forceinline__ float fp16_at(const uint8_t* p) {
+    return __half2float(*reinterpret_cast<const __half*>(p));
+}
+
+// Code of weight (rr, j) of one block: unpack_block (layout.cpp:77-83).
+__device__ __forceinline__ uint32_t block_code(const uint8_t* planes, int bits, uint64_t plane_bytes,
+                                               uint32_t rb, uint32_t rr, uint32_t j) {
+    uint32_t c = 0;
+    for (int i = 0; i < bits; ++i)
+        c |= ((planes[i * plane_bytes + static_cast<uint64_t>(rr) * rb + (j >> 3)] >> (j & 7)) & 1u) << i;
+    return c;
+}
+
+struct GenParams {
+    const uint8_t* payload;
+    const uint64_t* off;
+    const uint8_t* bits;
+    const uint32_t* col_perm;
+    const uint32_t* out_map;
+    const void* x;
+    float* y;
+    int64_t M;
+    uint64_t rows, cols, out_rows;
+    uint32_t m_b, n_b, BC;
+};
+
+// One warp per reordered row, 8 tokens per pass; dequantised weight
+// s*c+z (quantizer.cpp:53) times the gathered activation, f32 accumulate.
+template <sfmp_dtype DT>
+__global__ void __launch_bounds__(256) generic_kernel(const GenParams p) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= p.rows) return;
+    const uint32_t br = static_cast<uint32_t>(r / p.m_b), rr = static_cast<uint32_t>(r % p.m_b);
+    const uint32_t rb = p.n_b >> 3;
+    const uint64_t pb = static_cast<uint64_t>(p.m_b) * rb;
+    for (int64_t t0 = 0; t0 < p.M; t0 += 8) {
+        float acc[8];
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) acc[tt] = 0.f;
+        for (uint32_t bc = 0; bc < p.BC; ++bc) {
+            const uint64_t k = static_cast<uint64_t>(br) * p.BC + bc;
+            const int bits = p.bits[k];
+            const uint8_t* blk = p.payload + p.off[k];
+            const float s = fp16_at(blk + 2 * rr), z = fp16_at(blk + 2ull * p.m_b + 2 * rr);
+            const uint8_t* planes = blk + 4ull * p.m_b;
+            for (uint32_t j = lane; j < p.n_b; j += 32) {
+                const uint32_t c = block_code(planes, bits, pb, rb, rr, j);
+                const float w = __fadd_rn(__fmul_rn(s, static_cast<float>(c)), z);
+                const uint32_t col = p.col_perm[static_cast<uint64_t>(bc) * p.n_b + j];
+#pragma unroll
+                for (int tt = 0; tt < 8; ++tt)
+                    if (t0 + tt < p.M) acc[tt] += w * ldx<DT>(p.x, (t0 + tt) * p.cols + col);
+            }
+        }
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+            float v = acc[tt];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && t0 + tt < p.M) p.y[(t0 + tt) * p.out_rows + p.out_map[r]] = v;
+        }
+    }
+}
+
+// K3: dequantize_model (layout.cpp:316-332): w[orig_row][orig_col] = s*c + z
+// with the reference's two f32 roundings (no FMA contraction).
+__global__ void dequant_kernel(GenParams p, float* w) {
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= p.rows * p.cols) return;
+    const uint64_t r = idx / p.cols, j = idx % p.cols;
+    const uint32_t br = static_cast<uint32_t>(r / p.m_b), rr = static_cast<uint32_t>(r % p.m_b);
+    const uint32_t bc = static_cast<uint32_t>(j / p.n_b), jj = static_cast<uint32_t>(j % p.n_b);
+    const uint64_t k = static_cast<uint64_t>(br) * p.BC + bc;
+    const uint8_t* blk = p.payload + p.off[k];
+    const uint32_t rb = p.n_b >> 3;
+    const uint32_t c = block_code(blk + 4ull * p.m_b, p.bits[k], static_cast<uint64_t>(p.m_b) * rb, rb, rr, jj);
+    const float s = fp16_at(blk + 2 * rr), z = fp16_at(blk + 2ull * p.m_b + 2 * rr);
+    w[static_cast<uint64_t>(p.out_map[r]) * p.cols + p.col_perm[j]] =
+        __fadd_rn(__fmul_rn(s, static_cast<float>(c)), z);
+}
+
+__global__ void unpack_kernel(GenParams p, uint8_t* codes) {
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= p.rows * p.cols) return;
+    const uint64_t r = idx / p.cols, j = idx % p.cols;
+    const uint32_t br = static_cast<uint32_t>(r / p.m_b), rr = static_cast<uint32_t>(r % p.m_b);
+    const uint32_t bc = static_cast<uint32_t>(j / p.n_b), jj = static_cast<uint32_t>(j % p.n_b);
+    const uint64_t k = static_cast<uint64_t>(br) * p.BC + bc;
+    const uint8_t* blk = p.payload + p.off[k];
+    const uint32_t rb = p.n_b >> 3;
+    codes[idx] = static_cast<uint8_t>(
+        block_code(blk + 4ull * p.m_b, p.bits[k], static_cast<uint64_t>(p.m_b) * rb, rb, rr, jj));
+}
+
+// gathered[g][t][i] -> y[t][gather_map[g*SR+i]] (padding rows map to ~0u).
+__global__ void unpermute_kernel(const float* gathered, const uint32_t* gmap, float* y, int64_t M,
+                                 uint32_t G, uint64_t SR, uint64_t rows) {
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t total = static_cast<uint64_t>(G) * M * SR;
+    if (idx >= total) return;
+    const uint64_t i = idx % SR;
+    const uint64_t t = (idx / SR) % M;
+    const uint64_t g = idx / (SR * M);
+    const uint32_t dst = gmap[g * SR + i];
+    if (dst != 0xFFFFFFFFu) y[t * rows + dst] = gathered[idx];
+}
+
+GenParams make_params(const DevModel& m) {
+    GenParams p{};
+    p.payload = m.d_payload;
+    p.off = m.d_off;
+    p.bits = m.d_bits;
+    p.col_perm = m.d_col_perm;
+    p.out_map = m.d_out_map;
+    p.rows = m.rows;
+    p.cols = m.cols;
+    p.out_rows = m.out_rows;
+    p.m_b = m.m_b;
+    p.n_b = m.n_b;
+    p.BC = static_cast<uint32_t>(m.cols / m.n_b);
+    return p;
+}
+
+}  // namespace
+
+cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
+                           cudaStream_t st) {
+    GenParams p = make_params(m);
+    p.x = x;
+    p.y = y;
+    p.M = M;
+    const unsigned grid = static_cast<unsigned>((m.rows + 7) / 8);
+    switch (dt) {
+        case SFMP_F32: generic_kernel<SFMP_F32><<<grid, 256, 0, st>>>(p); break;
+        case SFMP_F16: generic_kernel<SFMP_F16><<<grid, 256, 0, st>>>(p); break;
+        default: generic_kernel<SFMP_BF16><<<grid, 256, 0, st>>>(p); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dequant(const DevModel& m, const uint32_t*, float* w, cudaStream_t st) {
+    GenParams p = make_params(m);
+    const uint64_t n = m.rows * m.cols;
+    dequant_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, w);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const DevModel& m, uint8_t* codes, cudaStream_t st) {
+    GenParams p = make_params(m);
+    const uint64_t n = m.rows * m.cols;
+    unpack_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, codes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, int64_t M, float* y,
+                                      cudaStream_t st) {
+    const uint64_t total = static_cast<uint64_t>(m.num_shards) * M * m.shard_rows;
+    if (total == 0) return cudaSuccess;
+    unpermute_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+        gathered, m.d_gather_map, y, M, m.num_shards, m.shard_rows, m.global_rows);
+    return cudaGetLastError();
+}
+
+}  // namespace sfmpk
