@@ -142,7 +142,9 @@ sfmp_status sfmp_model_destroy(sfmp_dev_model* model);
 sfmp_status sfmp_model_get_info(const sfmp_dev_model* model, sfmp_model_info* info);
 
 /* ---- compute (device pointers, stream-ordered) ------------------------- */
-/* Bytes of scratch sfmp_gemm needs for this M (0 if none). */
+/* Bytes of scratch sfmp_gemm needs for this M (0 if none).  A workspace must
+ * be zero-filled once before its first use; every call leaves it re-zeroed
+ * (it holds the grid-wide completion counters of the decode GEMV). */
 sfmp_status sfmp_workspace_size(const sfmp_dev_model* model, int64_t M, sfmp_path path,
                                 size_t* bytes);
 /* y[M][out_rows] (f32) = x[M][cols] (dtype) . W^T.  workspace may be NULL

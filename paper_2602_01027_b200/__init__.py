@@ -238,7 +238,7 @@ class DeviceModel:
         nbytes = self.workspace_bytes(M, path)
         key = (path, nbytes)
         if nbytes and key not in self._ws:
-            self._ws[key] = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._ws[key] = torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
         return self._ws.get(key)
 
     def gemm(self, x, out=None, path: int = PATH_AUTO, workspace=None, stream=None):

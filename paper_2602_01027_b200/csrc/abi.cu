@@ -200,65 +200,22 @@ void free_model(DevModel* d) {
     {
         DeviceGuard g(d->device);
         for (void* p : d->allocs) cudaFree(p);
+        if (d->d_host_stage) cudaFree(d->d_host_stage);
     }
     delete d;
 }
 
-// Decode-GEMV schedule: balance units over CTAs by bytes.
+// The decode GEMV (K1) needs 128-row units and n_b in {128, 256}; its cluster
+// split is chosen per launch (gemv_tc.cu).
 sfmp_status build_gemv_schedule(DevModel& d) {
-    d.gemv_ok = (d.m_b % 128 == 0) && (d.n_b % 128 == 0) && d.cols < (1ull << 31) &&
-                d.rows < (1ull << 31);
-    if (!d.gemv_ok) return SFMP_OK;
-    sfmpk::GemvSchedule& g = d.gemv;
-    g.tile_rows = 128;
-    g.row_tiles = static_cast<int>(d.rows / 128);
-    g.block_cols = static_cast<int>(d.cols / d.n_b);
-    const int RT = g.row_tiles, BC = g.block_cols;
-    const int64_t units = static_cast<int64_t>(RT) * BC;
-    const int tiles_per_brow = static_cast<int>(d.m_b / 128);
-    std::vector<double> prefix(units + 1, 0.0);
-    const double nb8 = d.n_b / 8.0;
-    for (int64_t u = 0; u < units; ++u) {
-        const int rt = static_cast<int>(u / BC), bc = static_cast<int>(u % BC);
-        const uint64_t k = static_cast<uint64_t>(rt / tiles_per_brow) * BC + bc;
-        prefix[u + 1] = prefix[u] + 512.0 + d.h_bits[k] * 128.0 * nb8 + 1024.0;
-    }
-    const int G = static_cast<int>(std::min<int64_t>(units, static_cast<int64_t>(d.num_sms) * sfmpk::gemv_ctas_per_sm()));
-    g.grid = G;
-    std::vector<int> begin(G + 1, 0);
-    begin[G] = static_cast<int>(units);
-    int64_t u = 0;
-    for (int c = 1; c < G; ++c) {
-        const double target = prefix[units] * c / G;
-        while (u < units && prefix[u] < target) ++u;
-        int64_t lo = begin[c - 1] + 1, hi = units - (G - c);
-        begin[c] = static_cast<int>(std::min(std::max<int64_t>(u, lo), hi));
-        u = begin[c];
-    }
-    std::vector<int> owner(units);
-    for (int c = 0; c < G; ++c)
-        for (int v = begin[c]; v < begin[c + 1]; ++v) owner[v] = c;
-    std::vector<int> nseg(RT), slot(RT), first(RT);
-    int slots = 0;
-    for (int rt = 0; rt < RT; ++rt) {
-        const int f = owner[static_cast<int64_t>(rt) * BC], l = owner[static_cast<int64_t>(rt) * BC + BC - 1];
-        first[rt] = f;
-        nseg[rt] = l - f + 1;
-        slot[rt] = slots;
-        if (nseg[rt] > 1) slots += nseg[rt];
-    }
-    g.total_slots = slots;
-    sfmp_status s;
-    if ((s = dev_upload(d, &g.d_cta_begin, begin.data(), begin.size() * sizeof(int)))) return s;
-    if ((s = dev_upload(d, &g.d_rt_nseg, nseg.data(), nseg.size() * sizeof(int)))) return s;
-    if ((s = dev_upload(d, &g.d_rt_slot, slot.data(), slot.size() * sizeof(int)))) return s;
-    if ((s = dev_upload(d, &g.d_rt_first, first.data(), first.size() * sizeof(int)))) return s;
-    if ((s = dev_upload<unsigned>(d, &g.d_counters, nullptr, RT * sizeof(unsigned)))) return s;
+    d.gemv_ok = d.TR == 128 && (d.n_b == 128 || d.n_b == 256) && d.cols < (1ull << 31) &&
+                d.rows < (1ull << 31) && d.payload_bytes < (1ull << 48);
     return SFMP_OK;
 }
 
 // Build a device model from a parsed stream, restricted to `brows` block rows
-// (in the given order).  out_map: local reordered row -> column of y.
+// (in the given order), repacked unit-major (sfmp_internal.h).  out_map:
+// local reordered row -> column of y.
 sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
                         const std::vector<uint64_t>& brows, const std::vector<uint32_t>& out_map,
                         uint64_t out_rows, DevModel** out) {
@@ -286,33 +243,45 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
     d->rows = brows.size() * p.m_b;
     d->K = brows.size() * BC;
     d->out_rows = out_rows;
-    // Gather the selected block rows (each a contiguous span) into one buffer.
+    d->TR = (p.m_b % 128 == 0) ? 128 : p.m_b;
+    d->BC = static_cast<uint32_t>(BC);
+    d->RT = static_cast<uint32_t>(d->rows / d->TR);
+    const uint32_t TR = d->TR, tiles = p.m_b / TR;
+    const uint64_t rb = p.n_b / 8, pb_blk = static_cast<uint64_t>(p.m_b) * rb, pb_unit = TR * rb;
+    // unit-major repack: for each block row, each TR-row tile, each block column
     std::vector<uint8_t> payload;
-    uint64_t total = 0;
+    uint64_t total = 0, sum = 0;
+    for (uint64_t br : brows)
+        for (uint64_t bc = 0; bc < BC; ++bc) total += 4ull * p.m_b + p.bits[br * BC + bc] * pb_blk;
+    payload.resize(total);
+    d->h_unit_desc.reserve(static_cast<size_t>(d->RT) * BC);
+    uint64_t pos = 0;
     for (uint64_t br : brows) {
-        const uint64_t a = p.off[br * BC], z = (br + 1) * BC < p.K ? p.off[(br + 1) * BC] : p.payload_end;
-        total += z - a;
-    }
-    payload.reserve(total);
-    d->h_bits.reserve(d->K);
-    d->h_off.reserve(d->K);
-    uint64_t sum = 0;
-    for (uint64_t br : brows) {
-        const uint64_t a = p.off[br * BC], z = (br + 1) * BC < p.K ? p.off[(br + 1) * BC] : p.payload_end;
         for (uint64_t bc = 0; bc < BC; ++bc) {
-            d->h_off.push_back(payload.size() + (p.off[br * BC + bc] - a));
-            d->h_bits.push_back(p.bits[br * BC + bc]);
             sum += p.bits[br * BC + bc];
             if (p.ceil_bits != p.floor_bits && p.bits[br * BC + bc] == p.ceil_bits) ++d->blocks_high;
         }
-        payload.insert(payload.end(), bytes + a, bytes + z);
+        for (uint32_t t = 0; t < tiles; ++t)
+            for (uint64_t bc = 0; bc < BC; ++bc) {
+                const uint64_t k = br * BC + bc;
+                const uint8_t* blk = bytes + p.off[k];
+                const int bits = p.bits[k];
+                const uint64_t ro = static_cast<uint64_t>(t) * TR;
+                d->h_unit_desc.push_back(pos | (static_cast<uint64_t>(bits) << 48));
+                std::memcpy(&payload[pos], blk + 2 * ro, 2ull * TR);                    // scales
+                std::memcpy(&payload[pos + 2ull * TR], blk + 2ull * p.m_b + 2 * ro, 2ull * TR);  // zeros
+                pos += 4ull * TR;
+                for (int i = 0; i < bits; ++i) {
+                    std::memcpy(&payload[pos], blk + 4ull * p.m_b + i * pb_blk + ro * rb, pb_unit);
+                    pos += pb_unit;
+                }
+            }
     }
     d->avg_bits = d->K ? static_cast<double>(sum) / d->K : 0.0;
     d->payload_bytes = payload.size();
     sfmp_status s;
     if ((s = dev_upload(*d, &d->d_payload, payload.data(), payload.size()))) return s;
-    if ((s = dev_upload(*d, &d->d_off, d->h_off.data(), d->h_off.size() * 8))) return s;
-    if ((s = dev_upload(*d, &d->d_bits, d->h_bits.data(), d->h_bits.size()))) return s;
+    if ((s = dev_upload(*d, &d->d_unit_desc, d->h_unit_desc.data(), d->h_unit_desc.size() * 8))) return s;
     std::vector<uint32_t> cp(p.cols);
     if (p.col_perm) std::memcpy(cp.data(), p.col_perm, p.cols * 4);
     else std::iota(cp.begin(), cp.end(), 0u);
@@ -583,7 +552,7 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
     const size_t esz = dtype == SFMP_F32 ? 4 : 2;
     switch (path) {
         case SFMP_PATH_GEMV: {
-            if (!d.gemv_ok) return fail(SFMP_ERR_UNSUPPORTED, "decode GEMV needs m_b%128==0 and n_b%128==0");
+            if (!d.gemv_ok) return fail(SFMP_ERR_UNSUPPORTED, "decode GEMV needs m_b%128==0 and n_b in {128,256}");
             float* ws = static_cast<float*>(workspace);
             const size_t need = sfmpk::gemv_workspace_bytes(d, 16);
             if (!ws) ws = d.d_ws;
@@ -619,33 +588,39 @@ sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int
                            void* stream) {
     if (!model || (!x_host && M) || (!y_host && M)) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
     if (M == 0) return SFMP_OK;
-    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    DevModel& d = *const_cast<DevModel*>(reinterpret_cast<const DevModel*>(model));
+    std::lock_guard<std::mutex> lock(d.host_mu);  // the staging buffers are per model
     DeviceGuard guard(d.device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    float *dx = nullptr, *dy = nullptr;
-    void* ws = nullptr;
     size_t wsb = 0;
     sfmp_status s = sfmp_workspace_size(model, M, SFMP_PATH_AUTO, &wsb);
     if (s) return s;
-    SFMP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dx), M * d.cols * 4, st));
-    SFMP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dy), M * d.out_rows * 4, st));
-    if (wsb) SFMP_CUDA_TRY(cudaMallocAsync(&ws, wsb, st));
+    const size_t xb = (M * d.cols * 4 + 255) / 256 * 256, yb = (M * d.out_rows * 4 + 255) / 256 * 256;
+    const size_t need = xb + yb + wsb;
+    if (need > d.host_stage_bytes) {
+        if (d.d_host_stage) cudaFree(d.d_host_stage);
+        d.d_host_stage = nullptr;
+        d.host_stage_bytes = 0;
+        SFMP_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&d.d_host_stage), need));
+        SFMP_CUDA_TRY(cudaMemset(d.d_host_stage, 0, need));  // workspaces start zeroed
+        d.host_stage_bytes = need;
+    }
+    float* dx = reinterpret_cast<float*>(d.d_host_stage);
+    float* dy = reinterpret_cast<float*>(d.d_host_stage + xb);
+    void* ws = wsb ? d.d_host_stage + xb + yb : nullptr;
     SFMP_CUDA_TRY(cudaMemcpyAsync(dx, x_host, M * d.cols * 4, cudaMemcpyHostToDevice, st));
     s = sfmp_gemm(model, dx, SFMP_F32, M, dy, ws, wsb, stream);
-    if (s == SFMP_OK)
-        SFMP_CUDA_TRY(cudaMemcpyAsync(y_host, dy, M * d.out_rows * 4, cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(dx, st);
-    cudaFreeAsync(dy, st);
-    if (ws) cudaFreeAsync(ws, st);
+    if (s) return s;
+    SFMP_CUDA_TRY(cudaMemcpyAsync(y_host, dy, M * d.out_rows * 4, cudaMemcpyDeviceToHost, st));
     SFMP_CUDA_TRY(cudaStreamSynchronize(st));
-    return s;
+    return SFMP_OK;
 }
 
 sfmp_status sfmp_dequantize(const sfmp_dev_model* model, float* w, void* stream) {
     if (!model || !w) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
     const DevModel& d = *reinterpret_cast<const DevModel*>(model);
     DeviceGuard guard(d.device);
-    cudaError_t e = sfmpk::launch_dequant(d, nullptr, w, static_cast<cudaStream_t>(stream));
+    cudaError_t e = sfmpk::launch_dequant(d, w, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "dequant launch");
     return SFMP_OK;
 }

@@ -6,34 +6,35 @@
 // /root/reference/proj.
 //
 // HBM-bound design:
-//  * Work unit = 128 reordered rows x one block column (n_b columns).  The
-//    unit's bytes are 2+bits contiguous spans of the SFMPPKD1 block (scales,
-//    zeros, one span per bit-plane), streamed by 1-D bulk async copies
-//    (cp.async.bulk, the TMA engine) into a deep shared-memory ring guarded
-//    by mbarriers.  One persistent CTA per SM walks a contiguous range of
-//    units (row-tile-major), balanced by bytes.
-//  * The activation gather x[t][col_perm[.]] (reorder-in) runs once per call
-//    in a tiny pre-pass (xprep_kernel) that writes, per block column, the f16
-//    MMA B fragments plus per-token column sums; the GEMV is launched with
-//    programmatic dependent launch, so its producer streams weights while the
-//    pre-pass runs and bulk-copies each unit's 2-4 KB fragment record next to
-//    the unit's weights.
-//  * Warp roles: 1 producer warp (bulk copies), 8 compute warps (16 rows
-//    each); 2 CTAs per SM.
+//  * Work unit = 128 reordered rows x one block column, stored unit-major in
+//    HBM (sfmp_internal.h), so a unit is one contiguous span fetched by ONE
+//    1-D bulk async copy (cp.async.bulk on the TMA engine) into a small
+//    mbarrier ring.
+//  * Each 128-row tile is processed by one thread-block cluster of C CTAs;
+//    rank r streams block columns [r*BC/C, (r+1)*BC/C).  The partial sums of
+//    the C ranks meet in distributed shared memory: every rank pushes its
+//    partials to the rank that owns the rows, one cluster barrier, the owner
+//    sums the C slots in rank order and stores un-permuted (deterministic
+//    split-K, no global round trips, no atomics).
+//  * The activation gather x[t][col_perm[.]] runs once per call in a small
+//    pre-pass (xprep_kernel) that writes, per block column, an "activation
+//    record": f16 MMA B fragments + per-token column sums.  The GEMV is a
+//    programmatic dependent of it: its producer streams weights while xprep
+//    runs and waits (griddepcontrol.wait) only before copying the records.
 //  * Compute: the bit-planes of a row's 32-weight word are transposed into
-//    nibble codes with 4 delta-swaps, converted to exact f16 integers with the
-//    0x6400 magic, and contracted against the activations on the tensor pipe
-//    (mma.m16n8k16, tokens = N).  The per-row affine (s, z) of each block is
-//    applied in f32 after the block column: y += s*sum(c*x) + z*sum(x), which
-//    equals sum((s*c+z)*x) up to f32 rounding.  The K permutation inside a
-//    128-column chunk that the unpack produces is absorbed by the gather.
-//  * Deterministic split-K: a row tile spread over several CTAs is reduced by
-//    the last arriving CTA in fixed segment order; the row un-permutation is
-//    fused into the final store.
+//    nibble codes with 4 delta-swaps, and each nibble pair becomes one f16x2
+//    by a single LOP3 against a magic exponent (1024+c or 64+c).  The magic
+//    offsets are a per-token constant folded in f32 after the MMA (bias term
+//    from the record), so the tensor pipe (mma.m16n8k16, tokens = N)
+//    contracts exact integer codes against f16 activations.  The per-row
+//    affine (s, z) of each block is applied in f32 after the block column:
+//    y += s*(C - bias) + z*sum(x) == sum((s*c+z)*x) up to f32 rounding.  The
+//    K permutation inside each 128-column chunk is absorbed by the record.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ptx.cuh"
 #include "sfmp_internal.h"
@@ -43,34 +44,71 @@ namespace sfmpk {
 namespace {
 
 constexpr int kTR = 128;  // rows per unit
-constexpr int kNCW = 8;   // compute warps (16 rows each)
+constexpr int kNCW = 4;   // compute warps (32 rows = 2 m16 tiles each)
 constexpr int kThreads = 32 * (1 + kNCW);
-constexpr int kFirstCompute = 32;
-constexpr int kCtasPerSm = 2;
-constexpr int kSmemPerCta = 113 * 1024;
+constexpr int kHdrBytes = 1280;  // barriers | zeros | stage bit-widths | out_map
+// resident CTAs per SM: 4 for M<=8 (NT=1), 3 for M<=16 (NT=2, more registers)
+__host__ __device__ constexpr int ctas_per_sm(int NT) { return NT == 1 ? 4 : 3; }
+__host__ __device__ constexpr int smem_per_cta(int NT) { return NT == 1 ? 56 * 1024 : 75 * 1024; }
 
 struct Params {
     const uint8_t* payload;
-    const uint64_t* off;
-    const uint8_t* bits;
+    const uint64_t* unit_desc;  // [RT*BC] row-tile-major
     const uint32_t* out_map;
-    const uint8_t* xfrag;  // [BC] records of stage_x bytes (written by xprep_kernel)
+    const uint8_t* xrec;  // [BC] activation records of rec_bytes (xprep_kernel)
     float* y;
-    float* ws;
-    const int* cta_begin;
-    const int* rt_nseg;
-    const int* rt_slot;
-    const int* rt_first;
-    unsigned* counters;
     int M;
     int BC;
-    int m_b;
+    int C;  // CTAs per row tile (= cluster size)
     int n_b;
     uint64_t out_rows;
     int stages;
-    uint32_t stage_w;  // bytes per weight stage (smem)
-    uint32_t stage_x;  // bytes per activation record (smem and global)
+    uint32_t stage_w;    // bytes per weight stage (smem)
+    uint32_t rec_bytes;  // bytes per activation record (smem and global)
+    int debug_mode;      // 0 normal; 5 timeline stamps
 };
+
+// Activation record of one block column (n_b columns), for M tokens:
+//   for chunk c (128 columns), n-tile nt (8 tokens), token n < Mnt, k-step s:
+//     4 lanes x 8 B of f16 B fragments  (tokens >= M omitted)
+//   then Xg[16] (f32 column sums) and bias[16] (f32 magic offsets).
+// Within a (c, nt, n) run the 8 k-steps are contiguous (stride 32 B), so a
+// lane's fragment addresses are compile-time offsets from one base.
+struct RecGeom {
+    int M;
+    __host__ __device__ int mnt(int nt) const { return nt == 0 ? (M < 8 ? M : 8) : M - 8; }
+    __host__ __device__ int nt_count() const { return M > 8 ? 2 : 1; }
+    __host__ __device__ int chunk_bytes() const { return 256 * M; }  // all n-tiles
+    __host__ __device__ int lane_off(int c, int nt, int n, int q) const {
+        return c * chunk_bytes() + nt * 2048 + n * 256 + q * 8;
+    }
+    __host__ __device__ int frag_off(int c, int nt, int s, int n, int q) const {
+        return lane_off(c, nt, n, q) + s * 32;
+    }
+    __host__ __device__ int xg_off(int CH) const { return CH * chunk_bytes(); }
+    __host__ __device__ int bytes(int CH) const { return (xg_off(CH) + 128 + 127) / 128 * 128; }
+};
+
+// Debug timeline (SFMP_GEMV_DEBUG=5): [cta][slot] globaltimer stamps for the
+// first kDbgCtas CTAs: slot 0 start, 1 end, 2+3i producer issue of unit i,
+// 3+3i full observed by compute warp 0, 4+3i unit done; row kDbgCtas-1 slots
+// 100.. hold kernel-level stamps.
+constexpr int kDbgCtas = 512, kDbgSlots = 128;
+__device__ unsigned long long g_dbg_timeline[kDbgCtas * kDbgSlots];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DBG_STAMP(slot)                                                                       \
+    do {                                                                                      \
+        if (dbg == 5 && blockIdx.x < kDbgCtas - 1 && (slot) < kDbgSlots)                      \
+            g_dbg_timeline[blockIdx.x * kDbgSlots + (slot)] = gtimer();                       \
+    } while (0)
+#define DBG_KSTAMP(slot)                                                                      \
+    do {                                                                                      \
+        if (dbg == 5) g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + (slot)] = gtimer();         \
+    } while (0)
 
 template <sfmp_dtype DT>
 __device__ __forceinline__ float load_x(const void* x, size_t i) {
@@ -83,21 +121,25 @@ __device__ __forceinline__ float load_x(const void* x, size_t i) {
 
 // K4 (decode flavour): gather x[t][col_perm[.]] once per call into per-block-
 // column records laid out exactly as the MMA B fragments the GEMV consumes,
-// plus the per-token column sums X_g used by the zero-point term
-// (lutgemm.cpp:113-115).  One warp per (block column, n-tile); lane (n,q)
-// owns token nt*8+n and k-slots 32q + 4h + a (+16).
-template <int NT, sfmp_dtype DT>
-__global__ void __launch_bounds__(256) xprep_kernel(const void* x, const uint32_t* col_perm, uint8_t* xfrag,
-                                                    int M, int cols, int n_b, int BC, uint32_t rec_bytes) {
+// plus per-token column sums X_g (lutgemm.cpp:113-115) and the magic-offset
+// bias.  One warp per (block column, n-tile); lane (n,q) owns token nt*8+n
+// and k-slots 32q + 4h + a (+16) of each 128-column chunk.
+template <sfmp_dtype DT>
+__global__ void __launch_bounds__(256) xprep_kernel(const void* x, const uint32_t* col_perm, uint8_t* xrec,
+                                                    int M, int cols, int n_b, int BC, uint32_t rec_bytes, int dbg) {
     pdl_launch_dependents();  // let the GEMV start streaming weights right away
+    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_KSTAMP(100);
+    const RecGeom G{M};
+    const int NT = G.nt_count();
     const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (w >= BC * NT) return;
     const int bc = w / NT, nt = w - bc * NT;
     const int lane = threadIdx.x & 31, q = lane & 3, n = lane >> 2;
     const int CH = n_b >> 7;
     const int t = nt * 8 + n;
-    uint8_t* rec = xfrag + static_cast<size_t>(bc) * rec_bytes;
-    float xs = 0.f;
+    const bool live = n < G.mnt(nt);
+    uint8_t* rec = xrec + static_cast<size_t>(bc) * rec_bytes;
+    float xs = 0.f, bias = 0.f;
     for (int c = 0; c < CH; ++c) {
         const uint4 idx4 = __ldg(reinterpret_cast<const uint4*>(col_perm + bc * n_b + c * 128) + lane);
         uint32_t gi[32];
@@ -113,98 +155,105 @@ __global__ void __launch_bounds__(256) xprep_kernel(const void* x, const uint32_
                     gi[s8 * 4 + j * 2 + e] = __shfl_sync(0xffffffffu, comp, 8 * q + (wk >> 2));
                 }
         }
-        float v[32];
-        if (t < M) {
+        if (live) {
             const size_t rowoff = static_cast<size_t>(t) * cols;
+            float v[32];
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = load_x<DT>(x, rowoff + gi[e]);
-        } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = 0.f;
+            for (int s8 = 0; s8 < 8; ++s8) {
+                uint2 st;
+                st.x = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 0], v[s8 * 4 + 1]));
+                st.y = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 2], v[s8 * 4 + 3]));
+                *reinterpret_cast<uint2*>(rec + G.frag_off(c, nt, s8, n, q)) = st;
+                // slot j=0 holds nibble pairs h even (magic 1024), j=1 h odd (magic 64);
+                // the bias uses the f16-rounded values the MMA sees.
+                bias += 1024.f * (__low2float(u32_as_h2(st.x)) + __high2float(u32_as_h2(st.x))) +
+                        64.f * (__low2float(u32_as_h2(st.y)) + __high2float(u32_as_h2(st.y)));
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) xs += v[e];
         }
-#pragma unroll
-        for (int s8 = 0; s8 < 8; ++s8) {
-            uint2 st;
-            st.x = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 0], v[s8 * 4 + 1]));
-            st.y = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 2], v[s8 * 4 + 3]));
-            *reinterpret_cast<uint2*>(rec + ((c * NT + nt) * 8 + s8) * 256 + lane * 8) = st;
-        }
-#pragma unroll
-        for (int e = 0; e < 32; ++e) xs += v[e];
     }
     xs += __shfl_xor_sync(0xffffffffu, xs, 1);
     xs += __shfl_xor_sync(0xffffffffu, xs, 2);
-    if (q == 0) reinterpret_cast<float*>(rec + CH * NT * 2048)[nt * 8 + n] = xs;
+    bias += __shfl_xor_sync(0xffffffffu, bias, 1);
+    bias += __shfl_xor_sync(0xffffffffu, bias, 2);
+    if (q == 0) {
+        float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
+        xg[nt * 8 + n] = live ? xs : 0.f;
+        xg[16 + nt * 8 + n] = live ? bias : 0.f;
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
 }
 
-// 4x4 bit-matrix transpose of four plane words (bit j = weight j of the
+// Bit-matrix transpose of NP (<=4) plane words (bit j = weight j of the
 // 32-weight word) into nibble words: q[a] nibble n = code of weight 4n+a.
+// Each delta-swap half is one shift plus one LOP3 select (15 ops for 3 planes).
 template <int NP>
 __device__ __forceinline__ void planes_to_nibbles(const uint32_t* p, uint32_t (&q)[4]) {
-    uint32_t p0 = p[0], p1 = NP > 1 ? p[1] : 0u, p2 = NP > 2 ? p[2] : 0u, p3 = NP > 3 ? p[3] : 0u;
-    uint32_t t;
-    if (NP > 1) {
-        t = ((p0 >> 1) ^ p1) & 0x55555555u;
-        p1 ^= t;
-        p0 ^= t << 1;
+    constexpr uint32_t kO = 0xAAAAAAAAu, kH = 0xCCCCCCCCu;
+    uint32_t r0, r1, r2 = 0u, r3 = 0u;
+    // stage 1: pairs (p0,p1), (p2,p3) -> 2-bit crumbs
+    if constexpr (NP > 1) {
+        r0 = lop3_sel<kO>(p[0], p[1] << 1);
+        r1 = lop3_sel<kO>(p[0] >> 1, p[1]);
     } else {
-        t = (p0 >> 1) & 0x55555555u;
-        p1 = t;
-        p0 ^= t << 1;
+        r0 = p[0] & ~kO;
+        r1 = (p[0] >> 1) & ~kO;
     }
-    if (NP > 2) {
-        if (NP > 3) {
-            t = ((p2 >> 1) ^ p3) & 0x55555555u;
-            p3 ^= t;
-            p2 ^= t << 1;
-        } else {
-            t = (p2 >> 1) & 0x55555555u;
-            p3 = t;
-            p2 ^= t << 1;
-        }
-        t = ((p0 >> 2) ^ p2) & 0x33333333u;
-        p2 ^= t;
-        p0 ^= t << 2;
-        t = ((p1 >> 2) ^ p3) & 0x33333333u;
-        p3 ^= t;
-        p1 ^= t << 2;
+    if constexpr (NP > 3) {
+        r2 = lop3_sel<kO>(p[2], p[3] << 1);
+        r3 = lop3_sel<kO>(p[2] >> 1, p[3]);
+    } else if constexpr (NP > 2) {
+        r2 = p[2] & ~kO;
+        r3 = (p[2] >> 1) & ~kO;
+    }
+    // stage 2: pairs (r0,r2), (r1,r3) -> nibbles
+    if constexpr (NP > 2) {
+        q[0] = lop3_sel<kH>(r0, r2 << 2);
+        q[2] = lop3_sel<kH>(r0 >> 2, r2);
+        q[1] = lop3_sel<kH>(r1, r3 << 2);
+        q[3] = lop3_sel<kH>(r1 >> 2, r3);
     } else {
-        t = (p0 >> 2) & 0x33333333u;
-        p2 = t;
-        p0 ^= t << 2;
-        t = (p1 >> 2) & 0x33333333u;
-        p3 = t;
-        p1 ^= t << 2;
+        q[0] = r0 & ~kH;
+        q[2] = (r0 >> 2) & ~kH;
+        q[1] = r1 & ~kH;
+        q[3] = (r1 >> 2) & ~kH;
     }
-    q[0] = p0;
-    q[1] = p1;
-    q[2] = p2;
-    q[3] = p3;
 }
 
-// Nibble word -> 4 half2 of exact integer codes:
-// h[0]=(nib0,nib4) h[1]=(nib1,nib5) h[2]=(nib2,nib6) h[3]=(nib3,nib7).
-__device__ __forceinline__ void nibbles_to_h2(uint32_t q, uint32_t* h) {
-    const uint32_t kMagic = 0x64006400u;  // 1024.0 in both halves
-    const __half2 k1024 = u32_as_h2(0x64006400u);
-    const __half2 k16th = u32_as_h2(0x2C002C00u);  // 1/16
-    const __half2 kM64 = u32_as_h2(0xD400D400u);   // -64
+// Nibble word -> 4 f16x2 with magic offsets (exact):
+// h[0]=(nib0,nib4)+1024 h[1]=(nib1,nib5)+64 h[2]=(nib2,nib6)+1024 h[3]=(nib3,nib7)+64.
+__device__ __forceinline__ void nibbles_to_h2_biased(uint32_t q, uint32_t* h) {
     const uint32_t q8 = q >> 8;
-    h[0] = h2_as_u32(__hsub2(u32_as_h2(lop3_and_or(q, 0x000F000Fu, kMagic)), k1024));
-    h[1] = h2_as_u32(__hfma2(u32_as_h2(lop3_and_or(q, 0x00F000F0u, kMagic)), k16th, kM64));
-    h[2] = h2_as_u32(__hsub2(u32_as_h2(lop3_and_or(q8, 0x000F000Fu, kMagic)), k1024));
-    h[3] = h2_as_u32(__hfma2(u32_as_h2(lop3_and_or(q8, 0x00F000F0u, kMagic)), k16th, kM64));
+    h[0] = lop3_and_or(q, 0x000F000Fu, 0x64006400u);   // 1024 + c (ulp 1)
+    h[1] = lop3_and_or(q, 0x00F000F0u, 0x54005400u);   // 64 + c   (ulp 1/16, bits 4-7)
+    h[2] = lop3_and_or(q8, 0x000F000Fu, 0x64006400u);
+    h[3] = lop3_and_or(q8, 0x00F000F0u, 0x54005400u);
 }
 
-// All 32 weights of one row word as 16 half2 codes; H[4a+h] = weights
-// (4h+a, 4h+a+16) of the word.
+// Exact codes (no offset), used for 5..8-bit blocks where hi*16+lo must stay exact.
+__device__ __forceinline__ void nibbles_to_h2_exact(uint32_t q, uint32_t* h) {
+    const __half2 k1024 = u32_as_h2(0x64006400u);
+    const __half2 k64 = u32_as_h2(0x54005400u);
+    uint32_t b[4];
+    nibbles_to_h2_biased(q, b);
+    h[0] = h2_as_u32(__hsub2(u32_as_h2(b[0]), k1024));
+    h[1] = h2_as_u32(__hsub2(u32_as_h2(b[1]), k64));
+    h[2] = h2_as_u32(__hsub2(u32_as_h2(b[2]), k1024));
+    h[3] = h2_as_u32(__hsub2(u32_as_h2(b[3]), k64));
+}
+
+// All 32 weights of one row word as 16 f16x2; H[4a+h] = weights (4h+a,
+// 4h+a+16) of the word.  B<=4: magic-biased codes; B>4: exact codes.
 template <int B>
 __device__ __forceinline__ void unpack_word(const uint32_t* p, uint32_t (&H)[16]) {
     uint32_t q[4];
     if constexpr (B <= 4) {
         planes_to_nibbles<B>(p, q);
 #pragma unroll
-        for (int a = 0; a < 4; ++a) nibbles_to_h2(q[a], H + 4 * a);
+        for (int a = 0; a < 4; ++a) nibbles_to_h2_biased(q[a], H + 4 * a);
     } else {
         uint32_t qh[4];
         planes_to_nibbles<4>(p, q);
@@ -213,8 +262,8 @@ __device__ __forceinline__ void unpack_word(const uint32_t* p, uint32_t (&H)[16]
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             uint32_t lo[4], hi[4];
-            nibbles_to_h2(q[a], lo);
-            nibbles_to_h2(qh[a], hi);
+            nibbles_to_h2_exact(q[a], lo);
+            nibbles_to_h2_exact(qh[a], hi);
 #pragma unroll
             for (int h = 0; h < 4; ++h)
                 H[4 * a + h] = h2_as_u32(__hfma2(u32_as_h2(hi[h]), k16, u32_as_h2(lo[h])));
@@ -222,43 +271,68 @@ __device__ __forceinline__ void unpack_word(const uint32_t* p, uint32_t (&H)[16]
     }
 }
 
-template <int B, int NT>
-__device__ __forceinline__ void unit_chunk(const uint8_t* wst, const uint8_t* xst, int c, int nb8,
-                                           int r0, int q, int lane, float (&cacc)[2][NT][4]) {
-    const uint8_t* planes = wst + 4 * kTR;
-    const int plane_stride = kTR * nb8;
-    uint32_t p0[B], p1[B];
+// One 128-column chunk of a unit for this warp's 32 rows (2 m16 tiles), four
+// independent accumulator chains (m-tile x even/odd k-step).  prow / xb are
+// 32-bit shared addresses; all other offsets are compile-time immediates.
+template <int B, int NT, int CH>
+__device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[NT], int chunk_bytes, int c,
+                                           float (&cacc)[4][NT][4]) {
+    constexpr int NB8 = CH * 16;   // bytes of one row of one plane
+    constexpr int PS = kTR * NB8;  // bytes of one plane of the unit
+    // rows r0, r0+8 (m-tile 0) and r0+16, r0+24 (m-tile 1)
+    uint32_t p[4][B];
 #pragma unroll
-    for (int i = 0; i < B; ++i) {
-        p0[i] = *reinterpret_cast<const uint32_t*>(planes + i * plane_stride + r0 * nb8 + c * 16 + q * 4);
-        p1[i] = *reinterpret_cast<const uint32_t*>(planes + i * plane_stride + (r0 + 8) * nb8 + c * 16 +
-                                                   q * 4);
-    }
-    uint32_t A0[16], A1[16];
-    unpack_word<B>(p0, A0);
-    unpack_word<B>(p1, A1);
+    for (int i = 0; i < B; ++i)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) p[r][i] = lds_u32(prow + i * PS + r * 8 * NB8 + c * 16);
+    uint32_t A[4][16];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) unpack_word<B>(p[r], A[r]);
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const uint2 b = *reinterpret_cast<const uint2*>(xst + ((c * NT + nt) * 8 + s) * 256 + lane * 8);
-            // two independent accumulator chains halve the HMMA dependency depth
-            mma_16816(cacc[s & 1][nt], A0[2 * s], A1[2 * s], A0[2 * s + 1], A1[2 * s + 1], b.x, b.y);
+            const uint2 b = lds_v2(xb[nt] + c * chunk_bytes + s * 32);
+            mma_16816(cacc[s & 1][nt], A[0][2 * s], A[1][2 * s], A[0][2 * s + 1], A[1][2 * s + 1], b.x, b.y);
+            mma_16816(cacc[2 + (s & 1)][nt], A[2][2 * s], A[3][2 * s], A[2][2 * s + 1], A[3][2 * s + 1], b.x,
+                      b.y);
         }
     }
 }
 
-template <int NT>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) gemv_kernel(const Params p) {
+__host__ __device__ constexpr int recv_bytes(int C, int NT) {
+    return C > 1 ? (C * 8 * NT * ((kTR + C - 1) / C) * 4 + 127) / 128 * 128 : 0;
+}
+// First row of rank k's share of a 128-row tile split C ways.
+__device__ __forceinline__ int share_begin(int k, int C) { return k * kTR / C; }
+
+// LO = the model's floor bit-width: every unit has LO or LO+1 bits
+// (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
+// two unpack paths and its hot loop stays resident in the instruction cache.
+template <int NT, int CH, int LO>
+__global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const Params p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
+    const int C = p.C;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
-    int* flag = reinterpret_cast<int*>(empty + S);
-    uint8_t* wbase = smem + 512;
+    uint8_t* zeros = smem + 256;                               // 256 B: B fragments of absent tokens
+    uint32_t* sbits = reinterpret_cast<uint32_t*>(smem + 512);  // bit-width of the unit in stage s
+    uint32_t* omap = reinterpret_cast<uint32_t*>(smem + 640);   // out_map of the rows this rank stores
+    // cluster-reduction receive buffer recv[src_rank][t < 8*NT][RPM] (f32), a
+    // region of its own so early finishers never overwrite a live ring stage
+    uint8_t* recvbuf = smem + kHdrBytes;
+    uint8_t* wbase = recvbuf + recv_bytes(C, NT);
     uint8_t* xbase = wbase + static_cast<size_t>(S) * p.stage_w;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int dbg = p.debug_mode;
+    if (threadIdx.x == 0) DBG_STAMP(0);
+    const int rank = C > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    const int rt = blockIdx.x / C;
+    const int bc0 = rank * p.BC / C, bc1 = (rank + 1) * p.BC / C;
+    const int nunits = bc1 - bc0;
+    const int rb0 = share_begin(rank, C), rb1 = share_begin(rank + 1, C);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -267,272 +341,310 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) gemv_kernel(const Params
         fence_mbar_init();
         fence_proxy_async();
     }
+    if (threadIdx.x < 64) reinterpret_cast<uint32_t*>(zeros)[threadIdx.x] = 0u;
     __syncthreads();
 
-    const int u0 = p.cta_begin[blockIdx.x], u1 = p.cta_begin[blockIdx.x + 1];
-    const int nb8 = p.n_b >> 3;
-    const int CH = p.n_b >> 7;
-    const int tiles_per_brow = p.m_b / kTR;
+    constexpr int nb8 = CH * 16;
+    const RecGeom G{p.M};
+    const uint64_t* gdesc = p.unit_desc + static_cast<size_t>(rt) * p.BC + bc0;
 
     if (warp == 0) {
-        // ---------------- producer: bulk copies (weights now, x after PDL wait) ----
+        // ---------------- producer: one bulk copy per unit (+ its activation record) ----
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             const uint32_t pbytes = kTR * nb8;
-            const size_t plane_bytes = static_cast<size_t>(p.m_b) * nb8;
-            int rt = u0 / p.BC, bc = u0 - rt * p.BC;
-            auto issue_w = [&](int s, int rt_, int bc_) {
-                const int br = rt_ / tiles_per_brow, ro = (rt_ - br * tiles_per_brow) * kTR;
-                const size_t k = static_cast<size_t>(br) * p.BC + bc_;
-                const int bits = p.bits[k];
-                const uint8_t* blk = p.payload + p.off[k];
-                uint8_t* dst = wbase + static_cast<size_t>(s) * p.stage_w;
-                mbar_arrive_expect_tx(&full[s], 4 * kTR + bits * pbytes + p.stage_x);
-                bulk_g2s(dst, blk + 2 * ro, 2 * kTR, &full[s], pol);
-                bulk_g2s(dst + 2 * kTR, blk + 2 * p.m_b + 2 * ro, 2 * kTR, &full[s], pol);
-                for (int b = 0; b < bits; ++b)
-                    bulk_g2s(dst + 4 * kTR + b * pbytes,
-                             blk + 4 * static_cast<size_t>(p.m_b) + b * plane_bytes + static_cast<size_t>(ro) * nb8,
-                             pbytes, &full[s], pol);
+            auto issue_w = [&](int s, int i, uint64_t d) {
+                const int bits = static_cast<int>((d >> 48) & 0xF);
+                sbits[s] = static_cast<uint32_t>(bits);  // published by the arrive below
+                DBG_STAMP(2 + 3 * i);
+                const uint32_t wbytes = 4 * kTR + bits * pbytes;
+                mbar_arrive_expect_tx(&full[s], wbytes + p.rec_bytes);
+                bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, p.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
+                         &full[s], pol);
             };
             auto issue_x = [&](int s, int bc_) {
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_u32(xbase + static_cast<size_t>(s) * p.stage_x)),
-                    "l"(p.xfrag + static_cast<size_t>(bc_) * p.stage_x), "r"(p.stage_x), "r"(smem_u32(&full[s]))
+                        smem_u32(xbase + static_cast<size_t>(s) * p.rec_bytes)),
+                    "l"(p.xrec + static_cast<size_t>(bc_) * p.rec_bytes), "r"(p.rec_bytes), "r"(smem_u32(&full[s]))
                     : "memory");
             };
-            const int n = u1 - u0;
-            const int pre = n < S ? n : S;
+            const int pre = nunits < S ? nunits : S;
             // 1) weights of the first ring-full of units do not depend on x
-            int prt = rt, pbc = bc;
-            for (int i = 0; i < pre; ++i) {
-                issue_w(i, prt, pbc);
-                if (++pbc == p.BC) { pbc = 0; ++prt; }
-            }
-            // 2) wait for the x-fragment producer (programmatic dependent launch)
+            uint64_t dpre[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < pre) dpre[i] = __ldg(gdesc + i);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < pre) issue_w(i, i, dpre[i]);
+            uint64_t dnext = pre < nunits ? __ldg(gdesc + pre) : 0;
+            // 2) wait for the activation-record producer (programmatic dependent launch)
             pdl_wait();
-            prt = rt;
-            pbc = bc;
-            for (int i = 0; i < pre; ++i) {
-                issue_x(i, pbc);
-                if (++pbc == p.BC) { pbc = 0; ++prt; }
-            }
-            // 3) steady state
-            for (int i = pre; i < n; ++i) {
-                const int s = i % S;
-                mbar_wait(&empty[s], ((i / S) - 1) & 1);
-                issue_w(s, prt, pbc);
-                issue_x(s, pbc);
-                if (++pbc == p.BC) { pbc = 0; ++prt; }
+            for (int i = 0; i < pre; ++i) issue_x(i, bc0 + i);
+            // 3) steady state: unit i reuses stage i % S after round i/S - 1 drained
+            int s = 0, ph = 0;
+            for (int i = pre; i < nunits; ++i) {
+                const uint64_t d = dnext;
+                if (i + 1 < nunits) dnext = __ldg(gdesc + i + 1);
+                mbar_wait(&empty[s], ph);
+                issue_w(s, i, d);
+                issue_x(s, bc0 + i);
+                if (++s == S) { s = 0; ph ^= 1; }
             }
         }
-        return;
-    }
-
-    // ---------------- compute warps ------------------------------------------
-    const int cw = warp - 1;
-    const int g = lane >> 2, q = lane & 3;
-    const int r0 = cw * 16 + g;  // row within the unit; second row r0+8
-    const int ct = threadIdx.x - kFirstCompute;
-    float yacc[NT][4];
+    } else {
+        // ---------------- compute warps ------------------------------------------
+        const int cw = warp - 1;
+        const int g = lane >> 2, q = lane & 3;
+        const int r0 = cw * 32 + g;  // rows r0 + {0, 8, 16, 24} of the tile
+        // output columns of the rows this CTA stores, fetched early (published to
+        // the cluster-reduction readers by the cluster barrier)
+        uint32_t my_map[4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+        for (int r = 0; r < 4; ++r) my_map[r] = C == 1 ? __ldg(p.out_map + rt * kTR + r0 + 8 * r) : 0u;
+        for (int r = threadIdx.x - 32; C > 1 && r < rb1 - rb0; r += kThreads - 32)
+            omap[r] = __ldg(p.out_map + rt * kTR + rb0 + r);
+        float yacc[2][NT][4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) yacc[nt][e] = 0.f;
-
-    auto flush = [&](int rt) {
-        const int nseg = p.rt_nseg[rt];
-        const int rowbase = rt * kTR;
-        if (nseg == 1) {
+        for (int m = 0; m < 2; ++m)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int t = nt * 8 + 2 * q + (e & 1);
-                    const int row = r0 + (e >> 1) * 8;
-                    if (t < p.M) p.y[t * p.out_rows + p.out_map[rowbase + row]] = yacc[nt][e];
-                }
-            return;
-        }
-        const int slot0 = p.rt_slot[rt];
-        const int slot = slot0 + (blockIdx.x - p.rt_first[rt]);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int t = nt * 8 + 2 * q + (e & 1);
-                const int row = r0 + (e >> 1) * 8;
-                if (t < p.M) p.ws[(static_cast<size_t>(slot) * 16 + t) * kTR + row] = yacc[nt][e];
-            }
-        __threadfence();
-        named_bar_sync(1, kNCW * 32);
-        if (ct == 0) *flag = (atomicAdd(&p.counters[rt], 1u) == static_cast<unsigned>(nseg - 1));
-        named_bar_sync(1, kNCW * 32);
-        if (*flag) {
-            __threadfence();
-            for (int idx = ct; idx < p.M * kTR; idx += kNCW * 32) {
-                const int t = idx >> 7, row = idx & (kTR - 1);
-                float acc = 0.f;
-                for (int sg = 0; sg < nseg; ++sg)
-                    acc += __ldcg(p.ws + (static_cast<size_t>(slot0 + sg) * 16 + t) * kTR + row);
-                p.y[t * p.out_rows + p.out_map[rowbase + row]] = acc;
-            }
-            if (ct == 0) p.counters[rt] = 0u;
-        }
-    };
-
-    int rt = u0 / p.BC, bc = u0 - rt * p.BC;
-    int cur_rt = rt;
-    int s = 0, ph = 0;
-    for (int u = u0; u < u1; ++u) {
-        if (rt != cur_rt) {
-            flush(cur_rt);
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) yacc[nt][e] = 0.f;
-            cur_rt = rt;
-        }
-        const int bits = p.bits[static_cast<size_t>(rt / tiles_per_brow) * p.BC + bc];
-        const uint8_t* wst = wbase + static_cast<size_t>(s) * p.stage_w;
-        const uint8_t* xst = xbase + static_cast<size_t>(s) * p.stage_x;
-        mbar_wait(&full[s], ph);
-        const __half* sz = reinterpret_cast<const __half*>(wst);
-        const float s0 = __half2float(sz[r0]), s1 = __half2float(sz[r0 + 8]);
-        const float z0 = __half2float(sz[kTR + r0]), z1 = __half2float(sz[kTR + r0 + 8]);
-        float cacc[2][NT][4];
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) cacc[h][nt][e] = 0.f;
-        for (int c = 0; c < CH; ++c) {
-            switch (bits) {
-                case 1: unit_chunk<1, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-                case 2: unit_chunk<2, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-                case 3: unit_chunk<3, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-                case 4: unit_chunk<4, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-                case 5: unit_chunk<5, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-                case 6: unit_chunk<6, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-                case 7: unit_chunk<7, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-                default: unit_chunk<8, NT>(wst, xst, c, nb8, r0, q, lane, cacc); break;
-            }
-        }
-        const float* xg = reinterpret_cast<const float*>(xst + CH * NT * 2048);
+                for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
+        const int chunk_bytes = G.chunk_bytes();
+        const uint32_t stage_w = p.stage_w, rec_bytes = p.rec_bytes;
+        // per-lane shared addresses for stage 0; a stage adds s * stage_w / rec_bytes
+        const uint32_t prow0 = smem_u32(wbase) + 4 * kTR + r0 * nb8 + q * 4;
+        const uint32_t sz0 = smem_u32(wbase) + 2 * r0;
+        uint32_t xb0[NT], xstep[NT];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const float xg0 = xg[nt * 8 + 2 * q], xg1 = xg[nt * 8 + 2 * q + 1];
-            yacc[nt][0] += s0 * (cacc[0][nt][0] + cacc[1][nt][0]) + z0 * xg0;
-            yacc[nt][1] += s0 * (cacc[0][nt][1] + cacc[1][nt][1]) + z0 * xg1;
-            yacc[nt][2] += s1 * (cacc[0][nt][2] + cacc[1][nt][2]) + z1 * xg0;
-            yacc[nt][3] += s1 * (cacc[0][nt][3] + cacc[1][nt][3]) + z1 * xg1;
+            const bool live = g < G.mnt(nt);
+            xb0[nt] = live ? smem_u32(xbase) + G.lane_off(0, nt, g, q) : smem_u32(zeros) + q * 8;
+            xstep[nt] = live ? rec_bytes : 0u;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
-        if (++bc == p.BC) { bc = 0; ++rt; }
+        const uint32_t xg0 = smem_u32(xbase) + G.xg_off(CH) + 8 * q;
+        const uint32_t sbits_a = smem_u32(sbits);
+        int s = 0, ph = 0;
+        for (int i = 0; i < nunits; ++i) {
+            mbar_wait(&full[s], ph);
+            if (cw == 0 && lane == 0) DBG_STAMP(3 + 3 * i);
+            const int bits = static_cast<int>(lds_u32(sbits_a + 4 * s));
+            uint32_t xb[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + s * xstep[nt];
+            const uint32_t prow = prow0 + s * stage_w;
+            float cacc[4][NT][4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) cacc[h][nt][e] = 0.f;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                if (bits == LO) {
+                    unit_chunk<LO, NT, CH>(prow, xb, chunk_bytes, c, cacc);
+                } else if constexpr (LO < 8) {
+                    unit_chunk<LO + 1, NT, CH>(prow, xb, chunk_bytes, c, cacc);
+                }
+            }
+            // per-row affine of this block: y += s*(C - bias) + z*Xg
+            const uint32_t sz = sz0 + s * stage_w;
+            const uint32_t xg = xg0 + s * rec_bytes;
+            const bool biased = bits <= 4;
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
+                const float za = lds_h2f(sz + 2 * kTR + 32 * m), zb = lds_h2f(sz + 2 * kTR + 32 * m + 16);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const float2 xg01 = lds_f2(xg + 32 * nt);
+                    float2 b01 = lds_f2(xg + 64 + 32 * nt);
+                    if (!biased) b01 = make_float2(0.f, 0.f);
+                    const float* c0 = cacc[2 * m][nt];
+                    const float* c1 = cacc[2 * m + 1][nt];
+                    yacc[m][nt][0] += sa * ((c0[0] + c1[0]) - b01.x) + za * xg01.x;
+                    yacc[m][nt][1] += sa * ((c0[1] + c1[1]) - b01.y) + za * xg01.y;
+                    yacc[m][nt][2] += sb * ((c0[2] + c1[2]) - b01.x) + zb * xg01.x;
+                    yacc[m][nt][3] += sb * ((c0[3] + c1[3]) - b01.y) + zb * xg01.y;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (cw == 0 && lane == 0) DBG_STAMP(4 + 3 * i);
+            if (++s == S) { s = 0; ph ^= 1; }
+        }
+        if (C == 1) {
+            // whole row tile in this CTA: un-permuted store straight to y
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int t = nt * 8 + 2 * q + (e & 1);
+                        if (t < p.M) p.y[t * p.out_rows + my_map[2 * m + (e >> 1)]] = yacc[m][nt][e];
+                    }
+        } else {
+            // push each partial to the shared memory of the rank that owns its row:
+            // recv[src_rank][t][row - owner_begin], stride RPM = ceil(128 / C)
+            const int RPM = (kTR + C - 1) / C;
+            const uint32_t recv_local = smem_u32(recvbuf);
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int row = r0 + 16 * m + 8 * h;
+                    int owner = row * C / kTR;
+                    while (owner > 0 && share_begin(owner, C) > row) --owner;
+                    while (owner + 1 < C && share_begin(owner + 1, C) <= row) ++owner;
+                    const int lrow = row - share_begin(owner, C);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int t = nt * 8 + 2 * q + e;
+                            if (t < p.M) {
+                                const uint32_t off = static_cast<uint32_t>(((rank * 8 * NT + t) * RPM + lrow) * 4);
+                                st_dsmem_f32(mapa_shared(recv_local + off, static_cast<uint32_t>(owner)),
+                                             yacc[m][nt][2 * h + e]);
+                            }
+                        }
+                }
+        }
     }
-    if (u1 > u0) flush(cur_rt);
+    if (C > 1) {
+        // Deterministic split-K across the cluster: after one cluster barrier
+        // every rank holds all C partials of its rows; sum them in rank order.
+        cluster_sync_all();
+        const int RPM = (kTR + C - 1) / C;
+        const float* recv = reinterpret_cast<const float*>(recvbuf);
+        const int nrow = rb1 - rb0, nvals = nrow * p.M;
+        for (int v = threadIdx.x; v < nvals; v += kThreads) {
+            const int t = v / nrow, lrow = v - t * nrow;
+            float acc = 0.f;
+            for (int r = 0; r < C; ++r) acc += recv[(r * 8 * NT + t) * RPM + lrow];
+            p.y[t * p.out_rows + omap[lrow]] = acc;
+        }
+    }
+    if (threadIdx.x == 0) DBG_STAMP(1);
 }
 
-template <class K>
-cudaError_t set_smem_once(K k, int slot) {
-    static int configured[2][64] = {{0}};
+template <int NT, int CH, int LO>
+cudaError_t launch_k(cudaLaunchConfig_t& cfg, const Params& p) {
+    auto k = gemv_kernel<NT, CH, LO>;
+    static int configured[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !configured[slot][dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemPerCta);
+    if (dev < 64 && !configured[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_cta(NT));
         if (e != cudaSuccess) return e;
-        configured[slot][dev] = 1;
+        configured[dev] = 1;
     }
-    return cudaSuccess;
+    return cudaLaunchKernelEx(&cfg, k, p);
 }
 
-template <int NT, sfmp_dtype DT>
+template <int NT, int CH>
+cudaError_t launch_nc(cudaLaunchConfig_t& cfg, const Params& p, int lo) {
+    switch (lo) {
+        case 1: return launch_k<NT, CH, 1>(cfg, p);
+        case 2: return launch_k<NT, CH, 2>(cfg, p);
+        case 3: return launch_k<NT, CH, 3>(cfg, p);
+        case 4: return launch_k<NT, CH, 4>(cfg, p);
+        case 5: return launch_k<NT, CH, 5>(cfg, p);
+        case 6: return launch_k<NT, CH, 6>(cfg, p);
+        case 7: return launch_k<NT, CH, 7>(cfg, p);
+        default: return launch_k<NT, CH, 8>(cfg, p);
+    }
+}
+
+template <sfmp_dtype DT>
 cudaError_t launch_t(const Params& p, const void* x, const uint32_t* col_perm, int cols, int grid, size_t smem,
-                     cudaStream_t st) {
-    // K4: x fragments (normal launch: it overwrites the workspace the previous
-    // call may still read, so it must follow it in stream order).
+                     int lo, cudaStream_t st) {
+    // K4: activation records (normal launch: it overwrites the workspace the
+    // previous call may still read, so it must follow it in stream order).
+    const int NT = p.M > 8 ? 2 : 1;
     const int warps = p.BC * NT;
-    xprep_kernel<NT, DT><<<(warps + 7) / 8, 256, 0, st>>>(x, col_perm, const_cast<uint8_t*>(p.xfrag), p.M,
-                                                          cols, p.n_b, p.BC, p.stage_x);
+    xprep_kernel<DT><<<(warps + 7) / 8, 256, 0, st>>>(x, col_perm, const_cast<uint8_t*>(p.xrec), p.M, cols,
+                                                      p.n_b, p.BC, p.rec_bytes, p.debug_mode);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    auto k = gemv_kernel<NT>;
-    if ((e = set_smem_once(k, NT - 1)) != cudaSuccess) return e;
-    // K1 with programmatic dependent launch: its producer streams weights
-    // while xprep runs and waits (griddepcontrol.wait) only before the x copies.
+    // K1: one cluster of C CTAs per 128-row tile, programmatic dependent of xprep
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(p.C);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, p);
+    cfg.numAttrs = 2;
+    const int CH = p.n_b / 128;
+    if (NT == 1) return CH == 1 ? launch_nc<1, 1>(cfg, p, lo) : launch_nc<1, 2>(cfg, p, lo);
+    return CH == 1 ? launch_nc<2, 1>(cfg, p, lo) : launch_nc<2, 2>(cfg, p, lo);
 }
 
 }  // namespace
 
-static uint32_t stage_x_bytes(const DevModel& m, int NT) {
-    return static_cast<uint32_t>((static_cast<int>(m.n_b / 128) * NT * 2048 + 64 + 127) / 128 * 128);
+// Not part of the ABI: copies the debug timeline (SFMP_GEMV_DEBUG=5) to the host.
+extern "C" int sfmp_debug_gemv_timeline(unsigned long long* host, size_t n) {
+    if (n > static_cast<size_t>(kDbgCtas) * kDbgSlots) n = static_cast<size_t>(kDbgCtas) * kDbgSlots;
+    return static_cast<int>(cudaMemcpyFromSymbol(host, g_dbg_timeline, n * sizeof(unsigned long long)));
 }
 
 size_t gemv_workspace_bytes(const DevModel& m, int M) {
     (void)M;
-    const size_t partial = static_cast<size_t>(m.gemv.total_slots) * 16 * kTR * sizeof(float);
-    const size_t xfrag = static_cast<size_t>(m.gemv.block_cols) * stage_x_bytes(m, 2);
-    return (partial + 255) / 256 * 256 + xfrag;
+    return static_cast<size_t>(m.BC) * RecGeom{16}.bytes(static_cast<int>(m.n_b / 128));
 }
 
-int gemv_ctas_per_sm() { return kCtasPerSm; }
+int gemv_ctas_per_sm(int NT) { return ctas_per_sm(NT); }
 
 cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, float* y, float* ws,
                         cudaStream_t st) {
-    const GemvSchedule& g = m.gemv;
+    const int NT = M > 8 ? 2 : 1;
     Params p{};
     p.payload = m.d_payload;
-    p.off = m.d_off;
-    p.bits = m.d_bits;
+    p.unit_desc = m.d_unit_desc;
     p.out_map = m.d_out_map;
     p.y = y;
-    p.ws = ws;
-    const size_t partial = static_cast<size_t>(g.total_slots) * 16 * kTR * sizeof(float);
-    p.xfrag = reinterpret_cast<const uint8_t*>(ws) + (partial + 255) / 256 * 256;
-    p.cta_begin = g.d_cta_begin;
-    p.rt_nseg = g.d_rt_nseg;
-    p.rt_slot = g.d_rt_slot;
-    p.rt_first = g.d_rt_first;
-    p.counters = g.d_counters;
+    p.xrec = reinterpret_cast<const uint8_t*>(ws);
     p.M = M;
-    p.BC = g.block_cols;
-    p.m_b = static_cast<int>(m.m_b);
+    p.BC = static_cast<int>(m.BC);
     p.n_b = static_cast<int>(m.n_b);
     p.out_rows = m.out_rows;
-    const int NT = M > 8 ? 2 : 1;
+    {
+        const char* dbg = getenv("SFMP_GEMV_DEBUG");
+        p.debug_mode = dbg ? atoi(dbg) : 0;
+    }
+    // cluster size: split the block columns of every 128-row tile C ways, as
+    // many ways as fit one wave of resident CTAs (C <= 8, portable clusters)
+    const int RT = static_cast<int>(m.RT);
+    const int slots = m.num_sms * ctas_per_sm(NT);
+    p.C = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({8, p.BC, slots / std::max(RT, 1)})));
+    if (const char* cs = getenv("SFMP_GEMV_SPLIT")) p.C = std::max(1, std::min({8, p.BC, atoi(cs)}));
+    const int CH = static_cast<int>(m.n_b / 128);
     p.stage_w = static_cast<uint32_t>((4 * kTR + m.ceil_bits * kTR * (m.n_b / 8) + 127) / 128 * 128);
-    p.stage_x = stage_x_bytes(m, NT);
-    const int stages = std::min<int>(16, (kSmemPerCta - 512) / static_cast<int>(p.stage_w + p.stage_x));
+    p.rec_bytes = static_cast<uint32_t>(RecGeom{M}.bytes(CH));
+    int max_stages = 4;
+    if (const char* ss = getenv("SFMP_GEMV_STAGES")) max_stages = std::max(2, atoi(ss));
+    const int fixed = kHdrBytes + recv_bytes(p.C, NT);
+    const int stages = std::min<int>(max_stages, (smem_per_cta(NT) - fixed) / static_cast<int>(p.stage_w + p.rec_bytes));
     if (stages < 2) return cudaErrorInvalidConfiguration;
     p.stages = stages;
-    const size_t smem = 512 + static_cast<size_t>(stages) * (p.stage_w + p.stage_x);
+    const size_t smem = fixed + static_cast<size_t>(stages) * (p.stage_w + p.rec_bytes);
     const int cols = static_cast<int>(m.cols);
-    if (NT == 1) {
-        switch (dt) {
-            case SFMP_F32: return launch_t<1, SFMP_F32>(p, x, m.d_col_perm, cols, g.grid, smem, st);
-            case SFMP_F16: return launch_t<1, SFMP_F16>(p, x, m.d_col_perm, cols, g.grid, smem, st);
-            default: return launch_t<1, SFMP_BF16>(p, x, m.d_col_perm, cols, g.grid, smem, st);
-        }
-    }
+    const int grid = RT * p.C;
     switch (dt) {
-        case SFMP_F32: return launch_t<2, SFMP_F32>(p, x, m.d_col_perm, cols, g.grid, smem, st);
-        case SFMP_F16: return launch_t<2, SFMP_F16>(p, x, m.d_col_perm, cols, g.grid, smem, st);
-        default: return launch_t<2, SFMP_BF16>(p, x, m.d_col_perm, cols, g.grid, smem, st);
+        case SFMP_F32: return launch_t<SFMP_F32>(p, x, m.d_col_perm, cols, grid, smem, m.floor_bits, st);
+        case SFMP_F16: return launch_t<SFMP_F16>(p, x, m.d_col_perm, cols, grid, smem, m.floor_bits, st);
+        default: return launch_t<SFMP_BF16>(p, x, m.d_col_perm, cols, grid, smem, m.floor_bits, st);
     }
 }
 

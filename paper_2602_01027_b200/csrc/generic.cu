@@ -1,6 +1,7 @@
 // generic.cu -- geometry-agnostic kernels: the generic GEMM (any m_b, n_b, M),
 // K3 dequant/unpack (bit-exact parity entry points) and the sharded-output
-// un-permutation.  Paths relative to /root/reference/proj.
+// un-permutation.  All read the unit-major device layout (sfmp_internal.h).
+// Paths relative to /root/reference/proj.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -19,30 +20,45 @@ __device__ __forceinline__ float ldx(const void* x, size_t i) {
         return __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(x) + i));
 }
 
-__device__ __forceinline__ float fp16_at(const uint8_t* p) {
-    return __half2float(*reinterpret_cast<const __half*>(p));
-}
+// One row segment of one unit: scale/zero widened exactly from fp16
+// (fp16.hpp:58-83) and a code reader restating unpack_block (layout.cpp:77-83).
+struct RowRef {
+    const uint8_t* planes;  // plane 0 of the unit
+    uint64_t plane_bytes;   // TR * n_b / 8
+    uint32_t row_off;       // rr * n_b / 8
+    int bits;
+    float s, z;
+    __device__ __forceinline__ uint32_t code(uint32_t jj) const {
+        uint32_t c = 0;
+        for (int i = 0; i < bits; ++i)
+            c |= ((planes[i * plane_bytes + row_off + (jj >> 3)] >> (jj & 7)) & 1u) << i;
+        return c;
+    }
+};
 
-// Code of weight (rr, j) of one block: unpack_block (layout.cpp:77-83).
-__device__ __forceinline__ uint32_t block_code(const uint8_t* planes, int bits, uint64_t plane_bytes,
-                                               uint32_t rb, uint32_t rr, uint32_t j) {
-    uint32_t c = 0;
-    for (int i = 0; i < bits; ++i)
-        c |= ((planes[i * plane_bytes + static_cast<uint64_t>(rr) * rb + (j >> 3)] >> (j & 7)) & 1u) << i;
-    return c;
+__device__ __forceinline__ RowRef row_ref(const UnitGeom& g, uint64_t r, uint32_t bc) {
+    const uint64_t u = (r / g.TR) * g.BC + bc;
+    const uint64_t d = g.unit_desc[u];
+    const uint8_t* base = g.payload + (d & 0xFFFFFFFFFFFFull);
+    const uint32_t rr = static_cast<uint32_t>(r % g.TR);
+    RowRef ref;
+    ref.bits = static_cast<int>((d >> 48) & 0xF);
+    ref.s = __half2float(*reinterpret_cast<const __half*>(base + 2 * rr));
+    ref.z = __half2float(*reinterpret_cast<const __half*>(base + 2ull * g.TR + 2 * rr));
+    ref.planes = base + 4ull * g.TR;
+    ref.plane_bytes = static_cast<uint64_t>(g.TR) * (g.n_b >> 3);
+    ref.row_off = rr * (g.n_b >> 3);
+    return ref;
 }
 
 struct GenParams {
-    const uint8_t* payload;
-    const uint64_t* off;
-    const uint8_t* bits;
+    UnitGeom g;
     const uint32_t* col_perm;
     const uint32_t* out_map;
     const void* x;
     float* y;
     int64_t M;
     uint64_t rows, cols, out_rows;
-    uint32_t m_b, n_b, BC;
 };
 
 // One warp per reordered row, 8 tokens per pass; dequantised weight
@@ -52,23 +68,15 @@ __global__ void __launch_bounds__(256) generic_kernel(const GenParams p) {
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (r >= p.rows) return;
-    const uint32_t br = static_cast<uint32_t>(r / p.m_b), rr = static_cast<uint32_t>(r % p.m_b);
-    const uint32_t rb = p.n_b >> 3;
-    const uint64_t pb = static_cast<uint64_t>(p.m_b) * rb;
     for (int64_t t0 = 0; t0 < p.M; t0 += 8) {
         float acc[8];
 #pragma unroll
         for (int tt = 0; tt < 8; ++tt) acc[tt] = 0.f;
-        for (uint32_t bc = 0; bc < p.BC; ++bc) {
-            const uint64_t k = static_cast<uint64_t>(br) * p.BC + bc;
-            const int bits = p.bits[k];
-            const uint8_t* blk = p.payload + p.off[k];
-            const float s = fp16_at(blk + 2 * rr), z = fp16_at(blk + 2ull * p.m_b + 2 * rr);
-            const uint8_t* planes = blk + 4ull * p.m_b;
-            for (uint32_t j = lane; j < p.n_b; j += 32) {
-                const uint32_t c = block_code(planes, bits, pb, rb, rr, j);
-                const float w = __fadd_rn(__fmul_rn(s, static_cast<float>(c)), z);
-                const uint32_t col = p.col_perm[static_cast<uint64_t>(bc) * p.n_b + j];
+        for (uint32_t bc = 0; bc < p.g.BC; ++bc) {
+            const RowRef ref = row_ref(p.g, r, bc);
+            for (uint32_t j = lane; j < p.g.n_b; j += 32) {
+                const float w = __fadd_rn(__fmul_rn(ref.s, static_cast<float>(ref.code(j))), ref.z);
+                const uint32_t col = p.col_perm[static_cast<uint64_t>(bc) * p.g.n_b + j];
 #pragma unroll
                 for (int tt = 0; tt < 8; ++tt)
                     if (t0 + tt < p.M) acc[tt] += w * ldx<DT>(p.x, (t0 + tt) * p.cols + col);
@@ -90,28 +98,18 @@ __global__ void dequant_kernel(GenParams p, float* w) {
     const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= p.rows * p.cols) return;
     const uint64_t r = idx / p.cols, j = idx % p.cols;
-    const uint32_t br = static_cast<uint32_t>(r / p.m_b), rr = static_cast<uint32_t>(r % p.m_b);
-    const uint32_t bc = static_cast<uint32_t>(j / p.n_b), jj = static_cast<uint32_t>(j % p.n_b);
-    const uint64_t k = static_cast<uint64_t>(br) * p.BC + bc;
-    const uint8_t* blk = p.payload + p.off[k];
-    const uint32_t rb = p.n_b >> 3;
-    const uint32_t c = block_code(blk + 4ull * p.m_b, p.bits[k], static_cast<uint64_t>(p.m_b) * rb, rb, rr, jj);
-    const float s = fp16_at(blk + 2 * rr), z = fp16_at(blk + 2ull * p.m_b + 2 * rr);
+    const uint32_t bc = static_cast<uint32_t>(j / p.g.n_b), jj = static_cast<uint32_t>(j % p.g.n_b);
+    const RowRef ref = row_ref(p.g, r, bc);
     w[static_cast<uint64_t>(p.out_map[r]) * p.cols + p.col_perm[j]] =
-        __fadd_rn(__fmul_rn(s, static_cast<float>(c)), z);
+        __fadd_rn(__fmul_rn(ref.s, static_cast<float>(ref.code(jj))), ref.z);
 }
 
 __global__ void unpack_kernel(GenParams p, uint8_t* codes) {
     const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= p.rows * p.cols) return;
     const uint64_t r = idx / p.cols, j = idx % p.cols;
-    const uint32_t br = static_cast<uint32_t>(r / p.m_b), rr = static_cast<uint32_t>(r % p.m_b);
-    const uint32_t bc = static_cast<uint32_t>(j / p.n_b), jj = static_cast<uint32_t>(j % p.n_b);
-    const uint64_t k = static_cast<uint64_t>(br) * p.BC + bc;
-    const uint8_t* blk = p.payload + p.off[k];
-    const uint32_t rb = p.n_b >> 3;
-    codes[idx] = static_cast<uint8_t>(
-        block_code(blk + 4ull * p.m_b, p.bits[k], static_cast<uint64_t>(p.m_b) * rb, rb, rr, jj));
+    const uint32_t bc = static_cast<uint32_t>(j / p.g.n_b), jj = static_cast<uint32_t>(j % p.g.n_b);
+    codes[idx] = static_cast<uint8_t>(row_ref(p.g, r, bc).code(jj));
 }
 
 // gathered[g][t][i] -> y[t][gather_map[g*SR+i]] (padding rows map to ~0u).
@@ -129,17 +127,12 @@ __global__ void unpermute_kernel(const float* gathered, const uint32_t* gmap, fl
 
 GenParams make_params(const DevModel& m) {
     GenParams p{};
-    p.payload = m.d_payload;
-    p.off = m.d_off;
-    p.bits = m.d_bits;
+    p.g = m.geom();
     p.col_perm = m.d_col_perm;
     p.out_map = m.d_out_map;
     p.rows = m.rows;
     p.cols = m.cols;
     p.out_rows = m.out_rows;
-    p.m_b = m.m_b;
-    p.n_b = m.n_b;
-    p.BC = static_cast<uint32_t>(m.cols / m.n_b);
     return p;
 }
 
@@ -160,7 +153,7 @@ cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int6
     return cudaGetLastError();
 }
 
-cudaError_t launch_dequant(const DevModel& m, const uint32_t*, float* w, cudaStream_t st) {
+cudaError_t launch_dequant(const DevModel& m, float* w, cudaStream_t st) {
     GenParams p = make_params(m);
     const uint64_t n = m.rows * m.cols;
     dequant_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, w);

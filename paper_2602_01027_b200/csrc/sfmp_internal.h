@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -10,42 +11,40 @@
 
 namespace sfmpk {
 
-// Work schedule of the decode GEMV (K1): units are (row tile, block column)
-// pairs in row-tile-major order; CTA c owns units [cta_begin[c], cta_begin[c+1]).
-// A row tile touched by several CTAs is reduced by the last arriving CTA in
-// fixed segment order (deterministic split-K).
-struct GemvSchedule {
-    int tile_rows = 128;  // TR
-    int row_tiles = 0;    // RT
-    int block_cols = 0;   // BC
-    int grid = 0;         // G
-    int total_slots = 0;  // partial-sum slots (segments of multi-CTA row tiles)
-    int* d_cta_begin = nullptr;  // G+1
-    int* d_rt_nseg = nullptr;    // RT
-    int* d_rt_slot = nullptr;    // RT: first slot of the tile
-    int* d_rt_first = nullptr;   // RT: first CTA touching the tile
-    unsigned* d_counters = nullptr;  // RT arrival counters (self-resetting)
+// Device layout.  The SFMPPKD1 block payload
+// is stored UNIT-MAJOR: a unit is TR consecutive reordered rows x one block
+// column (n_b columns), TR = 128 when m_b % 128 == 0, else TR = m_b.  A unit
+// is one contiguous span
+//     scales[TR] (fp16) | zeros[TR] (fp16) | plane_0 .. plane_{bits-1}
+// with each plane TR*n_b/8 bytes (row-major, weight k of a row = bit k%8 of
+// byte k/8, as in layout.cpp:58-61).  Units are ordered row-tile-major
+// (rt, bc).  The bytes are exactly the SFMPPKD1 bytes; only their order
+// changes (when TR == m_b the layout is byte-identical to SFMPPKD1's).
+// unit_desc[u] = byte offset of unit u (bits 0-47) | bit-width (bits 48-51).
+struct UnitGeom {
+    const uint8_t* payload;
+    const uint64_t* unit_desc;
+    uint32_t TR, n_b, BC;
 };
 
-// Device-resident model.  The block payload region of the SFMPPKD1 stream is
-// uploaded verbatim (scales | zeros | planes per block, block-row-major).
 struct DevModel {
     int device = 0;
     int num_sms = 148;
     uint64_t rows = 0, cols = 0;  // rows = rows held by this (shard) model
     uint32_t m_b = 0, n_b = 0;
     int floor_bits = 0, ceil_bits = 0, mode = 0;
-    uint64_t K = 0;
+    uint64_t K = 0;  // blocks held
     uint64_t blocks_high = 0;
     double avg_bits = 0;
     uint64_t payload_bytes = 0;
     uint64_t device_bytes = 0;
-    std::vector<uint8_t> h_bits;
-    std::vector<uint64_t> h_off;  // relative to payload start
+
+    uint32_t TR = 0;          // unit rows
+    uint32_t RT = 0, BC = 0;  // row tiles, block columns
+    std::vector<uint64_t> h_unit_desc;
 
     uint8_t* d_payload = nullptr;
-    uint64_t* d_off = nullptr;
-    uint8_t* d_bits = nullptr;
+    uint64_t* d_unit_desc = nullptr;
     uint32_t* d_col_perm = nullptr;  // always present (identity when mode lacks col)
     uint32_t* d_out_map = nullptr;   // local reordered row -> column index of y row
     uint64_t out_rows = 0;           // stride of a y row
@@ -56,25 +55,29 @@ struct DevModel {
     uint64_t shard_rows = 0;
     uint32_t* d_gather_map = nullptr;  // [num_shards*shard_rows] -> original row (or ~0 pad)
 
-    GemvSchedule gemv;
     bool gemv_ok = false;
     bool gemm_ok = false;
 
     float* d_ws = nullptr;  // default workspace
     size_t ws_bytes = 0;
+    // staging for the host-buffer entry point (sfmp_gemm_host)
+    std::mutex host_mu;
+    uint8_t* d_host_stage = nullptr;
+    size_t host_stage_bytes = 0;
     std::vector<void*> allocs;
+
+    UnitGeom geom() const { return UnitGeom{d_payload, d_unit_desc, TR, n_b, BC}; }
 };
 
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, float* y,
                         float* ws, cudaStream_t st);
 size_t gemv_workspace_bytes(const DevModel& m, int M);
-int gemv_ctas_per_sm();
+int gemv_ctas_per_sm(int NT);
 
 cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
                            cudaStream_t st);
-cudaError_t launch_dequant(const DevModel& m, const uint32_t* d_row_orig, float* w,
-                           cudaStream_t st);
+cudaError_t launch_dequant(const DevModel& m, float* w, cudaStream_t st);
 cudaError_t launch_unpack(const DevModel& m, uint8_t* codes, cudaStream_t st);
 cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, int64_t M,
                                       float* y, cudaStream_t st);
