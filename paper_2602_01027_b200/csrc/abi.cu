@@ -288,6 +288,16 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
     if ((s = dev_upload(*d, &d->d_col_perm, cp.data(), cp.size() * 4))) return s;
     if ((s = dev_upload(*d, &d->d_out_map, out_map.data(), out_map.size() * 4))) return s;
     if ((s = build_gemv_schedule(*d))) return s;
+    {
+        std::vector<uint8_t> wl;
+        std::vector<uint64_t> woff;
+        if (sfmpk::build_gemm_layout(*d, payload, out_map, wl, woff)) {
+            if ((s = dev_upload(*d, &d->d_gl, wl.data(), wl.size()))) return s;
+            if ((s = dev_upload(*d, &d->d_gl_off, woff.data(), woff.size() * 8))) return s;
+            d->gl_row_tiles = (d->out_rows + 255) / 256 * 2;
+            d->gl_bytes = wl.size();
+        }
+    }
     d->gemm_ok = sfmpk::gemm_supported(*d);
     const size_t ws = d->gemv_ok ? sfmpk::gemv_workspace_bytes(*d, 16) : 0;
     if (ws) {

@@ -55,6 +55,13 @@ struct DevModel {
     uint64_t shard_rows = 0;
     uint32_t* d_gather_map = nullptr;  // [num_shards*shard_rows] -> original row (or ~0 pad)
 
+    // K2 row-tile layout (gemm_tcgen05.cu): units of 128 output rows x 128
+    // reordered columns, per-row bit-widths, gl_row_tiles (even) x cols/128.
+    uint8_t* d_gl = nullptr;
+    uint64_t* d_gl_off = nullptr;
+    uint64_t gl_row_tiles = 0;
+    uint64_t gl_bytes = 0;
+
     bool gemv_ok = false;
     bool gemm_ok = false;
 
@@ -84,6 +91,8 @@ cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, 
 
 // K2 prefill GEMM (tcgen05)
 bool gemm_supported(const DevModel& m);
+bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const std::vector<uint32_t>& out_map,
+                       std::vector<uint8_t>& wl, std::vector<uint64_t>& woff);
 size_t gemm_workspace_bytes(const DevModel& m, int64_t M);
 cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
                         void* ws, cudaStream_t st);
