@@ -294,8 +294,9 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
         if (sfmpk::build_gemm_layout(*d, payload, out_map, wl, woff)) {
             if ((s = dev_upload(*d, &d->d_gl, wl.data(), wl.size()))) return s;
             if ((s = dev_upload(*d, &d->d_gl_off, woff.data(), woff.size() * 8))) return s;
-            d->gl_row_tiles = (d->out_rows + 255) / 256 * 2;
             d->gl_bytes = wl.size();
+            const std::vector<uint32_t> xslot = sfmpk::gemm_slot_table(cp);
+            if ((s = dev_upload(*d, &d->d_xslot, xslot.data(), xslot.size() * 4))) return s;
         }
     }
     d->gemm_ok = sfmpk::gemm_supported(*d);

@@ -41,6 +41,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "ptx.cuh"
 #include "sfmp_internal.h"
@@ -51,14 +52,20 @@ namespace sfmpk {
 
 namespace {
 
-constexpr int kRowsTile = 128;            // rows per layout tile (= MMA M)
 constexpr int kUnitHdr = 528;             // scales[128] | zeros[128] | highmask[4]
 constexpr int kPlaneBytes = 128 * 16;     // one plane of a unit
-constexpr int kThreads = 14 * 32;
-constexpr int kMaxN = 128;                // tokens per tile
+// Tile = 128 output rows (MMA M) x N <= 256 tokens (MMA N): a single
+// M=128,N=256,K=16 tcgen05.mma costs ~138 cycles vs ~118 for N<=128
+// (tools/mma_bench.cu, measured), so wide N is what reaches the tensor peak.
+constexpr int kDeqWarps = 8;              // dequant warps: 4 TMEM lane quarters x kKS K-splits
+constexpr int kKS = kDeqWarps / 4;        // K splits of a 128-column unit among dequant warps
+constexpr int kWords = 4 / kKS;           // 32-weight words per dequant thread per unit
+constexpr int kThreads = (6 + kDeqWarps) * 32;
+constexpr int kMaxN = 256;                // tokens per tile
 constexpr int kTmemCols = 512;
-constexpr int kAccCol = 0;                // accumulator rh at kAccCol + rh*128
-constexpr int kACol = 256;                // A buffer (ab, rh) at kACol + (ab*2+rh)*64
+constexpr int kAccCol = 0;                // accumulator: columns [0, N)
+constexpr int kACol = 256;                // A buffer ab at kACol + ab*64 (128 f16 of K per row)
+constexpr int kNA = 4;                    // A buffers
 constexpr int kSmemLimit = 227 * 1024;
 
 struct GemmParams {
@@ -66,19 +73,21 @@ struct GemmParams {
     const uint64_t* woff;    // [RT2*KC + 1] unit byte offsets
     const uint8_t* xs;       // [TT][KC][2][N][128 B] swizzled f16 X
     float* y;
-    int M, N, TT, KC, RP;    // tokens, tokens/tile, token tiles, 128-col chunks, row-tile pairs
+    int M, N, TT, KC, RT;    // tokens, tokens/tile, token tiles, 128-col chunks, row tiles
     uint64_t out_rows;
     int floor_bits, has_extra;
     int SX, SW;              // X / W ring stages
-    uint32_t stage_w, half_w;  // W stage bytes, offset of the bottom unit
+    int C;                   // cluster size: CTAs sharing (multicasting) one X tile
+    uint32_t stage_w;        // W stage bytes (one unit)
     uint32_t idesc;
+    int dbg;  // SFMP_GEMM_DEBUG bits: 1 skip dequant math, 2 skip MMAs, 4 skip y stores, 8 xprep only, 16 no xprep
 };
 
 // x[t][col_perm[...]] -> f16, in the K order of the unpacked A operand:
 // slot s of a 128-column chunk holds reordered column 32w + 4h + a + 16e
 // with w = s/32, p = s%32, j = p/2 = 4a + h, e = p%2 (unpack_word register
 // order: H[4a+h] = weights (4h+a, 4h+a+16) of the word, low half first).
-__device__ __forceinline__ int slot_col(int s) {
+__host__ __device__ __forceinline__ int slot_col(int s) {
     const int w = s >> 5, p = s & 31, j = p >> 1, e = p & 1;
     return 32 * w + 4 * (j & 3) + (j >> 2) + 16 * e;
 }
@@ -92,32 +101,73 @@ __device__ __forceinline__ float ldx(const void* x, size_t i) {
         return __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(x) + i));
 }
 
-// One CTA per (token tile, 128-column chunk): 2 atoms x N rows x 8 chunks of 16 B.
+// One CTA per token (grid-stride): the x row is staged in shared memory as
+// f16 with coalesced 16-byte loads, then every 16-byte chunk of the swizzled
+// B image is gathered from shared memory through the slot table xslot
+// (xslot[kc*128 + s] = col_perm[kc*128 + slot_col(s)], built at upload).
+// Tokens M..TT*N-1 of the last tile are written as zeros.
 template <sfmp_dtype DT>
-__global__ void __launch_bounds__(256) xprep_gemm_kernel(const void* x, const uint32_t* col_perm, uint8_t* xs,
-                                                         int M, int N, int KC, int cols) {
+__global__ void __launch_bounds__(256) xprep_gemm_kernel(const void* __restrict__ x, const uint32_t* __restrict__ xslot,
+                                                         uint8_t* __restrict__ xs, int M, int N, int KC, int cols,
+                                                         int Mpad) {
+    extern __shared__ __align__(16) __half xrow[];
     pdl_launch_dependents();
-    const int kc = blockIdx.x % KC, tt = blockIdx.x / KC;
-    uint8_t* dst = xs + (static_cast<size_t>(tt) * KC + kc) * 2 * N * 128;
-    const uint32_t* cp = col_perm + static_cast<size_t>(kc) * 128;
-    for (int c = threadIdx.x; c < 2 * N * 8; c += blockDim.x) {
-        const int a = c / (N * 8), rem = c - a * N * 8, r = rem >> 3, pc = rem & 7;
-        const int j = pc ^ (r & 7);  // logical 16-byte chunk stored at physical pc
-        const int t = tt * N + r;
-        uint32_t packed[4] = {0u, 0u, 0u, 0u};
+    for (int t = blockIdx.x; t < Mpad; t += gridDim.x) {
+        const int tt = t / N, r = t - tt * N;
+        uint8_t* dst = xs + static_cast<size_t>(tt) * KC * 2 * N * 128 + r * 128;
         if (t < M) {
-            const size_t row = static_cast<size_t>(t) * cols;
+            if constexpr (DT == SFMP_F32) {
+                const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(x) + static_cast<size_t>(t) * cols);
+                for (int i = threadIdx.x; i < cols / 4; i += blockDim.x) {
+                    const float4 v = __ldg(src + i);
+                    uint2 h;
+                    h.x = h2_as_u32(__floats2half2_rn(v.x, v.y));
+                    h.y = h2_as_u32(__floats2half2_rn(v.z, v.w));
+                    reinterpret_cast<uint2*>(xrow)[i] = h;
+                }
+            } else {
+                const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + static_cast<size_t>(t) * cols);
+                for (int i = threadIdx.x; i < cols / 8; i += blockDim.x) {
+                    uint4 v = __ldg(src + i);
+                    if constexpr (DT == SFMP_BF16) {
+                        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-                const int s = 64 * a + 8 * j + e;
-                const float v0 = ldx<DT>(x, row + __ldg(cp + slot_col(s)));
-                const float v1 = ldx<DT>(x, row + __ldg(cp + slot_col(s + 1)));
-                packed[e >> 1] = h2_as_u32(__floats2half2_rn(v0, v1));
+                        for (int e = 0; e < 4; ++e) {
+                            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
+                            w[e] = h2_as_u32(__float22half2_rn(__bfloat1622float2(b)));
+                        }
+                    }
+                    reinterpret_cast<uint4*>(xrow)[i] = v;
+                }
             }
+            __syncthreads();
         }
-        *reinterpret_cast<uint4*>(dst + static_cast<size_t>(a) * N * 128 + r * 128 + pc * 16) =
-            make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        for (int c = threadIdx.x; c < KC * 16; c += blockDim.x) {
+            const int kc = c >> 4, a = (c >> 3) & 1, j = c & 7;
+            uint4 out = make_uint4(0u, 0u, 0u, 0u);
+            if (t < M) {
+                const uint4* ip = reinterpret_cast<const uint4*>(xslot + kc * 128 + 64 * a + 8 * j);
+                const uint4 i0 = __ldg(ip), i1 = __ldg(ip + 1);
+                const unsigned short* xr = reinterpret_cast<const unsigned short*>(xrow);
+                out.x = static_cast<uint32_t>(xr[i0.x]) | (static_cast<uint32_t>(xr[i0.y]) << 16);
+                out.y = static_cast<uint32_t>(xr[i0.z]) | (static_cast<uint32_t>(xr[i0.w]) << 16);
+                out.z = static_cast<uint32_t>(xr[i1.x]) | (static_cast<uint32_t>(xr[i1.y]) << 16);
+                out.w = static_cast<uint32_t>(xr[i1.z]) | (static_cast<uint32_t>(xr[i1.w]) << 16);
+            }
+            *reinterpret_cast<uint4*>(dst + (static_cast<size_t>(kc) * 2 + a) * N * 128 + ((j ^ (r & 7)) << 4)) = out;
+        }
+        __syncthreads();
     }
+}
+
+// Debug timeline (SFMP_GEMM_DEBUG & 32): CTAs 0/1, [kind][unit] globaltimer:
+// 0 dequant wfull seen, 1 dequant math done, 2 aempty seen, 3 afull arrived,
+// 4 MMA afull seen, 5 MMA xfull seen, 6 MMA issued+committed, 7 epilogue accfull seen (per tile).
+__device__ unsigned long long g_gemm_tl[2 * 8 * 256];
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 // Dequantise one 32-weight word of this thread's row into 16 f16x2.
@@ -138,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     // 1024-byte alignment for the swizzled X stages
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int SX = p.SX, SW = p.SW, N = p.N;
-    const uint32_t xstage = static_cast<uint32_t>(2 * N * 128);
+    const uint32_t xstage = static_cast<uint32_t>(N * 128);  // one 64-column swizzle atom of X
     uint8_t* xbuf = smem;
     uint8_t* wbuf = xbuf + static_cast<size_t>(SX) * xstage;
     uint64_t* bars = reinterpret_cast<uint64_t*>(wbuf + static_cast<size_t>(SW) * p.stage_w);
@@ -146,25 +196,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     uint64_t* xempty = xfull + SX;
     uint64_t* wfull = xempty + SX;
     uint64_t* wempty = wfull + SW;
-    uint64_t* afull = wempty + SW;   // [2]
-    uint64_t* aempty = afull + 2;    // [2]
-    uint64_t* accfull = aempty + 2;  // [1]
+    uint64_t* afull = wempty + SW;     // [kNA]
+    uint64_t* aempty = afull + kNA;    // [kNA]
+    uint64_t* accfull = aempty + kNA;  // [1]
     uint64_t* accempty = accfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
-    uint64_t* offs = accempty + 2;  // [2*KC + 1] unit offsets of the producer's current tile
+    uint64_t* offs = accempty + 2;  // [KC + 1] unit offsets of the producer's current row tile
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < SX; ++s) {
             mbar_init(&xfull[s], 1);
-            mbar_init(&xempty[s], 1);
+            mbar_init(&xempty[s], p.C);  // one MMA commit from every CTA of the cluster
         }
         for (int s = 0; s < SW; ++s) {
             mbar_init(&wfull[s], 1);
-            mbar_init(&wempty[s], 8);
+            mbar_init(&wempty[s], kDeqWarps);
         }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&afull[a], 8);
+        for (int a = 0; a < kNA; ++a) {
+            mbar_init(&afull[a], kDeqWarps);
             mbar_init(&aempty[a], 1);
         }
         mbar_init(accfull, 1);
@@ -178,168 +228,227 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     }
     tc_fence_before();
     __syncthreads();
+    if (p.C > 1) cluster_sync_all();  // peers' barriers are initialised before any multicast
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
-    const int ntiles = p.RP * p.TT;
+    // Work: cluster tiles ct = (row-tile group, token tile); CTA `rank` of a
+    // cluster takes row tile group*C + rank, all ranks walk the same (tt, kc)
+    // sequence so each X atom is fetched once and multicast to all of them.
+    const int C = p.C;
+    const int rank = C > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    const int cid = blockIdx.x / C, ncl = gridDim.x / C;
+    const int nct = (p.RT / C) * p.TT;
     const int KC = p.KC;
+    const uint16_t cmask = static_cast<uint16_t>((1u << C) - 1u);
 
     if (warp == 0) {
         // ---------------- producer ----------------
-        // The unit offsets of a tile's two row tiles are staged in shared
-        // memory by the whole warp, so lane 0 never waits on a global load
-        // between bulk copies.
+        // Unit offsets of the current row tile are staged in shared memory by
+        // the whole warp, so lane 0 never waits on a global load between copies.
         const uint64_t pol_w = policy_evict_first();
         int xs = 0, xph = 0, ws = 0, wph = 0;
         bool waited = false;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int rp = tile / p.TT, tt = tile - rp * p.TT;
-            const uint64_t* off0 = p.woff + static_cast<size_t>(2 * rp) * KC;
+        const uint32_t xslice = xstage / C;
+        for (int ct = cid; ct < nct; ct += ncl) {
+            const int rg = ct / p.TT, tt = ct - rg * p.TT, rt = rg * C + rank;
+            const uint64_t* off0 = p.woff + static_cast<size_t>(rt) * KC;
             __syncwarp();
-            for (int i = lane; i <= 2 * KC; i += 32) offs[i] = __ldg(off0 + i);
+            for (int i = lane; i <= KC; i += 32) offs[i] = __ldg(off0 + i);
             __syncwarp();
             if (lane == 0) {
                 for (int kc = 0; kc < KC; ++kc) {
                     // weights (independent of the X pre-pass)
                     mbar_wait(&wempty[ws], wph ^ 1);
-                    const uint64_t a0 = offs[kc], a1 = offs[kc + 1];
-                    const uint64_t b0 = offs[KC + kc], b1 = offs[KC + kc + 1];
-                    const uint32_t n0 = static_cast<uint32_t>(a1 - a0), n1 = static_cast<uint32_t>(b1 - b0);
-                    mbar_arrive_expect_tx(&wfull[ws], n0 + n1);
-                    uint8_t* wdst = wbuf + static_cast<size_t>(ws) * p.stage_w;
-                    bulk_g2s(wdst, p.wl + a0, n0, &wfull[ws], pol_w);
-                    bulk_g2s(wdst + p.half_w, p.wl + b0, n1, &wfull[ws], pol_w);
+                    const uint64_t a0 = offs[kc];
+                    const uint32_t n0 = static_cast<uint32_t>(offs[kc + 1] - a0);
+                    mbar_arrive_expect_tx(&wfull[ws], n0);
+                    bulk_g2s(wbuf + static_cast<size_t>(ws) * p.stage_w, p.wl + a0, n0, &wfull[ws], pol_w);
                     if (++ws == SW) { ws = 0; wph ^= 1; }
-                    // activations
+                    // activations: the two 64-column atoms of this chunk
                     if (!waited) {
                         pdl_wait();
                         waited = true;
                     }
-                    mbar_wait(&xempty[xs], xph ^ 1);
-                    mbar_arrive_expect_tx(&xfull[xs], xstage);
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                            smem_u32(xbuf + static_cast<size_t>(xs) * xstage)),
-                        "l"(p.xs + (static_cast<size_t>(tt) * KC + kc) * xstage), "r"(xstage), "r"(smem_u32(&xfull[xs]))
-                        : "memory");
-                    if (++xs == SX) { xs = 0; xph ^= 1; }
+                    for (int h = 0; h < 2; ++h) {
+                        // slot free in every CTA of the cluster (xempty counts C commits)
+                        mbar_wait(&xempty[xs], xph ^ 1);
+                        mbar_arrive_expect_tx(&xfull[xs], xstage);
+                        const uint32_t xdst = smem_u32(xbuf + static_cast<size_t>(xs) * xstage) + rank * xslice;
+                        const uint8_t* xsrc = p.xs + ((static_cast<size_t>(tt) * KC + kc) * 2 + h) * xstage + rank * xslice;
+                        if (C > 1) {
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+                                "[%0], [%1], %2, [%3], %4;" ::"r"(xdst),
+                                "l"(xsrc), "r"(xslice), "r"(smem_u32(&xfull[xs])), "h"(cmask)
+                                : "memory");
+                        } else {
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                                "[%3];" ::"r"(xdst),
+                                "l"(xsrc), "r"(xslice), "r"(smem_u32(&xfull[xs]))
+                                : "memory");
+                        }
+                        if (++xs == SX) { xs = 0; xph ^= 1; }
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
+        // ---------------- MMA issuer (one thread) ----------------
         if (lane == 0) {
             int xs = 0, xph = 0, ab = 0, aph = 0, accph = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            unsigned long long* tl = ((p.dbg & 32) && blockIdx.x < 2) ? g_gemm_tl + blockIdx.x * 8 * 256 : nullptr;
+            int tcount = 0;
+            for (int ct = cid; ct < nct; ct += ncl) {
                 mbar_wait(accempty, accph ^ 1);
                 tc_fence_after();
-                for (int kc = 0; kc < KC; ++kc) {
+                for (int kc = 0; kc < KC; ++kc, ++tcount) {
                     mbar_wait(&afull[ab], aph);
-                    mbar_wait(&xfull[xs], xph);
+                    if (tl) tl[4 * 256 + (tcount & 255)] = gtimer_ns();
                     tc_fence_after();
-                    const uint32_t xaddr = smem_u32(xbuf + static_cast<size_t>(xs) * xstage);
+                    for (int h = 0; h < 2; ++h) {
+                        mbar_wait(&xfull[xs], xph);
+                        if (tl && h == 0) tl[5 * 256 + (tcount & 255)] = gtimer_ns();
+                        tc_fence_after();
+                        const uint32_t xaddr = smem_u32(xbuf + static_cast<size_t>(xs) * xstage);
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const uint64_t bdesc = tc_desc_sw128(xaddr + (kk >> 2) * N * 128 + (kk & 3) * 32);
-#pragma unroll
-                        for (int rh = 0; rh < 2; ++rh)
-                            tc_mma_ts(tbase + kAccCol + rh * 128, tbase + kACol + (ab * 2 + rh) * 64 + kk * 8, bdesc,
-                                      p.idesc, (kc | kk) != 0);
+                        for (int kk = 0; kk < 4; ++kk) {
+                            if (p.dbg & 2) continue;
+                            tc_mma_ts(tbase + kAccCol, tbase + kACol + ab * 64 + (h * 4 + kk) * 8,
+                                      tc_desc_sw128(xaddr + kk * 32), p.idesc, (kc | h | kk) != 0);
+                        }
+                        if (C > 1) tc_commit_mc(&xempty[xs], cmask);  // frees the slot in every CTA's view
+                        else tc_commit(&xempty[xs]);
+                        if (++xs == SX) { xs = 0; xph ^= 1; }
                     }
                     tc_commit(&aempty[ab]);
-                    tc_commit(&xempty[xs]);
-                    if (++ab == 2) { ab = 0; aph ^= 1; }
-                    if (++xs == SX) { xs = 0; xph ^= 1; }
+                    if (tl) tl[6 * 256 + (tcount & 255)] = gtimer_ns();
+                    if (++ab == kNA) { ab = 0; aph ^= 1; }
                 }
                 tc_commit(accfull);
                 accph ^= 1;
             }
         }
     } else if (warp < 6) {
-        // ---------------- epilogue ----------------
+        // ---------------- epilogue: TMEM -> coalesced y rows ----------------
         const int q = warp & 3;
-        int accph = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int rp = tile / p.TT, tt = tile - rp * p.TT;
+        int accph = 0, ecount = 0;
+        for (int ct = cid; ct < nct; ct += ncl) {
+            const int rg = ct / p.TT, tt = ct - rg * p.TT, rt = rg * C + rank;
             mbar_wait(accfull, accph);
+            if ((p.dbg & 32) && blockIdx.x < 2 && q == 2 && lane == 0)
+                g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + (ecount++ & 255)] = gtimer_ns();
             accph ^= 1;
             tc_fence_after();
             const int t0 = tt * N;
+            const uint64_t row = static_cast<uint64_t>(rt) * 128 + q * 32 + lane;
+            const bool row_ok = row < p.out_rows;
 #pragma unroll 1
-            for (int rh = 0; rh < 2; ++rh) {
-                const uint64_t row = static_cast<uint64_t>(rp) * 256 + rh * 128 + q * 32 + lane;
-                const bool row_ok = row < p.out_rows;
-#pragma unroll 1
-                for (int c0 = 0; c0 < N; c0 += 32) {
-                    uint32_t v[32];
-                    tc_ld_x32(tbase + (static_cast<uint32_t>(q * 32) << 16) + kAccCol + rh * 128 + c0, v);
-                    tc_wait_ld();
-                    if (row_ok) {
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                uint32_t v[32];
+                tc_ld_x32(tbase + (static_cast<uint32_t>(q * 32) << 16) + kAccCol + c0, v);
+                tc_wait_ld();
+                if (c0 + 32 >= N) {
+                    // accumulator drained: the next tile's MMAs may start
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(accempty);
+                }
+                if (row_ok && !(p.dbg & 4)) {
+                    float* yp = p.y + static_cast<size_t>(t0 + c0) * p.out_rows + row;
+                    const int lim = min(32, min(N - c0, p.M - t0 - c0));
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int t = t0 + c0 + j;
-                            if (c0 + j < N && t < p.M) p.y[static_cast<size_t>(t) * p.out_rows + row] = __uint_as_float(v[j]);
-                        }
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        if (j < lim) yp[static_cast<size_t>(j) * p.out_rows] = __uint_as_float(v[j]);
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(accempty);
         }
     } else {
-        // ---------------- dequant ----------------
-        const int dw = warp - 6, q = warp & 3, rh = dw >> 2;
+        // ---------------- dequant: bit-planes -> f16 A operand in TMEM ----------------
+        const int dw = warp - 6, q = warp & 3, kh = dw >> 2;
         const int r = q * 32 + lane;  // row within the unit = TMEM lane
-        const int F = p.floor_bits;
+        const uint32_t woff = static_cast<uint32_t>(kh * kWords * 4);  // byte offset of this warp's words in a row
         int ws = 0, wph = 0, ab = 0, aph = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        unsigned long long* tl = ((p.dbg & 32) && blockIdx.x < 2 && dw == 0 && lane == 0)
+                                     ? g_gemm_tl + blockIdx.x * 8 * 256 : nullptr;
+        int tcount = 0;
+        for (int ct = cid; ct < nct; ct += ncl) {
             for (int kc = 0; kc < KC; ++kc) {
                 mbar_wait(&wfull[ws], wph);
-                const uint32_t u = smem_u32(wbuf + static_cast<size_t>(ws) * p.stage_w + rh * p.half_w);
+                if (tl) tl[0 * 256 + (tcount & 255)] = gtimer_ns();
+                const uint32_t u = smem_u32(wbuf + static_cast<size_t>(ws) * p.stage_w);
                 const __half2 s2 = __half2half2(__ushort_as_half(lds_u16(u + 2 * r)));
                 const __half2 z2 = __half2half2(__ushort_as_half(lds_u16(u + 256 + 2 * r)));
-                uint4 pl[NP];
+                uint32_t pl[NP][kWords];
+                auto ldrow = [&](int i, uint32_t addr) {
+                    if constexpr (kWords == 4) {
+                        const uint4 v = lds_v4(addr);
+                        pl[i][0] = v.x; pl[i][1] = v.y; pl[i][2] = v.z; pl[i][3] = v.w;
+                    } else if constexpr (kWords == 2) {
+                        const uint2 v = lds_v2(addr);
+                        pl[i][0] = v.x; pl[i][1] = v.y;
+                    } else {
+                        pl[i][0] = lds_u32(addr);
+                    }
+                };
                 if (p.has_extra) {
                     const uint4 mk = lds_v4(u + 512);
                     const uint32_t mw = q == 0 ? mk.x : q == 1 ? mk.y : q == 2 ? mk.z : mk.w;
                     const int before = (q > 0 ? __popc(mk.x) : 0) + (q > 1 ? __popc(mk.y) : 0) + (q > 2 ? __popc(mk.z) : 0);
                     const bool high = (mw >> lane) & 1u;
-                    const int rank = before + __popc(mw & ((1u << lane) - 1u));
+                    const int rank_h = before + __popc(mw & ((1u << lane) - 1u));
 #pragma unroll
-                    for (int i = 0; i < NP - 1; ++i) pl[i] = lds_v4(u + kUnitHdr + i * kPlaneBytes + r * 16);
-                    pl[NP - 1] = high ? lds_v4(u + kUnitHdr + (NP - 1) * kPlaneBytes + rank * 16) : make_uint4(0, 0, 0, 0);
+                    for (int i = 0; i < NP - 1; ++i) ldrow(i, u + kUnitHdr + i * kPlaneBytes + r * 16 + woff);
+                    if (high) {
+                        ldrow(NP - 1, u + kUnitHdr + (NP - 1) * kPlaneBytes + rank_h * 16 + woff);
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < kWords; ++w) pl[NP - 1][w] = 0u;
+                    }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < NP; ++i) pl[i] = lds_v4(u + kUnitHdr + i * kPlaneBytes + r * 16);
+                    for (int i = 0; i < NP; ++i) ldrow(i, u + kUnitHdr + i * kPlaneBytes + r * 16 + woff);
                 }
-                (void)F;
-                mbar_wait(&aempty[ab], aph ^ 1);
-                tc_fence_after();
-                const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + (ab * 2 + rh) * 64;
+                // all math before the TMEM buffer is needed: after aempty only
+                // the tcgen05.st stores sit on the MMA's critical path
+                uint32_t H[kWords][16];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
+                for (int w = 0; w < kWords; ++w) {
                     uint32_t pw[NP];
 #pragma unroll
-                    for (int i = 0; i < NP; ++i) pw[i] = w == 0 ? pl[i].x : w == 1 ? pl[i].y : w == 2 ? pl[i].z : pl[i].w;
-                    uint32_t H[16];
-                    dequant_word<NP>(pw, s2, z2, H);
-                    tc_st_x16(ta + w * 16, H);
+                    for (int i = 0; i < NP; ++i) pw[i] = pl[i][w];
+                    if (p.dbg & 1) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) H[w][j] = 0x3C003C00u;
+                    } else {
+                        dequant_word<NP>(pw, s2, z2, H[w]);
+                    }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&wempty[ws]);  // shared-memory reads of this stage are done
+                if (tl) tl[1 * 256 + (tcount & 255)] = gtimer_ns();
+                mbar_wait(&aempty[ab], aph ^ 1);
+                if (tl) tl[2 * 256 + (tcount & 255)] = gtimer_ns();
+                tc_fence_after();
+                const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + ab * 64 + kh * kWords * 16;
+#pragma unroll
+                for (int w = 0; w < kWords; ++w) tc_st_x16(ta + w * 16, H[w]);
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&afull[ab]);
-                    mbar_arrive(&wempty[ws]);
-                }
+                if (lane == 0) mbar_arrive(&afull[ab]);
+                if (tl) tl[3 * 256 + (tcount & 255)] = gtimer_ns();
+                ++tcount;
                 if (++ws == SW) { ws = 0; wph ^= 1; }
-                if (++ab == 2) { ab = 0; aph ^= 1; }
+                if (++ab == kNA) { ab = 0; aph ^= 1; }
             }
         }
     }
     tc_fence_before();
     __syncthreads();
+    // no CTA may leave while a peer can still multicast into it / arrive on it
+    if (p.C > 1) cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
         tc_dealloc(tbase, kTmemCols);
@@ -361,9 +470,10 @@ uint32_t unit_max_bytes(const DevModel& m) {
 }
 
 template <int NP>
-cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
+cudaError_t launch_np(const GemmParams& p, size_t smem, int nct, int num_sms, cudaStream_t st) {
     auto k = gemm_kernel<NP>;
     static int configured[64] = {0};
+    static int max_clusters[64][5] = {{0}};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
@@ -372,19 +482,41 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t s
         configured[dev] = 1;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(p.C);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
+    // persistent grid: as many clusters as can be co-resident (GPC packing
+    // may allow fewer than num_sms / C)
+    int& mc = max_clusters[dev < 64 ? dev : 0][p.C];
+    if (mc == 0) {
+        cfg.gridDim = dim3(p.C * (num_sms / p.C));
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = num_sms / p.C;
+        }
+        mc = n;
+    }
+    const int ncl = std::max(1, std::min(nct, mc));
+    cfg.gridDim = dim3(ncl * p.C);
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
 }  // namespace
+
+extern "C" int sfmp_debug_gemm_timeline(unsigned long long* host, size_t n) {
+    if (n > 2 * 8 * 256) n = 2 * 8 * 256;
+    return static_cast<int>(cudaMemcpyFromSymbol(host, g_gemm_tl, n * sizeof(unsigned long long)));
+}
 
 // ---------------------------------------------------------------------------
 // Upload-time row-tile layout (host).  For output column c of y (0..out_rows)
@@ -393,7 +525,8 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t s
 bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const std::vector<uint32_t>& out_map,
                        std::vector<uint8_t>& wl, std::vector<uint64_t>& woff) {
     if (d.n_b % 128 != 0 || d.cols % 128 != 0 || d.out_rows == 0) return false;
-    const uint64_t KC = d.cols / 128, RT2 = (d.out_rows + 255) / 256 * 2;
+    // row tiles padded to a multiple of 4 so clusters of up to 4 CTAs tile them
+    const uint64_t KC = d.cols / 128, RT2 = (d.out_rows + 511) / 512 * 4;
     const uint32_t TR = d.TR, nb8 = d.n_b / 8;
     const uint64_t plane_unit = static_cast<uint64_t>(TR) * nb8;
     std::vector<uint32_t> inv(RT2 * 128, 0xFFFFFFFFu);
@@ -431,12 +564,20 @@ bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const s
             wl.insert(wl.end(), extra.begin(), extra.end());
         }
     woff[RT2 * KC] = wl.size();
+    d.gl_row_tiles = RT2;
     (void)C;
     return true;
 }
 
+std::vector<uint32_t> gemm_slot_table(const std::vector<uint32_t>& col_perm) {
+    std::vector<uint32_t> t(col_perm.size());
+    for (size_t kc = 0; kc + 128 <= col_perm.size(); kc += 128)
+        for (int sl = 0; sl < 128; ++sl) t[kc + sl] = col_perm[kc + slot_col(sl)];
+    return t;
+}
+
 bool gemm_supported(const DevModel& m) {
-    return m.d_gl != nullptr && m.ceil_bits >= 1 && m.ceil_bits <= 8 && m.cols < (1ull << 31);
+    return m.d_gl != nullptr && m.d_xslot != nullptr && m.cols * 2 <= static_cast<uint64_t>(kSmemLimit) && m.ceil_bits >= 1 && m.ceil_bits <= 8 && m.cols < (1ull << 31);
 }
 
 size_t gemm_workspace_bytes(const DevModel& m, int64_t M) {
@@ -452,7 +593,7 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     p.M = static_cast<int>(M);
     p.TT = static_cast<int>((M + p.N - 1) / p.N);
     p.KC = static_cast<int>(m.cols / 128);
-    p.RP = static_cast<int>(m.gl_row_tiles / 2);
+    p.RT = static_cast<int>(m.gl_row_tiles);
     p.wl = m.d_gl;
     p.woff = m.d_gl_off;
     p.xs = static_cast<const uint8_t*>(ws);
@@ -461,40 +602,61 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     p.floor_bits = m.floor_bits;
     p.has_extra = m.ceil_bits > m.floor_bits;
     p.idesc = tc_idesc_f16(128, p.N);
-    const uint32_t ub = (unit_max_bytes(m) + 127) / 128 * 128;
-    p.half_w = ub;
-    p.stage_w = 2 * ub;
-    const uint32_t xstage = 2u * p.N * 128;
-    const size_t bar_bytes = 256 + (2 * static_cast<size_t>(p.KC) + 1) * 8;
-    // X ring first (up to 4 stages), the rest of shared memory for weights
-    p.SX = 4;
+    if (const char* e = getenv("SFMP_GEMM_DEBUG")) p.dbg = atoi(e);
+    p.stage_w = (unit_max_bytes(m) + 127) / 128 * 128;
+    const uint32_t xstage = static_cast<uint32_t>(p.N) * 128;
+    const size_t bar_bytes = 256 + (static_cast<size_t>(p.KC) + 1) * 8;
+    // W ring: 4 units; X ring: as many 64-column atoms as the rest holds (<= 8)
     const size_t avail = kSmemLimit - 1024 - bar_bytes;
-    while (p.SX > 2 && p.SX * xstage + 2 * p.stage_w > avail) --p.SX;
-    p.SW = static_cast<int>(std::min<size_t>(4, (avail - p.SX * xstage) / p.stage_w));
-    if (p.SW < 2) return cudaErrorInvalidConfiguration;
+    p.SW = 4;
+    p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
+    if (p.SX < 2) {
+        p.SW = 2;
+        p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
+    }
+    if (p.SX < 2) return cudaErrorInvalidConfiguration;
     const size_t smem = 1024 + p.SX * xstage + p.SW * p.stage_w + bar_bytes;
     // K4 (prefill flavour): gather + convert + swizzle X
-    const int xgrid = p.TT * p.KC;
     const int cols = static_cast<int>(m.cols);
+    const int Mpad = p.TT * p.N;
+    const int xgrid = std::min(Mpad, m.num_sms * 8);
+    const size_t xsm = static_cast<size_t>(cols) * 2;
     uint8_t* xs = static_cast<uint8_t*>(ws);
-    switch (dt) {
-        case SFMP_F32: xprep_gemm_kernel<SFMP_F32><<<xgrid, 256, 0, st>>>(x, m.d_col_perm, xs, p.M, p.N, p.KC, cols); break;
-        case SFMP_F16: xprep_gemm_kernel<SFMP_F16><<<xgrid, 256, 0, st>>>(x, m.d_col_perm, xs, p.M, p.N, p.KC, cols); break;
-        default: xprep_gemm_kernel<SFMP_BF16><<<xgrid, 256, 0, st>>>(x, m.d_col_perm, xs, p.M, p.N, p.KC, cols); break;
+    if (!(p.dbg & 16)) {
+        cudaError_t e0 = cudaSuccess;
+        switch (dt) {
+            case SFMP_F32:
+                e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                xprep_gemm_kernel<SFMP_F32><<<xgrid, 256, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                break;
+            case SFMP_F16:
+                e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                xprep_gemm_kernel<SFMP_F16><<<xgrid, 256, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                break;
+            default:
+                e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                xprep_gemm_kernel<SFMP_BF16><<<xgrid, 256, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                break;
+        }
+        if (e0 != cudaSuccess) return e0;
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int ntiles = p.RP * p.TT;
-    const int grid = std::max(1, std::min(ntiles, m.num_sms));
+    if (p.dbg & 8) return cudaSuccess;
+    p.C = 4;
+    if (const char* e = getenv("SFMP_GEMM_CLUSTER")) p.C = std::max(1, std::min(4, atoi(e)));
+    while (p.RT % p.C) p.C >>= 1;
+    const int nct = (p.RT / p.C) * p.TT;
+    const int S = m.num_sms;
     switch (m.ceil_bits) {
-        case 1: return launch_np<1>(p, smem, grid, st);
-        case 2: return launch_np<2>(p, smem, grid, st);
-        case 3: return launch_np<3>(p, smem, grid, st);
-        case 4: return launch_np<4>(p, smem, grid, st);
-        case 5: return launch_np<5>(p, smem, grid, st);
-        case 6: return launch_np<6>(p, smem, grid, st);
-        case 7: return launch_np<7>(p, smem, grid, st);
-        default: return launch_np<8>(p, smem, grid, st);
+        case 1: return launch_np<1>(p, smem, nct, S, st);
+        case 2: return launch_np<2>(p, smem, nct, S, st);
+        case 3: return launch_np<3>(p, smem, nct, S, st);
+        case 4: return launch_np<4>(p, smem, nct, S, st);
+        case 5: return launch_np<5>(p, smem, nct, S, st);
+        case 6: return launch_np<6>(p, smem, nct, S, st);
+        case 7: return launch_np<7>(p, smem, nct, S, st);
+        default: return launch_np<8>(p, smem, nct, S, st);
     }
 }
 

@@ -61,6 +61,7 @@ struct DevModel {
     uint64_t* d_gl_off = nullptr;
     uint64_t gl_row_tiles = 0;
     uint64_t gl_bytes = 0;
+    uint32_t* d_xslot = nullptr;  // [cols] col_perm in the K order of the GEMM B operand
 
     bool gemv_ok = false;
     bool gemm_ok = false;
@@ -91,6 +92,7 @@ cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, 
 
 // K2 prefill GEMM (tcgen05)
 bool gemm_supported(const DevModel& m);
+std::vector<uint32_t> gemm_slot_table(const std::vector<uint32_t>& col_perm);
 bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const std::vector<uint32_t>& out_map,
                        std::vector<uint8_t>& wl, std::vector<uint64_t>& woff);
 size_t gemm_workspace_bytes(const DevModel& m, int64_t M);

@@ -1,0 +1,43 @@
+"""GEMM per-unit timeline of CTA 0 (SFMP_GEMM_DEBUG=32): intervals between pipeline events (ns)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+os.environ["SFMP_GEMM_DEBUG"] = str(32 | int(os.environ.get("EXTRA_DBG", "0")))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2602_01027_b200 as sfmp  # noqa: E402
+from oracle.oracle import Port  # noqa: E402
+from synth import LLAMA_8B, activations, model_bytes  # noqa: E402
+
+proj = sys.argv[1] if len(sys.argv) > 1 else "k_proj"
+M = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+P = Port()
+rows, cols = LLAMA_8B[proj]
+dm = sfmp.DeviceModel(model_bytes(P, rows, cols, 3.25))
+x = torch.from_numpy(activations(P, M, cols)).cuda().to(torch.bfloat16)
+y = dm.gemm(x, path=sfmp.PATH_GEMM)
+torch.cuda.synchronize()
+y = dm.gemm(x, path=sfmp.PATH_GEMM)
+torch.cuda.synchronize()
+buf = np.zeros(2 * 8 * 256, np.uint64)
+sfmp.lib().sfmp_debug_gemm_timeline(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_size_t(buf.size))
+t = buf.reshape(2, 8, 256).astype(np.int64)[0]
+n = int((t[4] > 0).sum())
+t0 = t[0, 0]
+names = ["deq wfull", "deq math", "deq aempty", "deq afull", "mma afull", "mma xfull", "mma commit"]
+print(f"{proj} M={M}: {n} units on CTA 0; times rel. to first wfull (us)")
+for k in list(range(0, min(n, 6))) + list(range(max(6, n - 3), n)):
+    print(f"unit {k:3d}: " + " ".join(f"{nm}={(t[i, k] - t0) / 1e3:7.2f}" for i, nm in enumerate(names)))
+d = np.diff(t[4, :n]) / 1e3
+print(f"mma afull-to-afull interval us: median {np.median(d):.3f} p90 {np.percentile(d, 90):.3f}")
+for i, nm in enumerate(names[1:4], 1):
+    print(f"  {names[i-1]} -> {nm}: median {np.median((t[i, :n] - t[i-1, :n])) / 1e3:.3f} us")
+print(f"  deq afull -> mma afull: median {np.median(t[4, :n] - t[3, :n]) / 1e3:.3f} us")
+print(f"  mma commit(k) -> deq aempty(k+2): median {np.median(t[2, 2:n] - t[6, :n-2]) / 1e3:.3f} us")
+print(f"  mma afull -> mma commit: median {np.median(t[6, :n] - t[4, :n]) / 1e3:.3f} us")
+print("epilogue accfull:", (t[7][t[7] > 0] - t0) / 1e3)

@@ -1,0 +1,82 @@
+// mma_bench.cu -- tcgen05.mma issue/throughput probe (sm_100a).
+// One CTA per SM; warp 1 lane 0 issues `iters` MMAs (kind::f16, M=128,
+// N=n) back to back on fixed operands, A from TMEM (TS) or SMEM (SS),
+// commits to an mbarrier and waits.  Optional busy warps burn ALU.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/mma_bench tools/mma_bench.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#include "../paper_2602_01027_b200/csrc/tc.cuh"
+
+using namespace sfmpk;
+
+__global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int busy, unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;  // 1.0h
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        tc_alloc(smem_u32(slot), 512);
+        tc_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = *slot;
+    if (warp == 1 && lane == 0) {
+        const uint32_t idesc = tc_idesc_f16(128, n);
+        const uint64_t bdesc = tc_desc_sw128(smem_u32(smem));
+        const uint64_t adesc = tc_desc_sw128(smem_u32(smem + 32768));
+        unsigned long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint64_t b = bdesc + ((i & 3) * 2);  // +32 B per k-step
+            if (ss) tc_mma_ss(tb, adesc + ((i & 3) * 2), b, idesc, i > 0);
+            else tc_mma_ts(tb, tb + 256 + (i & 7) * 8, b, idesc, i > 0);
+        }
+        tc_commit(bar);
+        mbar_wait(bar, 0);
+        unsigned long long t1 = clock64();
+        if (blockIdx.x == 0) out[0] = t1 - t0;
+    } else if (warp >= 2 && warp < 2 + busy) {
+        float a = threadIdx.x, b = 1.0001f;
+        for (int i = 0; i < iters * 16; ++i) a = a * b + 0.5f;
+        if (a == 12345.f) out[1] = 1;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc_dealloc(tb, 512);
+}
+
+int main(int argc, char** argv) {
+    unsigned long long* d;
+    cudaMalloc(&d, 16);
+    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+    const int iters = 4096;
+    for (int ss = 0; ss < 2; ++ss)
+        for (int n : {64, 128, 256})
+            for (int busy : {0, 12}) {
+                bench<<<148, 512, 70000>>>(iters, n, ss, busy, d);
+                cudaEvent_t e0, e1;
+                cudaEventCreate(&e0);
+                cudaEventCreate(&e1);
+                cudaEventRecord(e0);
+                bench<<<148, 512, 70000>>>(iters, n, ss, busy, d);
+                cudaEventRecord(e1);
+                cudaError_t err = cudaDeviceSynchronize();
+                float ms = 0;
+                cudaEventElapsedTime(&ms, e0, e1);
+                unsigned long long cyc = 0;
+                cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
+                const double flops = 2.0 * 128 * n * 16 * iters * 148;
+                printf("%s N=%3d busy=%2d: %6.1f cyc/mma  %7.1f TFLOP/s  (%s)\n", ss ? "SS" : "TS", n, busy,
+                       double(cyc) / iters, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(err));
+            }
+    return 0;
+}
