@@ -10,12 +10,11 @@
 //    HBM (sfmp_internal.h), so a unit is one contiguous span fetched by ONE
 //    1-D bulk async copy (cp.async.bulk on the TMA engine) into a small
 //    mbarrier ring.
-//  * Each 128-row tile is processed by one thread-block cluster of C CTAs;
-//    rank r streams block columns [r*BC/C, (r+1)*BC/C).  The partial sums of
-//    the C ranks meet in distributed shared memory: every rank pushes its
-//    partials to the rank that owns the rows, one cluster barrier, the owner
-//    sums the C slots in rank order and stores un-permuted (deterministic
-//    split-K, no global round trips, no atomics).
+//  * Each 128-row tile is split over C CTAs (split-K); CTA s streams block
+//    columns [s*BC/C, (s+1)*BC/C), writes its f32 partial tile to the
+//    workspace and bumps the tile's counter; the last CTA to finish sums the
+//    C partials in split order and stores them un-permuted (deterministic,
+//    no float atomics) and re-zeroes the counter for the next call.
 //  * The activation gather x[t][col_perm[.]] runs once per call in a small
 //    pre-pass (xprep_kernel) that writes, per block column, an "activation
 //    record": f16 MMA B fragments + per-token column sums.  The GEMV is a
@@ -60,7 +59,9 @@ struct Params {
     float* y;
     int M;
     int BC;
-    int C;  // CTAs per row tile (= cluster size)
+    int C;  // CTAs per row tile (split-K ways)
+    float* part;         // [RT][C][16][128] f32 split-K partials
+    unsigned* counters;  // [RT] completion counters (zero between calls)
     int n_b;
     uint64_t out_rows;
     int stages;
@@ -217,12 +218,6 @@ __device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[N
     }
 }
 
-__host__ __device__ constexpr int recv_bytes(int C, int NT) {
-    return C > 1 ? (C * 8 * NT * ((kTR + C - 1) / C) * 4 + 127) / 128 * 128 : 0;
-}
-// First row of rank k's share of a 128-row tile split C ways.
-__device__ __forceinline__ int share_begin(int k, int C) { return k * kTR / C; }
-
 // LO = the model's floor bit-width: every unit has LO or LO+1 bits
 // (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
 // two unpack paths and its hot loop stays resident in the instruction cache.
@@ -235,21 +230,17 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     uint64_t* empty = full + S;
     uint8_t* zeros = smem + 256;                               // 256 B: B fragments of absent tokens
     uint32_t* sbits = reinterpret_cast<uint32_t*>(smem + 512);  // bit-width of the unit in stage s
-    uint32_t* omap = reinterpret_cast<uint32_t*>(smem + 640);   // out_map of the rows this rank stores
-    // cluster-reduction receive buffer recv[src_rank][t < 8*NT][RPM] (f32), a
-    // region of its own so early finishers never overwrite a live ring stage
-    uint8_t* recvbuf = smem + kHdrBytes;
-    uint8_t* wbase = recvbuf + recv_bytes(C, NT);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(smem + 640);    // "this CTA finishes the tile"
+    uint8_t* wbase = smem + kHdrBytes;
     uint8_t* xbase = wbase + static_cast<size_t>(S) * p.stage_w;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int dbg = p.debug_mode;
     if (threadIdx.x == 0) DBG_STAMP(0);
-    const int rank = C > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    const int rank = blockIdx.x % C;
     const int rt = blockIdx.x / C;
     const int bc0 = rank * p.BC / C, bc1 = (rank + 1) * p.BC / C;
     const int nunits = bc1 - bc0;
-    const int rb0 = share_begin(rank, C), rb1 = share_begin(rank + 1, C);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -315,13 +306,10 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         const int cw = warp - 1;
         const int g = lane >> 2, q = lane & 3;
         const int r0 = cw * 32 + g;  // rows r0 + {0, 8, 16, 24} of the tile
-        // output columns of the rows this CTA stores, fetched early (published to
-        // the cluster-reduction readers by the cluster barrier)
+        // output columns of this thread's rows, fetched early
         uint32_t my_map[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) my_map[r] = C == 1 ? __ldg(p.out_map + rt * kTR + r0 + 8 * r) : 0u;
-        for (int r = threadIdx.x - 32; C > 1 && r < rb1 - rb0; r += kThreads - 32)
-            omap[r] = __ldg(p.out_map + rt * kTR + rb0 + r);
         float yacc[2][NT][4];
 #pragma unroll
         for (int m = 0; m < 2; ++m)
@@ -405,45 +393,38 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                         if (t < p.M) p.y[t * p.out_rows + my_map[2 * m + (e >> 1)]] = yacc[m][nt][e];
                     }
         } else {
-            // push each partial to the shared memory of the rank that owns its row:
-            // recv[src_rank][t][row - owner_begin], stride RPM = ceil(128 / C)
-            const int RPM = (kTR + C - 1) / C;
-            const uint32_t recv_local = smem_u32(recvbuf);
+            // split-K partial tile [t][128 rows] of this CTA (coalesced rows)
+            float* part = p.part + (static_cast<size_t>(rt) * C + rank) * (16 * kTR);
 #pragma unroll
             for (int m = 0; m < 2; ++m)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int row = r0 + 16 * m + 8 * h;
-                    int owner = row * C / kTR;
-                    while (owner > 0 && share_begin(owner, C) > row) --owner;
-                    while (owner + 1 < C && share_begin(owner + 1, C) <= row) ++owner;
-                    const int lrow = row - share_begin(owner, C);
+                for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int t = nt * 8 + 2 * q + e;
-                            if (t < p.M) {
-                                const uint32_t off = static_cast<uint32_t>(((rank * 8 * NT + t) * RPM + lrow) * 4);
-                                st_dsmem_f32(mapa_shared(recv_local + off, static_cast<uint32_t>(owner)),
-                                             yacc[m][nt][2 * h + e]);
-                            }
-                        }
-                }
+                    for (int e = 0; e < 4; ++e) {
+                        const int t = nt * 8 + 2 * q + (e & 1);
+                        if (t < p.M) part[t * kTR + r0 + 16 * m + 8 * (e >> 1)] = yacc[m][nt][e];
+                    }
         }
     }
     if (C > 1) {
-        // Deterministic split-K across the cluster: after one cluster barrier
-        // every rank holds all C partials of its rows; sum them in rank order.
-        cluster_sync_all();
-        const int RPM = (kTR + C - 1) / C;
-        const float* recv = reinterpret_cast<const float*>(recvbuf);
-        const int nrow = rb1 - rb0, nvals = nrow * p.M;
-        for (int v = threadIdx.x; v < nvals; v += kThreads) {
-            const int t = v / nrow, lrow = v - t * nrow;
-            float acc = 0.f;
-            for (int r = 0; r < C; ++r) acc += recv[(r * 8 * NT + t) * RPM + lrow];
-            p.y[t * p.out_rows + omap[lrow]] = acc;
+        // Deterministic split-K: the last of the C CTAs of this row tile sums
+        // the partials in split order and stores them un-permuted.
+        __syncthreads();  // every partial store of this CTA precedes the release below
+        if (threadIdx.x == 0) {
+            const unsigned old = atomic_add_acq_rel_gpu(p.counters + rt, 1u);
+            *flag = (old == static_cast<unsigned>(C - 1)) ? 1u : 0u;
+        }
+        __syncthreads();
+        if (*flag) {
+            __threadfence();
+            const float* part = p.part + static_cast<size_t>(rt) * C * (16 * kTR);
+            for (int v = threadIdx.x; v < p.M * kTR; v += kThreads) {
+                const int t = v / kTR, row = v - t * kTR;
+                float acc = 0.f;
+                for (int r = 0; r < C; ++r) acc += __ldcg(part + static_cast<size_t>(r) * (16 * kTR) + v);
+                p.y[t * p.out_rows + __ldg(p.out_map + rt * kTR + row)] = acc;
+            }
+            if (threadIdx.x == 0) p.counters[rt] = 0u;  // ready for the next call (stream-ordered)
         }
     }
     if (threadIdx.x == 0) DBG_STAMP(1);
@@ -481,28 +462,28 @@ template <sfmp_dtype DT>
 cudaError_t launch_t(const Params& p, const void* x, const uint32_t* col_perm, int cols, int grid, size_t smem,
                      int lo, cudaStream_t st) {
     // K4: activation records (normal launch: it overwrites the workspace the
-    // previous call may still read, so it must follow it in stream order).
+    // previous call may still read, and x may be that call's output, so it
+    // follows it in stream order).  Measured: chaining it programmatically
+    // lets the next GEMV's CTAs occupy slots early and slows both calls.
     const int NT = p.M > 8 ? 2 : 1;
     const int warps = p.BC * NT;
-    xprep_kernel<DT><<<(warps + 7) / 8, 256, 0, st>>>(x, col_perm, const_cast<uint8_t*>(p.xrec), p.M, cols,
-                                                      p.n_b, p.BC, p.rec_bytes, p.debug_mode);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    // K1: one cluster of C CTAs per 128-row tile, programmatic dependent of xprep
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    xprep_kernel<DT><<<(warps + 7) / 8, 256, 0, st>>>(x, col_perm, const_cast<uint8_t*>(p.xrec), p.M, cols, p.n_b,
+                                                      p.BC, p.rec_bytes, p.debug_mode);
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    // K1: C CTAs per 128-row tile, programmatic dependent of xprep
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = static_cast<unsigned>(p.C);
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
     const int CH = p.n_b / 128;
     if (NT == 1) return CH == 1 ? launch_nc<1, 1>(cfg, p, lo) : launch_nc<1, 2>(cfg, p, lo);
     return CH == 1 ? launch_nc<2, 1>(cfg, p, lo) : launch_nc<2, 2>(cfg, p, lo);
@@ -516,9 +497,17 @@ extern "C" int sfmp_debug_gemv_timeline(unsigned long long* host, size_t n) {
     return static_cast<int>(cudaMemcpyFromSymbol(host, g_dbg_timeline, n * sizeof(unsigned long long)));
 }
 
+// Workspace: activation records | split-K partials | completion counters.
+constexpr int kMaxSplit = 32;
+size_t gemv_rec_bytes(const DevModel& m) {
+    return (static_cast<size_t>(m.BC) * RecGeom{16}.bytes(static_cast<int>(m.n_b / 128)) + 255) / 256 * 256;
+}
+size_t gemv_part_bytes(const DevModel& m) {
+    return static_cast<size_t>(m.RT) * std::min<int>(kMaxSplit, m.BC) * 16 * kTR * 4;
+}
 size_t gemv_workspace_bytes(const DevModel& m, int M) {
     (void)M;
-    return static_cast<size_t>(m.BC) * RecGeom{16}.bytes(static_cast<int>(m.n_b / 128));
+    return gemv_rec_bytes(m) + gemv_part_bytes(m) + static_cast<size_t>(m.RT) * 4;
 }
 
 int gemv_ctas_per_sm(int NT) { return ctas_per_sm(NT); }
@@ -540,18 +529,21 @@ cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, 
         const char* dbg = getenv("SFMP_GEMV_DEBUG");
         p.debug_mode = dbg ? atoi(dbg) : 0;
     }
-    // cluster size: split the block columns of every 128-row tile C ways, as
-    // many ways as fit one wave of resident CTAs (C <= 8, portable clusters)
+    // split-K: the block columns of every 128-row tile go to C CTAs, as many
+    // as fill the resident slots while keeping >= 2 units per CTA
     const int RT = static_cast<int>(m.RT);
     const int slots = m.num_sms * ctas_per_sm(NT);
-    p.C = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({8, p.BC, slots / std::max(RT, 1)})));
-    if (const char* cs = getenv("SFMP_GEMV_SPLIT")) p.C = std::max(1, std::min({8, p.BC, atoi(cs)}));
+    const int cmax = std::min(kMaxSplit, p.BC);
+    p.C = std::max(1, std::min({cmax, std::max(1, p.BC / 2), slots / std::max(RT, 1)}));
+    if (const char* cs = getenv("SFMP_GEMV_SPLIT")) p.C = std::max(1, std::min(cmax, atoi(cs)));
+    p.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + gemv_rec_bytes(m));
+    p.counters = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(ws) + gemv_rec_bytes(m) + gemv_part_bytes(m));
     const int CH = static_cast<int>(m.n_b / 128);
     p.stage_w = static_cast<uint32_t>((4 * kTR + m.ceil_bits * kTR * (m.n_b / 8) + 127) / 128 * 128);
     p.rec_bytes = static_cast<uint32_t>(RecGeom{M}.bytes(CH));
     int max_stages = 4;
     if (const char* ss = getenv("SFMP_GEMV_STAGES")) max_stages = std::max(2, atoi(ss));
-    const int fixed = kHdrBytes + recv_bytes(p.C, NT);
+    const int fixed = kHdrBytes;
     const int stages = std::min<int>(max_stages, (smem_per_cta(NT) - fixed) / static_cast<int>(p.stage_w + p.rec_bytes));
     if (stages < 2) return cudaErrorInvalidConfiguration;
     p.stages = stages;
