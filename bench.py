@@ -196,6 +196,63 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# prefill leg (configs[2]): the 7 linears at M=2048 through K2 (tcgen05 GEMM)
+# ---------------------------------------------------------------------------
+def prefill_leg(sfmp, port, models, dev, stream, args):
+    import torch
+    from synth import errors
+    M = args.prefill_M
+    xs = {p: torch.from_numpy(port.gen_activation(M, SHAPES[p][1], 4000)).to(dev).to(torch.bfloat16)
+          for p in PROJS}
+    ys = {p: torch.empty(M, SHAPES[p][0], device=dev) for p in PROJS}
+    ws = {p: models[0][p].workspace(M, sfmp.PATH_GEMM) for p in PROJS}
+
+    def one(c, p):
+        models[c][p].gemm(xs[p], out=ys[p], path=sfmp.PATH_GEMM, workspace=ws[p])
+
+    # parity spot check (q_proj, 8 sampled tokens) against the oracle
+    one(0, "q_proj")
+    torch.cuda.synchronize()
+    sample = [0, 1, 777, 1024, 1500, 2000, M - 2, M - 1]
+    w = port.load(build_bytes(port, "q_proj")).dequantize()
+    ref = port.matmul(xs["q_proj"][sample].float().cpu().numpy(), w, threads=8)
+    par = errors(ys["q_proj"][sample].cpu().numpy(), ref)[0]
+    per = {}
+    hbm, tc, src = peaks()
+    for p in PROJS:
+        with torch.cuda.stream(stream):
+            for c in range(COPIES):
+                one(c, p)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for c in range(COPIES):
+                one(c, p)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(2, args.steps // 10)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(reps):
+                g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (reps * COPIES)
+        rows, cols = SHAPES[p]
+        per[p] = {"us": round(us, 2), "tflops": round(2.0 * M * rows * cols / us / 1e6, 1)}
+    tot_us = sum(v["us"] for v in per.values())
+    flops = sum(2.0 * M * SHAPES[p][0] * SHAPES[p][1] for p in PROJS)
+    ach = flops / tot_us / 1e6
+    return {"metric": "prefill GEMM us per decoder layer (7 linears)", "M": M, "value": round(tot_us, 1),
+            "unit": "us", "kernel": "K2 tcgen05 GEMM (gemm_kernel) + xprep_gemm_kernel",
+            "per_proj": per, "parity_max_rel_err_q_proj_sampled": round(par, 7),
+            "roofline": {"bound": "tensor", "achieved": round(ach, 1), "peak": tc, "unit": "TFLOP/s",
+                         "frac": round(ach / tc, 4), "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({src})",
+                         "note": "time includes the x gather/convert pre-pass"}}
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 def main():
@@ -207,6 +264,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--soak-ms", type=float, default=1500.0)
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--prefill-M", type=int, default=2048)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -410,6 +469,8 @@ def main():
         "gpu_launches": args.steps * launches_per_step,
         "clocks": clk,
     }
+    if world == 1 and not args.no_prefill:
+        out["prefill"] = prefill_leg(sfmp, port, models, dev, stream, args)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_sample(port, blobs)
     print(json.dumps(out), flush=True)

@@ -136,6 +136,12 @@ sfmp_status sfmp_model_create_from_parts(const sfmp_model_parts* parts, int devi
  * gather_map=NULL to query *shard_rows only. */
 sfmp_status sfmp_shard_plan(const uint8_t* bytes, size_t len, uint32_t num_shards,
                             uint32_t* gather_map, uint64_t* shard_rows);
+/* Host-only: the shard's block rows as a stand-alone SFMPPKD1 stream (rows in
+ * shard-local order, so the row permutation is dropped; col_perm kept).  Its
+ * gemv equals the shard's sfmp_gemm output without padding.  Pass out=NULL to
+ * query *out_len. */
+sfmp_status sfmp_shard_extract(const uint8_t* bytes, size_t len, uint32_t shard, uint32_t num_shards,
+                               uint8_t* out, size_t* out_len);
 sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device,
                                     uint32_t shard, uint32_t num_shards, sfmp_dev_model** out);
 sfmp_status sfmp_model_destroy(sfmp_dev_model* model);

@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "sfmp_model_create_from_parts", "sfmp_model_create_shard", "sfmp_model_destroy",
     "sfmp_model_get_info", "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
     "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered", "sfmp_shard_plan",
+    "sfmp_shard_extract",
 )
 
 
@@ -125,11 +126,12 @@ def lib() -> C.CDLL:
     L.sfmp_unpack_codes.argtypes = [vp, vp, vp]
     L.sfmp_unpermute_gathered.argtypes = [vp, vp, i64, vp, vp]
     L.sfmp_shard_plan.argtypes = [vp, sz, C.c_uint32, vp, C.POINTER(C.c_uint64)]
+    L.sfmp_shard_extract.argtypes = [vp, sz, C.c_uint32, C.c_uint32, vp, C.POINTER(C.c_size_t)]
     for name in ("sfmp_parse_header", "sfmp_block_offsets", "sfmp_model_create",
                  "sfmp_model_create_shard", "sfmp_model_destroy", "sfmp_model_get_info",
                  "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
                  "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered",
-                 "sfmp_shard_plan"):
+                 "sfmp_shard_plan", "sfmp_shard_extract"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -180,6 +182,26 @@ def shard_plan(data: bytes, num_shards: int):
     gmap = np.zeros(num_shards * sr.value, np.uint32)
     check(lib().sfmp_shard_plan(data, len(data), num_shards, gmap.ctypes.data, C.byref(sr)))
     return gmap.reshape(num_shards, sr.value), int(sr.value)
+
+
+def shard_extract(data: bytes, shard: int, num_shards: int) -> bytes:
+    """The shard's block rows as a stand-alone SFMPPKD1 stream (host only)."""
+    n = C.c_size_t(0)
+    check(lib().sfmp_shard_extract(data, len(data), shard, num_shards, None, C.byref(n)))
+    buf = (C.c_uint8 * n.value)()
+    check(lib().sfmp_shard_extract(data, len(data), shard, num_shards, buf, C.byref(n)))
+    return bytes(buf)
+
+
+def assemble_gathered(gathered: np.ndarray, gather_map: np.ndarray, rows: int) -> np.ndarray:
+    """Host mirror of sfmp_unpermute_gathered: gathered[G, M, SR] -> y[M, rows]."""
+    G, M, SR = gathered.shape
+    y = np.zeros((M, rows), gathered.dtype)
+    gm = gather_map.reshape(G * SR)
+    valid = gm != 0xFFFFFFFF
+    flat = gathered.transpose(1, 0, 2).reshape(M, G * SR)
+    y[:, gm[valid]] = flat[:, valid]
+    return y
 
 
 def _dtype_code(t) -> int:

@@ -475,6 +475,58 @@ sfmp_status sfmp_shard_plan(const uint8_t* bytes, size_t len, uint32_t num_shard
     return SFMP_OK;
 }
 
+sfmp_status sfmp_shard_extract(const uint8_t* bytes, size_t len, uint32_t shard, uint32_t num_shards, uint8_t* out,
+                               size_t* out_len) {
+    if (!out_len) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out_len");
+    if (num_shards < 1 || shard >= num_shards) return fail(SFMP_ERR_CONFIG, "bad shard index/count");
+    Parsed p;
+    sfmp_status s = parse(bytes, len, p);
+    if (s) return s;
+    std::vector<std::vector<uint64_t>> owned;
+    std::vector<uint32_t> gmap;
+    uint64_t SR = 0;
+    if ((s = shard_plan(p, num_shards, owned, gmap, SR))) return s;
+    const std::vector<uint64_t>& br = owned[shard];
+    const uint64_t BC = p.cols / p.n_b, rows = br.size() * p.m_b, K = br.size() * BC;
+    const uint8_t mode = static_cast<uint8_t>(p.mode & 2);  // local rows are in shard order
+    uint64_t need = 38 + (mode & 2 ? 4 * p.cols : 0) + 8 + K;
+    for (uint64_t b : br)
+        for (uint64_t bc = 0; bc < BC; ++bc) {
+            const uint64_t k = b * BC + bc;
+            need += (k + 1 < p.K ? p.off[k + 1] : p.payload_end) - p.off[k];
+        }
+    if (!out) {
+        *out_len = need;
+        return SFMP_OK;
+    }
+    if (*out_len < need) return fail(SFMP_ERR_SHAPE, "output buffer too small");
+    uint8_t* o = out;
+    auto put = [&](const void* src, size_t n) {
+        std::memcpy(o, src, n);
+        o += n;
+    };
+    const uint16_t ver = 1;
+    const uint32_t mb = p.m_b, nb = p.n_b;
+    const uint8_t hdr[4] = {static_cast<uint8_t>(p.floor_bits), static_cast<uint8_t>(p.ceil_bits), mode, 0};
+    put("SFMPPKD1", 8);
+    put(&ver, 2);
+    put(&rows, 8);
+    put(&p.cols, 8);
+    put(&mb, 4);
+    put(&nb, 4);
+    put(hdr, 4);
+    if (mode & 2) put(p.col_perm, p.cols * 4);
+    put(&K, 8);
+    for (uint64_t b : br) put(p.bits + b * BC, BC);
+    for (uint64_t b : br)
+        for (uint64_t bc = 0; bc < BC; ++bc) {
+            const uint64_t k = b * BC + bc;
+            put(bytes + p.off[k], (k + 1 < p.K ? p.off[k + 1] : p.payload_end) - p.off[k]);
+        }
+    *out_len = need;
+    return SFMP_OK;
+}
+
 sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device, uint32_t shard,
                                     uint32_t num_shards, sfmp_dev_model** out) {
     if (!out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out");
