@@ -265,6 +265,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--soak-ms", type=float, default=1500.0)
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-group", action="store_true", help="one launch per linear instead of per decoder layer")
     ap.add_argument("--prefill-M", type=int, default=2048)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -299,14 +300,23 @@ def main():
                 for p in PROJS for M in MS}
         yfull = {(p, M): torch.empty(M, SHAPES[p][0], device=dev) for p in PROJS for M in MS}
 
-    launches_per_step = len(MS) * len(PROJS) * (2 if world > 1 else 1)
+    grouped = not args.no_group
+    # launches of OUR kernels per step: grouped = (x pre-pass + GEMV) per M;
+    # per-linear = (x pre-pass + GEMV) per call; sharded adds the un-permute
+    launches_per_step = (len(MS) * 2 if grouped else len(MS) * len(PROJS) * 2) + \
+        (len(MS) * len(PROJS) if world > 1 else 0)
 
-    def step(i):
+    def step(i, group=grouped):
         for mi, M in enumerate(MS):
             c = (i * len(MS) + mi) % COPIES
-            for p in PROJS:
-                models[c][p].gemm(xs[(p, M)], out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
-                if world > 1:
+            if group:
+                sfmp.gemm_grouped([models[c][p] for p in PROJS], [xs[(p, M)] for p in PROJS],
+                                  outs=[ys[(p, M)] for p in PROJS], workspaces=[ws[p] for p in PROJS])
+            else:
+                for p in PROJS:
+                    models[c][p].gemm(xs[(p, M)], out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
+            if world > 1:
+                for p in PROJS:
                     dist.all_gather_into_tensor(gath[(p, M)], ys[(p, M)])
                     models[c][p].unpermute_gathered(gath[(p, M)], M, out=yfull[(p, M)])
 
@@ -379,6 +389,30 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
 
+    # ---- secondary: the same step with one launch per linear (no grouping) ----
+    ungrouped_ms = None
+    if world == 1 and grouped and use_graph:
+        with torch.cuda.stream(stream):
+            step(0, group=False)
+        torch.cuda.synchronize()
+        ug = []
+        for i in range(COPIES):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(i, group=False)
+            ug.append(g)
+        reps = max(COPIES, args.steps // 2)
+        u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            for i in range(3):
+                ug[i % COPIES].replay()
+            u0.record(stream)
+            for i in range(reps):
+                ug[i % COPIES].replay()
+            u1.record(stream)
+        torch.cuda.synchronize()
+        ungrouped_ms = u0.elapsed_time(u1) / reps
+
     # ---- e2e: the public host-buffer API (sfmp_gemm_host), pinned host memory ----
     hx = {(p, M): torch.from_numpy(port.gen_activation(M, SHAPES[p][1], 3000 + M)).pin_memory()
           for p in PROJS for M in MS}
@@ -386,9 +420,20 @@ def main():
     h2d = sum(M * SHAPES[p][1] * 4 for p in PROJS for M in MS)
     d2h = sum(M * SHAPES[p][0] * 4 for p in PROJS for M in MS)
 
+    dx = {(p, M): torch.empty(M, SHAPES[p][1], device=dev) for p in PROJS for M in MS}
+
     def e2e_step(i):
         for mi, M in enumerate(MS):
             c = (i * len(MS) + mi) % COPIES
+            if world == 1 and grouped:
+                # public Python API: pinned host x -> device, grouped GEMM, y -> pinned host
+                for p in PROJS:
+                    dx[(p, M)].copy_(hx[(p, M)], non_blocking=True)
+                sfmp.gemm_grouped([models[c][p] for p in PROJS], [dx[(p, M)] for p in PROJS],
+                                  outs=[ys[(p, M)] for p in PROJS], workspaces=[ws[p] for p in PROJS])
+                for p in PROJS:
+                    hy[(p, M)].copy_(ys[(p, M)], non_blocking=True)
+                continue
             for p in PROJS:
                 if world == 1:
                     sfmp.check(sfmp.lib().sfmp_gemm_host(
@@ -452,7 +497,10 @@ def main():
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16", "data": "synthetic",
         "config": {"workload": WORKLOAD, "avg_code_bits": AVG_BITS, "M": MS,
-                   "projections": PROJS, "kernel": "K1 decode GEMV (gemv_kernel)",
+                   "projections": PROJS, "kernel": "K1 decode GEMV (gemv_kernel) + x pre-pass (xprep_kernel)",
+                   "launch_grouping": ("the 7 linears of one M share one pre-pass + one GEMV launch "
+                                       "(sfmp_gemm_grouped)") if grouped else "one launch per linear",
+                   "ungrouped_step_us": round(ungrouped_ms * 1e3, 2) if ungrouped_ms else None,
                    "l2": f"inputs larger than L2: {COPIES} rotating device copies of the layer "
                          f"({sum(i['payload_bytes'] for i in infos.values()) * COPIES / 1e6:.0f} MB)",
                    "cuda_graph": use_graph,

@@ -160,6 +160,15 @@ sfmp_status sfmp_gemm(const sfmp_dev_model* model, const void* x, sfmp_dtype dty
 sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype,
                          int64_t M, float* y, void* workspace, size_t workspace_bytes,
                          sfmp_path path, void* stream);
+/* Several independent linears (e.g. the q/k/v/o/gate/up/down of a decoder
+ * layer, each with its own x) in one call.  For M <= 16 consecutive models
+ * with the same n_b and floor bits share ONE activation pre-pass and ONE GEMV
+ * launch, so launch and first-byte latencies are paid once per group; other
+ * cases run model by model.  workspaces[i] as for sfmp_gemm on models[i]
+ * (required for the decode path); workspace_bytes may be NULL. */
+sfmp_status sfmp_gemm_grouped(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                              int64_t M, float* const* ys, void* const* workspaces, const size_t* workspace_bytes,
+                              int count, void* stream);
 /* Host-buffer convenience with the reference's calling convention: x and y
  * are HOST arrays; copies, kernel and synchronisation happen inside. */
 sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M,

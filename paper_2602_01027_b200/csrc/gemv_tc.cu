@@ -44,30 +44,52 @@ namespace sfmpk {
 namespace {
 
 constexpr int kTR = 128;  // rows per unit
-constexpr int kNCW = 4;   // compute warps (32 rows = 2 m16 tiles each)
+constexpr int kMT = 1;            // m16 tiles (16 rows each) per compute warp
+constexpr int kNCW = 8 / kMT;     // compute warps per 128-row tile
 constexpr int kThreads = 32 * (1 + kNCW);
 constexpr int kHdrBytes = 1280;  // barriers | zeros | stage bit-widths | out_map
 // resident CTAs per SM: 4 for M<=8 (NT=1), 3 for M<=16 (NT=2, more registers)
-__host__ __device__ constexpr int ctas_per_sm(int NT) { return NT == 1 ? 4 : 3; }
-__host__ __device__ constexpr int smem_per_cta(int NT) { return NT == 1 ? 56 * 1024 : 75 * 1024; }
+__host__ __device__ constexpr int ctas_per_sm(int NT) { return kMT == 2 ? (NT == 1 ? 4 : 3) : (NT == 1 ? 3 : 2); }
+__host__ __device__ constexpr int smem_per_cta(int NT) { return (225 * 1024) / ctas_per_sm(NT); }
 
-struct Params {
+// One linear of a (possibly grouped) launch: independent matrices -- e.g. the
+// seven linears of a decoder layer -- share one launch so the fixed per-call
+// latencies (launch, first HBM bytes, split-K tail) are paid once.
+constexpr int kMaxLin = 16;
+struct Lin {
     const uint8_t* payload;
     const uint64_t* unit_desc;  // [RT*BC] row-tile-major
     const uint32_t* out_map;
-    const uint8_t* xrec;  // [BC] activation records of rec_bytes (xprep_kernel)
+    const uint8_t* xrec;        // [BC] activation records of rec_bytes (xprep_kernel)
     float* y;
-    int M;
-    int BC;
-    int C;  // CTAs per row tile (split-K ways)
-    float* part;         // [RT][C][16][128] f32 split-K partials
-    unsigned* counters;  // [RT] completion counters (zero between calls)
-    int n_b;
+    float* part;                // [RT][C][16][128] f32 split-K partials
+    unsigned* counters;         // [RT] completion counters (zero between calls)
     uint64_t out_rows;
+    int BC;
+    int C;                      // CTAs per row tile (split-K ways)
+    int cta0;                   // first CTA of this linear in the grid
+};
+struct Params {
+    Lin lin[kMaxLin];
+    int nlin;
+    int M;
+    int n_b;
     int stages;
     uint32_t stage_w;    // bytes per weight stage (smem)
     uint32_t rec_bytes;  // bytes per activation record (smem and global)
     int debug_mode;      // 0 normal; 5 timeline stamps
+};
+struct XLin {
+    const void* x;
+    const uint32_t* col_perm;
+    uint8_t* xrec;
+    int BC, cols, warp0;
+};
+struct XParams {
+    XLin lin[kMaxLin];
+    int nlin, M, n_b;
+    uint32_t rec_bytes;
+    int dbg;
 };
 
 // Activation record of one block column (n_b columns), for M tokens:
@@ -127,13 +149,23 @@ __device__ __forceinline__ float load_x(const void* x, size_t i) {
 // bias.  One warp per (block column, n-tile); lane (n,q) owns token nt*8+n
 // and k-slots 32q + 4h + a (+16) of each 128-column chunk.
 template <sfmp_dtype DT>
-__global__ void __launch_bounds__(256) xprep_kernel(const void* x, const uint32_t* col_perm, uint8_t* xrec,
-                                                    int M, int cols, int n_b, int BC, uint32_t rec_bytes, int dbg) {
+__global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     pdl_launch_dependents();  // let the GEMV start streaming weights right away
+    const int dbg = xp.dbg;
     if (blockIdx.x == 0 && threadIdx.x == 0) DBG_KSTAMP(100);
+    const int M = xp.M, n_b = xp.n_b;
+    const uint32_t rec_bytes = xp.rec_bytes;
     const RecGeom G{M};
     const int NT = G.nt_count();
-    const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    int li = 0;
+    while (li + 1 < xp.nlin && w >= xp.lin[li + 1].warp0) ++li;
+    const XLin& XL = xp.lin[li];
+    w -= XL.warp0;
+    const int BC = XL.BC, cols = XL.cols;
+    const void* x = XL.x;
+    const uint32_t* col_perm = XL.col_perm;
+    uint8_t* xrec = XL.xrec;
     if (w >= BC * NT) return;
     const int bc = w / NT, nt = w - bc * NT;
     const int lane = threadIdx.x & 31, q = lane & 3, n = lane >> 2;
@@ -194,26 +226,27 @@ __global__ void __launch_bounds__(256) xprep_kernel(const void* x, const uint32_
 // 32-bit shared addresses; all other offsets are compile-time immediates.
 template <int B, int NT, int CH>
 __device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[NT], int chunk_bytes, int c,
-                                           float (&cacc)[4][NT][4]) {
+                                           float (&cacc)[2 * kMT][NT][4]) {
     constexpr int NB8 = CH * 16;   // bytes of one row of one plane
     constexpr int PS = kTR * NB8;  // bytes of one plane of the unit
-    // rows r0, r0+8 (m-tile 0) and r0+16, r0+24 (m-tile 1)
-    uint32_t p[4][B];
+    // rows r0 + 8*r: (r0, r0+8) is m-tile 0, (r0+16, r0+24) m-tile 1
+    uint32_t p[2 * kMT][B];
 #pragma unroll
     for (int i = 0; i < B; ++i)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) p[r][i] = lds_u32(prow + i * PS + r * 8 * NB8 + c * 16);
-    uint32_t A[4][16];
+        for (int r = 0; r < 2 * kMT; ++r) p[r][i] = lds_u32(prow + i * PS + r * 8 * NB8 + c * 16);
+    uint32_t A[2 * kMT][16];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) unpack_word<B>(p[r], A[r]);
+    for (int r = 0; r < 2 * kMT; ++r) unpack_word<B>(p[r], A[r]);
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             const uint2 b = lds_v2(xb[nt] + c * chunk_bytes + s * 32);
-            mma_16816(cacc[s & 1][nt], A[0][2 * s], A[1][2 * s], A[0][2 * s + 1], A[1][2 * s + 1], b.x, b.y);
-            mma_16816(cacc[2 + (s & 1)][nt], A[2][2 * s], A[3][2 * s], A[2][2 * s + 1], A[3][2 * s + 1], b.x,
-                      b.y);
+#pragma unroll
+            for (int m = 0; m < kMT; ++m)
+                mma_16816(cacc[2 * m + (s & 1)][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
+                          A[2 * m + 1][2 * s + 1], b.x, b.y);
         }
     }
 }
@@ -225,7 +258,10 @@ template <int NT, int CH, int LO>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const Params p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
-    const int C = p.C;
+    int li = 0;
+    while (li + 1 < p.nlin && static_cast<int>(blockIdx.x) >= p.lin[li + 1].cta0) ++li;
+    const Lin& L = p.lin[li];
+    const int C = L.C;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
     uint8_t* zeros = smem + 256;                               // 256 B: B fragments of absent tokens
@@ -237,9 +273,10 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int dbg = p.debug_mode;
     if (threadIdx.x == 0) DBG_STAMP(0);
-    const int rank = blockIdx.x % C;
-    const int rt = blockIdx.x / C;
-    const int bc0 = rank * p.BC / C, bc1 = (rank + 1) * p.BC / C;
+    const int lcta = static_cast<int>(blockIdx.x) - L.cta0;
+    const int rank = lcta % C;
+    const int rt = lcta / C;
+    const int bc0 = rank * L.BC / C, bc1 = (rank + 1) * L.BC / C;
     const int nunits = bc1 - bc0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -254,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 
     constexpr int nb8 = CH * 16;
     const RecGeom G{p.M};
-    const uint64_t* gdesc = p.unit_desc + static_cast<size_t>(rt) * p.BC + bc0;
+    const uint64_t* gdesc = L.unit_desc + static_cast<size_t>(rt) * L.BC + bc0;
 
     if (warp == 0) {
         // ---------------- producer: one bulk copy per unit (+ its activation record) ----
@@ -267,14 +304,14 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 DBG_STAMP(2 + 3 * i);
                 const uint32_t wbytes = 4 * kTR + bits * pbytes;
                 mbar_arrive_expect_tx(&full[s], wbytes + p.rec_bytes);
-                bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, p.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
+                bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
                          &full[s], pol);
             };
             auto issue_x = [&](int s, int bc_) {
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         smem_u32(xbase + static_cast<size_t>(s) * p.rec_bytes)),
-                    "l"(p.xrec + static_cast<size_t>(bc_) * p.rec_bytes), "r"(p.rec_bytes), "r"(smem_u32(&full[s]))
+                    "l"(L.xrec + static_cast<size_t>(bc_) * p.rec_bytes), "r"(p.rec_bytes), "r"(smem_u32(&full[s]))
                     : "memory");
             };
             const int pre = nunits < S ? nunits : S;
@@ -305,14 +342,14 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         // ---------------- compute warps ------------------------------------------
         const int cw = warp - 1;
         const int g = lane >> 2, q = lane & 3;
-        const int r0 = cw * 32 + g;  // rows r0 + {0, 8, 16, 24} of the tile
+        const int r0 = cw * 16 * kMT + g;  // rows r0 + 8*r of the tile
         // output columns of this thread's rows, fetched early
-        uint32_t my_map[4];
+        uint32_t my_map[2 * kMT];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) my_map[r] = C == 1 ? __ldg(p.out_map + rt * kTR + r0 + 8 * r) : 0u;
-        float yacc[2][NT][4];
+        for (int r = 0; r < 2 * kMT; ++r) my_map[r] = C == 1 ? __ldg(L.out_map + rt * kTR + r0 + 8 * r) : 0u;
+        float yacc[kMT][NT][4];
 #pragma unroll
-        for (int m = 0; m < 2; ++m)
+        for (int m = 0; m < kMT; ++m)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -340,9 +377,9 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + s * xstep[nt];
             const uint32_t prow = prow0 + s * stage_w;
-            float cacc[4][NT][4];
+            float cacc[2 * kMT][NT][4];
 #pragma unroll
-            for (int h = 0; h < 4; ++h)
+            for (int h = 0; h < 2 * kMT; ++h)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -360,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
             const uint32_t xg = xg0 + s * rec_bytes;
             const bool biased = bits <= 4;
 #pragma unroll
-            for (int m = 0; m < 2; ++m) {
+            for (int m = 0; m < kMT; ++m) {
                 const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
                 const float za = lds_h2f(sz + 2 * kTR + 32 * m), zb = lds_h2f(sz + 2 * kTR + 32 * m + 16);
 #pragma unroll
@@ -384,19 +421,19 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         if (C == 1) {
             // whole row tile in this CTA: un-permuted store straight to y
 #pragma unroll
-            for (int m = 0; m < 2; ++m)
+            for (int m = 0; m < kMT; ++m)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int t = nt * 8 + 2 * q + (e & 1);
-                        if (t < p.M) p.y[t * p.out_rows + my_map[2 * m + (e >> 1)]] = yacc[m][nt][e];
+                        if (t < p.M) L.y[t * L.out_rows + my_map[2 * m + (e >> 1)]] = yacc[m][nt][e];
                     }
         } else {
             // split-K partial tile [t][128 rows] of this CTA (coalesced rows)
-            float* part = p.part + (static_cast<size_t>(rt) * C + rank) * (16 * kTR);
+            float* part = L.part + (static_cast<size_t>(rt) * C + rank) * (16 * kTR);
 #pragma unroll
-            for (int m = 0; m < 2; ++m)
+            for (int m = 0; m < kMT; ++m)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -411,20 +448,20 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         // the partials in split order and stores them un-permuted.
         __syncthreads();  // every partial store of this CTA precedes the release below
         if (threadIdx.x == 0) {
-            const unsigned old = atomic_add_acq_rel_gpu(p.counters + rt, 1u);
+            const unsigned old = atomic_add_acq_rel_gpu(L.counters + rt, 1u);
             *flag = (old == static_cast<unsigned>(C - 1)) ? 1u : 0u;
         }
         __syncthreads();
         if (*flag) {
             __threadfence();
-            const float* part = p.part + static_cast<size_t>(rt) * C * (16 * kTR);
+            const float* part = L.part + static_cast<size_t>(rt) * C * (16 * kTR);
             for (int v = threadIdx.x; v < p.M * kTR; v += kThreads) {
                 const int t = v / kTR, row = v - t * kTR;
                 float acc = 0.f;
                 for (int r = 0; r < C; ++r) acc += __ldcg(part + static_cast<size_t>(r) * (16 * kTR) + v);
-                p.y[t * p.out_rows + __ldg(p.out_map + rt * kTR + row)] = acc;
+                L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = acc;
             }
-            if (threadIdx.x == 0) p.counters[rt] = 0u;  // ready for the next call (stream-ordered)
+            if (threadIdx.x == 0) L.counters[rt] = 0u;  // ready for the next call (stream-ordered)
         }
     }
     if (threadIdx.x == 0) DBG_STAMP(1);
@@ -459,24 +496,21 @@ cudaError_t launch_nc(cudaLaunchConfig_t& cfg, const Params& p, int lo) {
 }
 
 template <sfmp_dtype DT>
-cudaError_t launch_t(const Params& p, const void* x, const uint32_t* col_perm, int cols, int grid, size_t smem,
-                     int lo, cudaStream_t st) {
+cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int grid, size_t smem, int lo, cudaStream_t st) {
     // K4: activation records (normal launch: it overwrites the workspace the
     // previous call may still read, and x may be that call's output, so it
     // follows it in stream order).  Measured: chaining it programmatically
     // lets the next GEMV's CTAs occupy slots early and slows both calls.
     const int NT = p.M > 8 ? 2 : 1;
-    const int warps = p.BC * NT;
-    cudaLaunchAttribute pdl[1];
-    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    xprep_kernel<DT><<<(warps + 7) / 8, 256, 0, st>>>(x, col_perm, const_cast<uint8_t*>(p.xrec), p.M, cols, p.n_b,
-                                                      p.BC, p.rec_bytes, p.debug_mode);
+    xprep_kernel<DT><<<(xwarps + 7) / 8, 256, 0, st>>>(xp);
     {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    // K1: C CTAs per 128-row tile, programmatic dependent of xprep
+    // K1: C CTAs per 128-row tile of every linear, programmatic dependent of xprep
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -512,35 +546,65 @@ size_t gemv_workspace_bytes(const DevModel& m, int M) {
 
 int gemv_ctas_per_sm(int NT) { return ctas_per_sm(NT); }
 
-cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, float* y, float* ws,
-                        cudaStream_t st) {
+bool gemv_groupable(const DevModel& a, const DevModel& b) {
+    return a.gemv_ok && b.gemv_ok && a.n_b == b.n_b && a.floor_bits == b.floor_bits && a.device == b.device;
+}
+
+cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, float* const* ys, uint8_t* const* wss,
+                              int n, sfmp_dtype dt, int M, cudaStream_t st) {
+    if (n < 1 || n > kMaxLin) return cudaErrorInvalidValue;
+    const DevModel& m0 = *ms[0];
     const int NT = M > 8 ? 2 : 1;
+    const int CH = static_cast<int>(m0.n_b / 128);
     Params p{};
-    p.payload = m.d_payload;
-    p.unit_desc = m.d_unit_desc;
-    p.out_map = m.d_out_map;
-    p.y = y;
-    p.xrec = reinterpret_cast<const uint8_t*>(ws);
-    p.M = M;
-    p.BC = static_cast<int>(m.BC);
-    p.n_b = static_cast<int>(m.n_b);
-    p.out_rows = m.out_rows;
+    XParams xp{};
+    p.nlin = xp.nlin = n;
+    p.M = xp.M = M;
+    p.n_b = xp.n_b = static_cast<int>(m0.n_b);
+    p.rec_bytes = xp.rec_bytes = static_cast<uint32_t>(RecGeom{M}.bytes(CH));
     {
         const char* dbg = getenv("SFMP_GEMV_DEBUG");
-        p.debug_mode = dbg ? atoi(dbg) : 0;
+        p.debug_mode = xp.dbg = dbg ? atoi(dbg) : 0;
     }
-    // split-K: the block columns of every 128-row tile go to C CTAs, as many
-    // as fill the resident slots while keeping >= 2 units per CTA
-    const int RT = static_cast<int>(m.RT);
-    const int slots = m.num_sms * ctas_per_sm(NT);
-    const int cmax = std::min(kMaxSplit, p.BC);
-    p.C = std::max(1, std::min({cmax, std::max(1, p.BC / 2), slots / std::max(RT, 1)}));
-    if (const char* cs = getenv("SFMP_GEMV_SPLIT")) p.C = std::max(1, std::min(cmax, atoi(cs)));
-    p.part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + gemv_rec_bytes(m));
-    p.counters = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(ws) + gemv_rec_bytes(m) + gemv_part_bytes(m));
-    const int CH = static_cast<int>(m.n_b / 128);
-    p.stage_w = static_cast<uint32_t>((4 * kTR + m.ceil_bits * kTR * (m.n_b / 8) + 127) / 128 * 128);
-    p.rec_bytes = static_cast<uint32_t>(RecGeom{M}.bytes(CH));
+    // split-K: every CTA gets ~U units so that all linears' CTAs fit one wave
+    // of resident slots with equal work (balanced across the group)
+    int ceil_bits = 0;
+    int64_t units = 0;
+    for (int i = 0; i < n; ++i) {
+        units += static_cast<int64_t>(ms[i]->RT) * ms[i]->BC;
+        ceil_bits = std::max(ceil_bits, ms[i]->ceil_bits);
+    }
+    const int slots = m0.num_sms * ctas_per_sm(NT);
+    const int U = static_cast<int>(std::max<int64_t>(2, (units + slots - 1) / slots));
+    int grid = 0, xwarps = 0;
+    for (int i = 0; i < n; ++i) {
+        const DevModel& m = *ms[i];
+        Lin& L = p.lin[i];
+        const int BC = static_cast<int>(m.BC);
+        const int cmax = std::min(kMaxSplit, BC);
+        L.C = std::max(1, std::min(cmax, (BC + U - 1) / U));
+        if (const char* cs = getenv("SFMP_GEMV_SPLIT")) L.C = std::max(1, std::min(cmax, atoi(cs)));
+        L.payload = m.d_payload;
+        L.unit_desc = m.d_unit_desc;
+        L.out_map = m.d_out_map;
+        L.xrec = wss[i];
+        L.y = ys[i];
+        L.part = reinterpret_cast<float*>(wss[i] + gemv_rec_bytes(m));
+        L.counters = reinterpret_cast<unsigned*>(wss[i] + gemv_rec_bytes(m) + gemv_part_bytes(m));
+        L.out_rows = m.out_rows;
+        L.BC = BC;
+        L.cta0 = grid;
+        grid += static_cast<int>(m.RT) * L.C;
+        XLin& X = xp.lin[i];
+        X.x = xs[i];
+        X.col_perm = m.d_col_perm;
+        X.xrec = wss[i];
+        X.BC = BC;
+        X.cols = static_cast<int>(m.cols);
+        X.warp0 = xwarps;
+        xwarps += BC * NT;
+    }
+    p.stage_w = static_cast<uint32_t>((4 * kTR + ceil_bits * kTR * (m0.n_b / 8) + 127) / 128 * 128);
     int max_stages = 4;
     if (const char* ss = getenv("SFMP_GEMV_STAGES")) max_stages = std::max(2, atoi(ss));
     const int fixed = kHdrBytes;
@@ -548,13 +612,20 @@ cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, 
     if (stages < 2) return cudaErrorInvalidConfiguration;
     p.stages = stages;
     const size_t smem = fixed + static_cast<size_t>(stages) * (p.stage_w + p.rec_bytes);
-    const int cols = static_cast<int>(m.cols);
-    const int grid = RT * p.C;
     switch (dt) {
-        case SFMP_F32: return launch_t<SFMP_F32>(p, x, m.d_col_perm, cols, grid, smem, m.floor_bits, st);
-        case SFMP_F16: return launch_t<SFMP_F16>(p, x, m.d_col_perm, cols, grid, smem, m.floor_bits, st);
-        default: return launch_t<SFMP_BF16>(p, x, m.d_col_perm, cols, grid, smem, m.floor_bits, st);
+        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, grid, smem, m0.floor_bits, st);
+        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, grid, smem, m0.floor_bits, st);
+        default: return launch_t<SFMP_BF16>(p, xp, xwarps, grid, smem, m0.floor_bits, st);
     }
+}
+
+cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, float* y, float* ws,
+                        cudaStream_t st) {
+    const DevModel* ms[1] = {&m};
+    const void* xs[1] = {x};
+    float* ys[1] = {y};
+    uint8_t* wss[1] = {reinterpret_cast<uint8_t*>(ws)};
+    return launch_gemv_group(ms, xs, ys, wss, 1, dt, M, st);
 }
 
 }  // namespace sfmpk

@@ -1,0 +1,57 @@
+"""Grouped decode (the bench step for one M): the 7 Llama-3.1-8B linears in one launch.
+--eager: plain launches for ncu; else graph + events timing."""
+import argparse
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2602_01027_b200 as sfmp  # noqa: E402
+from oracle.oracle import Port  # noqa: E402
+from synth import LLAMA_8B, activations, model_bytes  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--M", type=int, default=1)
+ap.add_argument("--copies", type=int, default=4)
+ap.add_argument("--launches", type=int, default=8)
+ap.add_argument("--eager", action="store_true")
+args = ap.parse_args()
+P = Port()
+projs = list(LLAMA_8B)
+datas = {p: model_bytes(P, *LLAMA_8B[p], 3.25, m_b=128 if p in ("k_proj", "v_proj") else 512,
+                        seed={"up_proj": 4, "v_proj": 1}.get(p, 0)) for p in projs}
+models = [[sfmp.DeviceModel(datas[p]) for p in projs] for _ in range(args.copies)]
+xs = [torch.from_numpy(activations(P, args.M, LLAMA_8B[p][1])).cuda().to(torch.bfloat16) for p in projs]
+ys = [torch.empty(args.M, LLAMA_8B[p][0], device="cuda") for p in projs]
+ws = [m.workspace(16, sfmp.PATH_GEMV) for m in models[0]]
+
+
+def run():
+    for i in range(args.launches):
+        sfmp.gemm_grouped(models[i % args.copies], xs, outs=ys, workspaces=ws)
+
+
+run()
+torch.cuda.synchronize()
+if args.eager:
+    sys.exit(0)
+s = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=s):
+    run()
+g.replay()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record()
+for _ in range(5):
+    g.replay()
+e1.record()
+torch.cuda.synchronize()
+t = e0.elapsed_time(e1) * 1e3 / (5 * args.launches)
+byts = sum(m.info["payload_bytes"] + 4 * m.cols + 4 * m.rows + 2 * args.M * m.cols + 4 * args.M * m.rows
+           for m in models[0])
+print(f"grouped 8B layer M={args.M}: {t:.2f} us/launch, {byts / t / 1e3:.1f} GB/s = "
+      f"{byts / t / 1e3 / 6514.2 * 100:.1f}% of 6514.2", flush=True)
