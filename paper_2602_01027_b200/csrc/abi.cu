@@ -280,7 +280,6 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
     d->avg_bits = d->K ? static_cast<double>(sum) / d->K : 0.0;
     d->payload_bytes = payload.size();
     sfmp_status s;
-    if ((s = dev_upload(*d, &d->d_payload, payload.data(), payload.size()))) return s;
     if ((s = dev_upload(*d, &d->d_unit_desc, d->h_unit_desc.data(), d->h_unit_desc.size() * 8))) return s;
     std::vector<uint32_t> cp(p.cols);
     if (p.col_perm) std::memcpy(cp.data(), p.col_perm, p.cols * 4);
@@ -300,6 +299,10 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
         }
     }
     d->gemm_ok = sfmpk::gemm_supported(*d);
+    // The decode layout stores <= 4-bit units repacked for one-LOP3 unpacking
+    // (same bytes, csrc/repack.cuh); the GEMM layout above was built from the planes.
+    sfmpk::repack_units(*d, payload);
+    if ((s = dev_upload(*d, &d->d_payload, payload.data(), payload.size()))) return s;
     const size_t ws = d->gemv_ok ? sfmpk::gemv_workspace_bytes(*d, 16) : 0;
     if (ws) {
         if ((s = dev_upload<float>(*d, &d->d_ws, nullptr, ws))) return s;

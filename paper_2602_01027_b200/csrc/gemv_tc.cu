@@ -36,6 +36,7 @@
 #include <cstdlib>
 
 #include "ptx.cuh"
+#include "repack.cuh"
 #include "unpack.cuh"
 #include "sfmp_internal.h"
 
@@ -56,6 +57,7 @@ __host__ __device__ constexpr int smem_per_cta(int NT) { return (225 * 1024) / c
 // seven linears of a decoder layer -- share one launch so the fixed per-call
 // latencies (launch, first HBM bytes, split-K tail) are paid once.
 constexpr int kMaxLin = 16;
+constexpr int kMaxSplit = 32;  // CTAs that may share one row tile
 struct Lin {
     const uint8_t* payload;
     const uint64_t* unit_desc;  // [RT*BC] row-tile-major
@@ -66,12 +68,13 @@ struct Lin {
     unsigned* counters;         // [RT] completion counters (zero between calls)
     uint64_t out_rows;
     int BC;
-    int C;                      // CTAs per row tile (split-K ways)
-    int cta0;                   // first CTA of this linear in the grid
+    int64_t unit0;              // first unit of this linear in the group's unit sequence
 };
 struct Params {
     Lin lin[kMaxLin];
     int nlin;
+    int64_t units;  // units of all linears
+    int64_t Q;      // units per CTA
     int M;
     int n_b;
     int stages;
@@ -84,6 +87,7 @@ struct XLin {
     const uint32_t* col_perm;
     uint8_t* xrec;
     int BC, cols, warp0;
+    int lo;  // floor bit-width: records carry the magic biases of lo and lo+1 bit units
 };
 struct XParams {
     XLin lin[kMaxLin];
@@ -95,7 +99,8 @@ struct XParams {
 // Activation record of one block column (n_b columns), for M tokens:
 //   for chunk c (128 columns), n-tile nt (8 tokens), token n < Mnt, k-step s:
 //     4 lanes x 8 B of f16 B fragments  (tokens >= M omitted)
-//   then Xg[16] (f32 column sums) and bias[16] (f32 magic offsets).
+//   then Xg[16] (f32 column sums), bias[16] of floor-bit units, bias[16] of
+//   ceil-bit units (f32 magic offsets of the repacked layout, repack.cuh).
 // Within a (c, nt, n) run the 8 k-steps are contiguous (stride 32 B), so a
 // lane's fragment addresses are compile-time offsets from one base.
 struct RecGeom {
@@ -110,7 +115,7 @@ struct RecGeom {
         return lane_off(c, nt, n, q) + s * 32;
     }
     __host__ __device__ int xg_off(int CH) const { return CH * chunk_bytes(); }
-    __host__ __device__ int bytes(int CH) const { return (xg_off(CH) + 128 + 127) / 128 * 128; }
+    __host__ __device__ int bytes(int CH) const { return (xg_off(CH) + 192 + 127) / 128 * 128; }
 };
 
 // Debug timeline (SFMP_GEMV_DEBUG=5): [cta][slot] globaltimer stamps for the
@@ -166,6 +171,7 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     const void* x = XL.x;
     const uint32_t* col_perm = XL.col_perm;
     uint8_t* xrec = XL.xrec;
+    const int lo = XL.lo;
     if (w >= BC * NT) return;
     const int bc = w / NT, nt = w - bc * NT;
     const int lane = threadIdx.x & 31, q = lane & 3, n = lane >> 2;
@@ -173,7 +179,7 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     const int t = nt * 8 + n;
     const bool live = n < G.mnt(nt);
     uint8_t* rec = xrec + static_cast<size_t>(bc) * rec_bytes;
-    float xs = 0.f, bias = 0.f;
+    float xs = 0.f, bias_lo = 0.f, bias_hi = 0.f;
     for (int c = 0; c < CH; ++c) {
         const uint4 idx4 = __ldg(reinterpret_cast<const uint4*>(col_perm + bc * n_b + c * 128) + lane);
         uint32_t gi[32];
@@ -200,10 +206,15 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
                 st.x = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 0], v[s8 * 4 + 1]));
                 st.y = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 2], v[s8 * 4 + 3]));
                 *reinterpret_cast<uint2*>(rec + G.frag_off(c, nt, s8, n, q)) = st;
-                // slot j=0 holds nibble pairs h even (magic 1024), j=1 h odd (magic 64);
-                // the bias uses the f16-rounded values the MMA sees.
-                bias += 1024.f * (__low2float(u32_as_h2(st.x)) + __high2float(u32_as_h2(st.x))) +
-                        64.f * (__low2float(u32_as_h2(st.y)) + __high2float(u32_as_h2(st.y)));
+                // st.x pairs with A register 2*s8, st.y with 2*s8+1; each carries the
+                // magic of its register in the repacked layout of a lo / lo+1 bit
+                // unit (0 for the exact >4-bit path).  The bias uses the f16-rounded
+                // values the MMA sees.
+                const float sx = __low2float(u32_as_h2(st.x)) + __high2float(u32_as_h2(st.x));
+                const float sy = __low2float(u32_as_h2(st.y)) + __high2float(u32_as_h2(st.y));
+                auto mag = [](int B, int j) { return B <= 4 ? rp_magic(B, j) : 0.f; };
+                bias_lo += mag(lo, 2 * s8) * sx + mag(lo, 2 * s8 + 1) * sy;
+                bias_hi += mag(lo + 1, 2 * s8) * sx + mag(lo + 1, 2 * s8 + 1) * sy;
             }
 #pragma unroll
             for (int e = 0; e < 32; ++e) xs += v[e];
@@ -211,12 +222,15 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     }
     xs += __shfl_xor_sync(0xffffffffu, xs, 1);
     xs += __shfl_xor_sync(0xffffffffu, xs, 2);
-    bias += __shfl_xor_sync(0xffffffffu, bias, 1);
-    bias += __shfl_xor_sync(0xffffffffu, bias, 2);
+    bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 1);
+    bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 2);
+    bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 1);
+    bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 2);
     if (q == 0) {
         float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
         xg[nt * 8 + n] = live ? xs : 0.f;
-        xg[16 + nt * 8 + n] = live ? bias : 0.f;
+        xg[16 + nt * 8 + n] = live ? bias_lo : 0.f;
+        xg[32 + nt * 8 + n] = live ? bias_hi : 0.f;
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
 }
@@ -237,7 +251,10 @@ __device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[N
         for (int r = 0; r < 2 * kMT; ++r) p[r][i] = lds_u32(prow + i * PS + r * 8 * NB8 + c * 16);
     uint32_t A[2 * kMT][16];
 #pragma unroll
-    for (int r = 0; r < 2 * kMT; ++r) unpack_word<B>(p[r], A[r]);
+    for (int r = 0; r < 2 * kMT; ++r) {
+        if constexpr (B <= 4) unpack_rp<B>(p[r], A[r]);  // repacked layout (repack.cuh)
+        else unpack_word<B>(p[r], A[r]);                // bit planes, exact codes
+    }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
 #pragma unroll
@@ -254,14 +271,39 @@ __device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[N
 // LO = the model's floor bit-width: every unit has LO or LO+1 bits
 // (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
 // two unpack paths and its hot loop stays resident in the instruction cache.
+// Work split: all units of all linears form one sequence (linear, row tile,
+// block column); CTA b streams units [b*Q, (b+1)*Q) -- equal work per CTA,
+// one wave.  A CTA's range is cut into segments at row-tile boundaries; a
+// row tile covered by several CTAs is reduced split-K style (part k of the
+// tile = the k-th CTA that touches it, summed in k order).
+struct Seg {
+    int li, rt, bc0, bc1;  // units [bc0, bc1) of row tile rt of linear li
+    int k, C;              // this CTA is the k-th of the C CTAs touching the tile
+};
+__device__ __forceinline__ Seg seg_at(const Params& p, int64_t u, int64_t end) {
+    int li = 0;
+    while (li + 1 < p.nlin && u >= p.lin[li + 1].unit0) ++li;
+    const Lin& L = p.lin[li];
+    const int64_t rel = u - L.unit0;
+    Seg sg;
+    sg.li = li;
+    sg.rt = static_cast<int>(rel / L.BC);
+    sg.bc0 = static_cast<int>(rel - static_cast<int64_t>(sg.rt) * L.BC);
+    const int64_t t0 = L.unit0 + static_cast<int64_t>(sg.rt) * L.BC, t1 = t0 + L.BC;  // tile's unit range
+    sg.bc1 = static_cast<int>((end < t1 ? end : t1) - t0);
+    const int64_t c0 = t0 / p.Q, c1 = (t1 - 1) / p.Q;
+    sg.C = static_cast<int>(c1 - c0 + 1);
+    sg.k = static_cast<int>(static_cast<int64_t>(blockIdx.x) - c0);
+    return sg;
+}
+
+// LO = the model's floor bit-width: every unit has LO or LO+1 bits
+// (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
+// two unpack paths and its hot loop stays resident in the instruction cache.
 template <int NT, int CH, int LO>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const Params p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
-    int li = 0;
-    while (li + 1 < p.nlin && static_cast<int>(blockIdx.x) >= p.lin[li + 1].cta0) ++li;
-    const Lin& L = p.lin[li];
-    const int C = L.C;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
     uint8_t* zeros = smem + 256;                               // 256 B: B fragments of absent tokens
@@ -273,11 +315,6 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int dbg = p.debug_mode;
     if (threadIdx.x == 0) DBG_STAMP(0);
-    const int lcta = static_cast<int>(blockIdx.x) - L.cta0;
-    const int rank = lcta % C;
-    const int rt = lcta / C;
-    const int bc0 = rank * L.BC / C, bc1 = (rank + 1) * L.BC / C;
-    const int nunits = bc1 - bc0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -291,51 +328,70 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 
     constexpr int nb8 = CH * 16;
     const RecGeom G{p.M};
-    const uint64_t* gdesc = L.unit_desc + static_cast<size_t>(rt) * L.BC + bc0;
 
     if (warp == 0) {
         // ---------------- producer: one bulk copy per unit (+ its activation record) ----
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             const uint32_t pbytes = kTR * nb8;
-            auto issue_w = [&](int s, int i, uint64_t d) {
+            int gi = 0;  // unit counter of this CTA (debug stamps)
+            auto issue_w = [&](int s, const Lin& L, uint64_t d) {
                 const int bits = static_cast<int>((d >> 48) & 0xF);
                 sbits[s] = static_cast<uint32_t>(bits);  // published by the arrive below
-                DBG_STAMP(2 + 3 * i);
+                DBG_STAMP(2 + 3 * gi);
                 const uint32_t wbytes = 4 * kTR + bits * pbytes;
                 mbar_arrive_expect_tx(&full[s], wbytes + p.rec_bytes);
                 bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
                          &full[s], pol);
             };
-            auto issue_x = [&](int s, int bc_) {
+            auto issue_x = [&](int s, const Lin& L, int bc_) {
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         smem_u32(xbase + static_cast<size_t>(s) * p.rec_bytes)),
                     "l"(L.xrec + static_cast<size_t>(bc_) * p.rec_bytes), "r"(p.rec_bytes), "r"(smem_u32(&full[s]))
                     : "memory");
             };
-            const int pre = nunits < S ? nunits : S;
-            // 1) weights of the first ring-full of units do not depend on x
-            uint64_t dpre[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if (i < pre) dpre[i] = __ldg(gdesc + i);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if (i < pre) issue_w(i, i, dpre[i]);
-            uint64_t dnext = pre < nunits ? __ldg(gdesc + pre) : 0;
-            // 2) wait for the activation-record producer (programmatic dependent launch)
-            pdl_wait();
-            for (int i = 0; i < pre; ++i) issue_x(i, bc0 + i);
-            // 3) steady state: unit i reuses stage i % S after round i/S - 1 drained
             int s = 0, ph = 0;
-            for (int i = pre; i < nunits; ++i) {
-                const uint64_t d = dnext;
-                if (i + 1 < nunits) dnext = __ldg(gdesc + i + 1);
-                mbar_wait(&empty[s], ph);
-                issue_w(s, i, d);
-                issue_x(s, bc0 + i);
-                if (++s == S) { s = 0; ph ^= 1; }
+            bool first = true;
+            const int64_t uend = min(p.units, (static_cast<int64_t>(blockIdx.x) + 1) * p.Q);
+            for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.Q; u < uend;) {
+                const Seg I = seg_at(p, u, uend);
+                u += I.bc1 - I.bc0;
+                const Lin& L = p.lin[I.li];
+                const uint64_t* gdesc = L.unit_desc + static_cast<size_t>(I.rt) * L.BC + I.bc0;
+                const int nunits = I.bc1 - I.bc0;
+                int i0 = 0;
+                if (first) {
+                    // weights of the first ring-full do not depend on x: issue them,
+                    // then wait for the activation records (programmatic dependent launch)
+                    const int pre = nunits < S ? nunits : S;
+                    uint64_t dpre[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (i < pre) dpre[i] = __ldg(gdesc + i);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (i < pre) {
+                            issue_w(i, L, dpre[i]);
+                            ++gi;
+                        }
+                    pdl_wait();
+                    for (int i = 0; i < pre; ++i) issue_x(i, L, I.bc0 + i);
+                    s = pre % S;
+                    ph = pre == S ? 1 : 0;
+                    i0 = pre;
+                    first = false;
+                }
+                uint64_t dnext = i0 < nunits ? __ldg(gdesc + i0) : 0;
+                for (int i = i0; i < nunits; ++i) {
+                    const uint64_t d = dnext;
+                    if (i + 1 < nunits) dnext = __ldg(gdesc + i + 1);
+                    mbar_wait(&empty[s], ph ^ 1);
+                    issue_w(s, L, d);
+                    issue_x(s, L, I.bc0 + i);
+                    ++gi;
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
             }
         }
     } else {
@@ -343,17 +399,6 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         const int cw = warp - 1;
         const int g = lane >> 2, q = lane & 3;
         const int r0 = cw * 16 * kMT + g;  // rows r0 + 8*r of the tile
-        // output columns of this thread's rows, fetched early
-        uint32_t my_map[2 * kMT];
-#pragma unroll
-        for (int r = 0; r < 2 * kMT; ++r) my_map[r] = C == 1 ? __ldg(L.out_map + rt * kTR + r0 + 8 * r) : 0u;
-        float yacc[kMT][NT][4];
-#pragma unroll
-        for (int m = 0; m < kMT; ++m)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
         const int chunk_bytes = G.chunk_bytes();
         const uint32_t stage_w = p.stage_w, rec_bytes = p.rec_bytes;
         // per-lane shared addresses for stage 0; a stage adds s * stage_w / rec_bytes
@@ -368,70 +413,85 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         }
         const uint32_t xg0 = smem_u32(xbase) + G.xg_off(CH) + 8 * q;
         const uint32_t sbits_a = smem_u32(sbits);
-        int s = 0, ph = 0;
-        for (int i = 0; i < nunits; ++i) {
-            mbar_wait(&full[s], ph);
-            if (cw == 0 && lane == 0) DBG_STAMP(3 + 3 * i);
-            const int bits = static_cast<int>(lds_u32(sbits_a + 4 * s));
-            uint32_t xb[NT];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + s * xstep[nt];
-            const uint32_t prow = prow0 + s * stage_w;
-            float cacc[2 * kMT][NT][4];
-#pragma unroll
-            for (int h = 0; h < 2 * kMT; ++h)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) cacc[h][nt][e] = 0.f;
-#pragma unroll
-            for (int c = 0; c < CH; ++c) {
-                if (bits == LO) {
-                    unit_chunk<LO, NT, CH>(prow, xb, chunk_bytes, c, cacc);
-                } else if constexpr (LO < 8) {
-                    unit_chunk<LO + 1, NT, CH>(prow, xb, chunk_bytes, c, cacc);
-                }
-            }
-            // per-row affine of this block: y += s*(C - bias) + z*Xg
-            const uint32_t sz = sz0 + s * stage_w;
-            const uint32_t xg = xg0 + s * rec_bytes;
-            const bool biased = bits <= 4;
-#pragma unroll
-            for (int m = 0; m < kMT; ++m) {
-                const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
-                const float za = lds_h2f(sz + 2 * kTR + 32 * m), zb = lds_h2f(sz + 2 * kTR + 32 * m + 16);
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const float2 xg01 = lds_f2(xg + 32 * nt);
-                    float2 b01 = lds_f2(xg + 64 + 32 * nt);
-                    if (!biased) b01 = make_float2(0.f, 0.f);
-                    const float* c0 = cacc[2 * m][nt];
-                    const float* c1 = cacc[2 * m + 1][nt];
-                    yacc[m][nt][0] += sa * ((c0[0] + c1[0]) - b01.x) + za * xg01.x;
-                    yacc[m][nt][1] += sa * ((c0[1] + c1[1]) - b01.y) + za * xg01.y;
-                    yacc[m][nt][2] += sb * ((c0[2] + c1[2]) - b01.x) + zb * xg01.x;
-                    yacc[m][nt][3] += sb * ((c0[3] + c1[3]) - b01.y) + zb * xg01.y;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            if (cw == 0 && lane == 0) DBG_STAMP(4 + 3 * i);
-            if (++s == S) { s = 0; ph ^= 1; }
-        }
-        if (C == 1) {
-            // whole row tile in this CTA: un-permuted store straight to y
+        int s = 0, ph = 0, gi = 0;
+        const int64_t uend = min(p.units, (static_cast<int64_t>(blockIdx.x) + 1) * p.Q);
+        for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.Q; u < uend;) {
+            const Seg I = seg_at(p, u, uend);
+            u += I.bc1 - I.bc0;
+            const Lin& L = p.lin[I.li];
+            const int C = I.C, rt = I.rt, nunits = I.bc1 - I.bc0;
+            float yacc[kMT][NT][4];
 #pragma unroll
             for (int m = 0; m < kMT; ++m)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int t = nt * 8 + 2 * q + (e & 1);
-                        if (t < p.M) L.y[t * L.out_rows + my_map[2 * m + (e >> 1)]] = yacc[m][nt][e];
+                    for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
+            for (int i = 0; i < nunits; ++i, ++gi) {
+                mbar_wait(&full[s], ph);
+                if (cw == 0 && lane == 0) DBG_STAMP(3 + 3 * gi);
+                const int bits = static_cast<int>(lds_u32(sbits_a + 4 * s));
+                uint32_t xb[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + s * xstep[nt];
+                const uint32_t prow = prow0 + s * stage_w;
+                float cacc[2 * kMT][NT][4];
+#pragma unroll
+                for (int h = 0; h < 2 * kMT; ++h)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) cacc[h][nt][e] = 0.f;
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    if (bits == LO) {
+                        unit_chunk<LO, NT, CH>(prow, xb, chunk_bytes, c, cacc);
+                    } else if constexpr (LO < 8) {
+                        unit_chunk<LO + 1, NT, CH>(prow, xb, chunk_bytes, c, cacc);
                     }
-        } else {
-            // split-K partial tile [t][128 rows] of this CTA (coalesced rows)
-            float* part = L.part + (static_cast<size_t>(rt) * C + rank) * (16 * kTR);
+                }
+                // per-row affine of this block: y += s*(C - bias) + z*Xg
+                const uint32_t sz = sz0 + s * stage_w;
+                const uint32_t xg = xg0 + s * rec_bytes;
+                const uint32_t boff = bits == LO ? 64u : 128u;  // bias of this unit's layout (0 for > 4 bits)
+#pragma unroll
+                for (int m = 0; m < kMT; ++m) {
+                    const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
+                    const float za = lds_h2f(sz + 2 * kTR + 32 * m), zb = lds_h2f(sz + 2 * kTR + 32 * m + 16);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        const float2 xg01 = lds_f2(xg + 32 * nt);
+                        const float2 b01 = lds_f2(xg + boff + 32 * nt);
+                        const float* c0 = cacc[2 * m][nt];
+                        const float* c1 = cacc[2 * m + 1][nt];
+                        yacc[m][nt][0] += sa * ((c0[0] + c1[0]) - b01.x) + za * xg01.x;
+                        yacc[m][nt][1] += sa * ((c0[1] + c1[1]) - b01.y) + za * xg01.y;
+                        yacc[m][nt][2] += sb * ((c0[2] + c1[2]) - b01.x) + zb * xg01.x;
+                        yacc[m][nt][3] += sb * ((c0[3] + c1[3]) - b01.y) + zb * xg01.y;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                if (cw == 0 && lane == 0) DBG_STAMP(4 + 3 * gi);
+                if (++s == S) { s = 0; ph ^= 1; }
+            }
+            if (C == 1) {
+                // whole row tile in this item: un-permuted store straight to y
+#pragma unroll
+                for (int m = 0; m < kMT; ++m)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int t = nt * 8 + 2 * q + (e & 1);
+                            if (t < p.M)
+                                L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + r0 + 16 * m + 8 * (e >> 1))] =
+                                    yacc[m][nt][e];
+                        }
+                continue;
+            }
+            // split-K partial tile [t][128 rows] of this item (coalesced rows)
+            float* part = L.part + (static_cast<size_t>(rt) * kMaxSplit + I.k) * (16 * kTR);
 #pragma unroll
             for (int m = 0; m < kMT; ++m)
 #pragma unroll
@@ -441,27 +501,26 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                         const int t = nt * 8 + 2 * q + (e & 1);
                         if (t < p.M) part[t * kTR + r0 + 16 * m + 8 * (e >> 1)] = yacc[m][nt][e];
                     }
-        }
-    }
-    if (C > 1) {
-        // Deterministic split-K: the last of the C CTAs of this row tile sums
-        // the partials in split order and stores them un-permuted.
-        __syncthreads();  // every partial store of this CTA precedes the release below
-        if (threadIdx.x == 0) {
-            const unsigned old = atomic_add_acq_rel_gpu(L.counters + rt, 1u);
-            *flag = (old == static_cast<unsigned>(C - 1)) ? 1u : 0u;
-        }
-        __syncthreads();
-        if (*flag) {
-            __threadfence();
-            const float* part = L.part + static_cast<size_t>(rt) * C * (16 * kTR);
-            for (int v = threadIdx.x; v < p.M * kTR; v += kThreads) {
-                const int t = v / kTR, row = v - t * kTR;
-                float acc = 0.f;
-                for (int r = 0; r < C; ++r) acc += __ldcg(part + static_cast<size_t>(r) * (16 * kTR) + v);
-                L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = acc;
+            // Deterministic split-K: the last of the C items of this row tile
+            // sums the partials in split order and stores them un-permuted.
+            // Compute warps only (the producer streams on): named barrier 1.
+            named_bar_sync(1, kNCW * 32);  // every partial store precedes the release below
+            if (threadIdx.x == 32) {
+                const unsigned old = atomic_add_acq_rel_gpu(L.counters + rt, 1u);
+                *flag = (old == static_cast<unsigned>(C - 1)) ? 1u : 0u;
             }
-            if (threadIdx.x == 0) L.counters[rt] = 0u;  // ready for the next call (stream-ordered)
+            named_bar_sync(1, kNCW * 32);
+            if (*flag) {
+                __threadfence();
+                const float* pp = L.part + static_cast<size_t>(rt) * kMaxSplit * (16 * kTR);
+                for (int v = threadIdx.x - 32; v < p.M * kTR; v += kNCW * 32) {
+                    const int t = v / kTR, row = v - t * kTR;
+                    float acc = 0.f;
+                    for (int r = 0; r < C; ++r) acc += __ldcg(pp + static_cast<size_t>(r) * (16 * kTR) + v);
+                    L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = acc;
+                }
+                if (threadIdx.x == 32) L.counters[rt] = 0u;  // ready for the next call (stream-ordered)
+            }
         }
     }
     if (threadIdx.x == 0) DBG_STAMP(1);
@@ -532,12 +591,11 @@ extern "C" int sfmp_debug_gemv_timeline(unsigned long long* host, size_t n) {
 }
 
 // Workspace: activation records | split-K partials | completion counters.
-constexpr int kMaxSplit = 32;
 size_t gemv_rec_bytes(const DevModel& m) {
     return (static_cast<size_t>(m.BC) * RecGeom{16}.bytes(static_cast<int>(m.n_b / 128)) + 255) / 256 * 256;
 }
 size_t gemv_part_bytes(const DevModel& m) {
-    return static_cast<size_t>(m.RT) * std::min<int>(kMaxSplit, m.BC) * 16 * kTR * 4;
+    return static_cast<size_t>(m.RT) * kMaxSplit * 16 * kTR * 4;
 }
 size_t gemv_workspace_bytes(const DevModel& m, int M) {
     (void)M;
@@ -575,15 +633,18 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         ceil_bits = std::max(ceil_bits, ms[i]->ceil_bits);
     }
     const int slots = m0.num_sms * ctas_per_sm(NT);
-    const int U = static_cast<int>(std::max<int64_t>(2, (units + slots - 1) / slots));
-    int grid = 0, xwarps = 0;
+    // One wave: G CTAs, each Q consecutive units of the group's unit sequence
+    // (Q large enough that no row tile is shared by more than kMaxSplit CTAs).
+    int max_bc = 1;
+    for (int i = 0; i < n; ++i) max_bc = std::max(max_bc, static_cast<int>(ms[i]->BC));
+    int64_t Q = std::max<int64_t>({2, (units + slots - 1) / slots, (max_bc + kMaxSplit - 2) / (kMaxSplit - 1)});
+    if (const char* e = getenv("SFMP_GEMV_Q")) Q = std::max<int64_t>(Q, atoi(e));
+    int64_t unit0 = 0;
+    int xwarps = 0;
     for (int i = 0; i < n; ++i) {
         const DevModel& m = *ms[i];
         Lin& L = p.lin[i];
         const int BC = static_cast<int>(m.BC);
-        const int cmax = std::min(kMaxSplit, BC);
-        L.C = std::max(1, std::min(cmax, (BC + U - 1) / U));
-        if (const char* cs = getenv("SFMP_GEMV_SPLIT")) L.C = std::max(1, std::min(cmax, atoi(cs)));
         L.payload = m.d_payload;
         L.unit_desc = m.d_unit_desc;
         L.out_map = m.d_out_map;
@@ -593,8 +654,8 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         L.counters = reinterpret_cast<unsigned*>(wss[i] + gemv_rec_bytes(m) + gemv_part_bytes(m));
         L.out_rows = m.out_rows;
         L.BC = BC;
-        L.cta0 = grid;
-        grid += static_cast<int>(m.RT) * L.C;
+        L.unit0 = unit0;
+        unit0 += static_cast<int64_t>(m.RT) * BC;
         XLin& X = xp.lin[i];
         X.x = xs[i];
         X.col_perm = m.d_col_perm;
@@ -602,6 +663,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         X.BC = BC;
         X.cols = static_cast<int>(m.cols);
         X.warp0 = xwarps;
+        X.lo = m.floor_bits;
         xwarps += BC * NT;
     }
     p.stage_w = static_cast<uint32_t>((4 * kTR + ceil_bits * kTR * (m0.n_b / 8) + 127) / 128 * 128);
@@ -612,6 +674,9 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     if (stages < 2) return cudaErrorInvalidConfiguration;
     p.stages = stages;
     const size_t smem = fixed + static_cast<size_t>(stages) * (p.stage_w + p.rec_bytes);
+    p.units = unit0;
+    p.Q = Q;
+    const int grid = static_cast<int>((unit0 + Q - 1) / Q);
     switch (dt) {
         case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, grid, smem, m0.floor_bits, st);
         case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, grid, smem, m0.floor_bits, st);

@@ -5,6 +5,9 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstring>
+
+#include "repack.cuh"
 #include "sfmp_internal.h"
 
 namespace sfmpk {
@@ -27,8 +30,17 @@ struct RowRef {
     uint64_t plane_bytes;   // TR * n_b / 8
     uint32_t row_off;       // rr * n_b / 8
     int bits;
+    bool repacked;
     float s, z;
+    // Units of <= 4 bits are stored in the repacked decode layout
+    // (repack.cuh); wider units keep the SFMPPKD1 bit planes.
     __device__ __forceinline__ uint32_t code(uint32_t jj) const {
+        if (repacked && bits <= 4) {
+            uint32_t w[4];
+            for (int i = 0; i < bits; ++i)
+                w[i] = *reinterpret_cast<const uint32_t*>(planes + i * plane_bytes + row_off + (jj >> 5) * 4);
+            return rp_code(w, bits, static_cast<int>(jj & 31));
+        }
         uint32_t c = 0;
         for (int i = 0; i < bits; ++i)
             c |= ((planes[i * plane_bytes + row_off + (jj >> 3)] >> (jj & 7)) & 1u) << i;
@@ -43,6 +55,7 @@ __device__ __forceinline__ RowRef row_ref(const UnitGeom& g, uint64_t r, uint32_
     const uint32_t rr = static_cast<uint32_t>(r % g.TR);
     RowRef ref;
     ref.bits = static_cast<int>((d >> 48) & 0xF);
+    ref.repacked = g.repacked;
     ref.s = __half2float(*reinterpret_cast<const __half*>(base + 2 * rr));
     ref.z = __half2float(*reinterpret_cast<const __half*>(base + 2ull * g.TR + 2 * rr));
     ref.planes = base + 4ull * g.TR;
@@ -137,6 +150,31 @@ GenParams make_params(const DevModel& m) {
 }
 
 }  // namespace
+
+// Host: rewrite every <= 4-bit unit of the unit-major payload from bit planes
+// to the repacked decode layout (repack.cuh), in place, byte count unchanged.
+void repack_units(const DevModel& d, std::vector<uint8_t>& payload) {
+    if (!d.gemv_ok) return;  // only the decode GEMV's geometry (TR=128, n_b in {128, 256})
+    const uint32_t TR = d.TR, nb8 = d.n_b / 8, groups = d.n_b / 32;
+    const uint64_t PS = static_cast<uint64_t>(TR) * nb8;
+    for (uint64_t desc : d.h_unit_desc) {
+        const int B = static_cast<int>((desc >> 48) & 0xF);
+        if (B > 4) continue;
+        uint8_t* planes = payload.data() + (desc & 0xFFFFFFFFFFFFull) + 4ull * TR;
+        for (uint32_t r = 0; r < TR; ++r)
+            for (uint32_t g = 0; g < groups; ++g) {
+                uint32_t pw[4], codes[32], out[4];
+                for (int i = 0; i < B; ++i) std::memcpy(&pw[i], planes + i * PS + r * nb8 + g * 4, 4);
+                for (int k = 0; k < 32; ++k) {
+                    uint32_t c = 0;
+                    for (int i = 0; i < B; ++i) c |= ((pw[i] >> k) & 1u) << i;
+                    codes[k] = c;
+                }
+                rp_pack(codes, B, out);
+                for (int i = 0; i < B; ++i) std::memcpy(planes + i * PS + r * nb8 + g * 4, &out[i], 4);
+            }
+    }
+}
 
 cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
                            cudaStream_t st) {

@@ -25,6 +25,7 @@ struct UnitGeom {
     const uint8_t* payload;
     const uint64_t* unit_desc;
     uint32_t TR, n_b, BC;
+    bool repacked;  // <= 4-bit units in the decode layout of repack.cuh
 };
 
 struct DevModel {
@@ -74,7 +75,7 @@ struct DevModel {
     size_t host_stage_bytes = 0;
     std::vector<void*> allocs;
 
-    UnitGeom geom() const { return UnitGeom{d_payload, d_unit_desc, TR, n_b, BC}; }
+    UnitGeom geom() const { return UnitGeom{d_payload, d_unit_desc, TR, n_b, BC, gemv_ok}; }
 };
 
 // Launchers (return cudaError_t of the launch).
@@ -96,6 +97,7 @@ cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, 
 
 // K2 prefill GEMM (tcgen05)
 bool gemm_supported(const DevModel& m);
+void repack_units(const DevModel& d, std::vector<uint8_t>& payload);
 std::vector<uint32_t> gemm_slot_table(const std::vector<uint32_t>& col_perm);
 bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const std::vector<uint32_t>& out_map,
                        std::vector<uint8_t>& wl, std::vector<uint64_t>& woff);

@@ -55,3 +55,37 @@ byts = sum(m.info["payload_bytes"] + 4 * m.cols + 4 * m.rows + 2 * args.M * m.co
            for m in models[0])
 print(f"grouped 8B layer M={args.M}: {t:.2f} us/launch, {byts / t / 1e3:.1f} GB/s = "
       f"{byts / t / 1e3 / 6514.2 * 100:.1f}% of 6514.2", flush=True)
+
+if os.environ.get("SFMP_GEMV_DEBUG") == "5":
+    import ctypes as C
+    import numpy as np
+    g.replay()
+    torch.cuda.synchronize()
+    buf = np.zeros(512 * 128, np.uint64)
+    sfmp.lib().sfmp_debug_gemv_timeline(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_size_t(buf.size))
+    t = buf.reshape(512, 128).astype(np.int64)
+    valid = t[:511, 0] > 0
+    t0 = t[:511][valid, 0].min()
+    nun = np.array([sum(1 for j in range(40) if 2 + 3 * j < 128 and t[c, 2 + 3 * j] >= t0) for c in range(511)])
+    sel = valid & (nun > 0)
+
+    def pct(a):
+        a = a[:511][sel]
+        return " ".join(f"{np.percentile((a - t0) / 1e3, q):6.2f}" for q in (0, 10, 50, 90, 100))
+    last = np.array([t[c, 4 + 3 * (n - 1)] if n > 0 else 0 for c, n in enumerate(nun)])
+    print("timeline (us) percentiles 0/10/50/90/100 over CTAs 0..510")
+    print("  start      ", pct(t[:, 0]))
+    print("  first issue", pct(t[:, 2]))
+    print("  first full ", pct(t[:, 3]))
+    print("  last done  ", pct(np.concatenate([last, [0]])))
+    print("  end        ", pct(t[:, 1]))
+    print("  units/CTA  ", np.percentile(nun[sel], [0, 50, 100]))
+    # per-unit processing interval (compute warp 0) median over CTAs
+    iv = []
+    for c in np.where(sel)[0]:
+        n = nun[c]
+        d = [t[c, 4 + 3 * (j + 1)] - t[c, 4 + 3 * j] for j in range(min(n, 40) - 1) if 4 + 3 * (j + 1) < 128]
+        iv += d
+    print("  unit interval us: median %.3f p90 %.3f" % (np.median(iv) / 1e3, np.percentile(iv, 90) / 1e3))
+    fw = [t[c, 3 + 3 * j] - t[c, 4 + 3 * (j - 1)] for c in np.where(sel)[0] for j in range(1, min(nun[c], 40)) if 4 + 3 * j < 128]
+    print("  wait-for-full after prev unit us: median %.3f p90 %.3f" % (np.median(fw) / 1e3, np.percentile(fw, 90) / 1e3))
