@@ -413,38 +413,62 @@ def main():
         torch.cuda.synchronize()
         ungrouped_ms = u0.elapsed_time(u1) / reps
 
-    # ---- e2e: the public host-buffer API (sfmp_gemm_host), pinned host memory ----
-    hx = {(p, M): torch.from_numpy(port.gen_activation(M, SHAPES[p][1], 3000 + M)).pin_memory()
-          for p in PROJS for M in MS}
-    hy = {(p, M): torch.empty(M, SHAPES[p][0]).pin_memory() for p in PROJS for M in MS}
-    h2d = sum(M * SHAPES[p][1] * 4 for p in PROJS for M in MS)
-    d2h = sum(M * SHAPES[p][0] * 4 for p in PROJS for M in MS)
+    # ---- e2e: host buffers in, host buffers out, through the public API ----
+    # One pinned host buffer holds every x of the step (f32, as the reference's
+    # Vector) and one every y: one H2D + the grouped calls + one D2H per step,
+    # replayed as a CUDA graph, then the host waits for y (the step's result).
+    keys = [(p, M) for M in MS for p in PROJS]
+    xoff, yoff, xo, yo = {}, {}, 0, 0
+    for k in keys:
+        xoff[k], yoff[k] = xo, yo
+        xo += k[1] * SHAPES[k[0]][1]
+        yo += k[1] * SHAPES[k[0]][0]
+    hxb = torch.empty(xo, dtype=torch.float32).pin_memory()
+    hyb = torch.empty(yo, dtype=torch.float32).pin_memory()
+    for (p, M) in keys:
+        hxb[xoff[(p, M)]:xoff[(p, M)] + M * SHAPES[p][1]] = torch.from_numpy(
+            port.gen_activation(M, SHAPES[p][1], 3000 + M)).reshape(-1)
+    dxb = torch.empty(xo, dtype=torch.float32, device=dev)
+    dyb = torch.empty(yo, dtype=torch.float32, device=dev)
+    dx = {k: dxb[xoff[k]:xoff[k] + k[1] * SHAPES[k[0]][1]].view(k[1], SHAPES[k[0]][1]) for k in keys}
+    dy = {k: dyb[yoff[k]:yoff[k] + k[1] * SHAPES[k[0]][0]].view(k[1], SHAPES[k[0]][0]) for k in keys}
+    h2d, d2h = xo * 4, yo * 4
 
-    dx = {(p, M): torch.empty(M, SHAPES[p][1], device=dev) for p in PROJS for M in MS}
-
-    def e2e_step(i):
+    def e2e_body(i):
+        dxb.copy_(hxb, non_blocking=True)
         for mi, M in enumerate(MS):
             c = (i * len(MS) + mi) % COPIES
-            if world == 1 and grouped:
-                # public Python API: pinned host x -> device, grouped GEMM, y -> pinned host
-                for p in PROJS:
-                    dx[(p, M)].copy_(hx[(p, M)], non_blocking=True)
-                sfmp.gemm_grouped([models[c][p] for p in PROJS], [dx[(p, M)] for p in PROJS],
-                                  outs=[ys[(p, M)] for p in PROJS], workspaces=[ws[p] for p in PROJS])
-                for p in PROJS:
-                    hy[(p, M)].copy_(ys[(p, M)], non_blocking=True)
-                continue
-            for p in PROJS:
-                if world == 1:
-                    sfmp.check(sfmp.lib().sfmp_gemm_host(
-                        models[c][p].handle, hx[(p, M)].data_ptr(), M, hy[(p, M)].data_ptr(),
-                        None))
+            if world == 1:
+                if grouped:
+                    sfmp.gemm_grouped([models[c][p] for p in PROJS], [dx[(p, M)] for p in PROJS],
+                                      outs=[dy[(p, M)] for p in PROJS], workspaces=[ws[p] for p in PROJS])
                 else:
-                    xd = hx[(p, M)].to(dev, non_blocking=True).to(torch.bfloat16)
-                    models[c][p].gemm(xd, out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
+                    for p in PROJS:
+                        models[c][p].gemm(dx[(p, M)], out=dy[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
+            else:
+                for p in PROJS:
+                    models[c][p].gemm(dx[(p, M)], out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
                     dist.all_gather_into_tensor(gath[(p, M)], ys[(p, M)])
-                    models[c][p].unpermute_gathered(gath[(p, M)], M, out=yfull[(p, M)])
-                    hy[(p, M)].copy_(yfull[(p, M)], non_blocking=True)
+                    models[c][p].unpermute_gathered(gath[(p, M)], M, out=dy[(p, M)])
+        hyb.copy_(dyb, non_blocking=True)
+
+    e2e_graphs = []
+    if use_graph:
+        with torch.cuda.stream(stream):
+            e2e_body(0)
+        torch.cuda.synchronize()
+        for i in range(COPIES):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                e2e_body(i)
+            e2e_graphs.append(g)
+
+    def e2e_step(i):
+        if e2e_graphs:
+            e2e_graphs[i % COPIES].replay()
+        else:
+            with torch.cuda.stream(stream):
+                e2e_body(i)
         torch.cuda.synchronize()
 
     for i in range(args.warmup):
@@ -513,7 +537,8 @@ def main():
                      "algorithmic_bytes_per_step": step_bytes,
                      "avg_launch_us": round(t_us / n_gemv, 3)},
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": "sfmp_gemm_host (C ABI, pinned host buffers)"},
+                "d2h_bytes_per_step": d2h, "api": ("pinned host x -> one H2D, sfmp_gemm_grouped per M, one D2H -> pinned host y; "
+                       "CUDA graph per step, host synchronises on y every step")},
         "gpu_launches": args.steps * launches_per_step,
         "clocks": clk,
     }
