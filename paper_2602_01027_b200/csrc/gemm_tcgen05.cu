@@ -295,11 +295,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (one thread) ----------------
-        if (lane == 0) {
+        // ---------------- MMA issuer ----------------
+        // The whole warp walks the loop (warp-uniform operands stay in uniform
+        // registers, no per-MMA waterfall); one elected lane issues tcgen05.
+        {
             int xs = 0, xph = 0, ab = 0, aph = 0, accph = 0;
-            unsigned long long* tl = ((p.dbg & 32) && blockIdx.x < 2) ? g_gemm_tl + blockIdx.x * 8 * 256 : nullptr;
+            unsigned long long* tl =
+                ((p.dbg & 32) && blockIdx.x < 2 && lane == 0) ? g_gemm_tl + blockIdx.x * 8 * 256 : nullptr;
             int tcount = 0;
+            const uint32_t idesc = p.idesc;
+            const bool do_mma = !(p.dbg & 2);
             for (int ct = cid; ct < nct; ct += ncl) {
                 mbar_wait(accempty, accph ^ 1);
                 tc_fence_after();
@@ -307,26 +312,32 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                     mbar_wait(&afull[ab], aph);
                     if (tl) tl[4 * 256 + (tcount & 255)] = gtimer_ns();
                     tc_fence_after();
+                    const uint32_t a0 = tbase + kACol + ab * 64;
                     for (int h = 0; h < 2; ++h) {
                         mbar_wait(&xfull[xs], xph);
                         if (tl && h == 0) tl[5 * 256 + (tcount & 255)] = gtimer_ns();
                         tc_fence_after();
-                        const uint32_t xaddr = smem_u32(xbuf + static_cast<size_t>(xs) * xstage);
+                        const uint64_t bdesc = tc_desc_sw128(smem_u32(xbuf + static_cast<size_t>(xs) * xstage));
+                        if (elect_one()) {
+                            if (do_mma) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            if (p.dbg & 2) continue;
-                            tc_mma_ts(tbase + kAccCol, tbase + kACol + ab * 64 + (h * 4 + kk) * 8,
-                                      tc_desc_sw128(xaddr + kk * 32), p.idesc, (kc | h | kk) != 0);
+                                for (int kk = 0; kk < 4; ++kk)
+                                    tc_mma_ts(tbase + kAccCol, a0 + (h * 4 + kk) * 8, bdesc + 2 * kk, idesc,
+                                              (kc | h | kk) != 0);
+                            }
+                            if (C > 1) tc_commit_mc(&xempty[xs], cmask);  // frees the slot in every CTA's view
+                            else tc_commit(&xempty[xs]);
                         }
-                        if (C > 1) tc_commit_mc(&xempty[xs], cmask);  // frees the slot in every CTA's view
-                        else tc_commit(&xempty[xs]);
+                        __syncwarp();
                         if (++xs == SX) { xs = 0; xph ^= 1; }
                     }
-                    tc_commit(&aempty[ab]);
+                    if (elect_one()) tc_commit(&aempty[ab]);
+                    __syncwarp();
                     if (tl) tl[6 * 256 + (tcount & 255)] = gtimer_ns();
                     if (++ab == kNA) { ab = 0; aph ^= 1; }
                 }
-                tc_commit(accfull);
+                if (elect_one()) tc_commit(accfull);
+                __syncwarp();
                 accph ^= 1;
             }
         }

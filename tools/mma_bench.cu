@@ -11,15 +11,20 @@
 
 using namespace sfmpk;
 
-__global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int busy, unsigned long long* out) {
+__global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int busy, unsigned long long* out, int mode,
+                                                 const uint8_t* gsrc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
-    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    // mode bit 0: B walks a 64 KB X ring like the GEMM; bit 1: a producer warp
+    // streams bulk copies into a separate 64 KB smem region; bit 2: warps 4-7
+    // write TMEM columns 256.. with tcgen05.st (dequant traffic)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 196608);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;  // 1.0h
+    for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;  // 1.0h
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -36,7 +41,8 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int bu
         const uint64_t adesc = tc_desc_sw128(smem_u32(smem + 32768));
         unsigned long long t0 = clock64();
         for (int i = 0; i < iters; ++i) {
-            const uint64_t b = bdesc + ((i & 3) * 2);  // +32 B per k-step
+            uint64_t b = bdesc + ((i & 3) * 2);  // +32 B per k-step
+            if (mode & 1) b += ((i >> 2) & 1) * ((32768) >> 4);  // alternate two 32 KB atoms
             if (ss) tc_mma_ss(tb, adesc + ((i & 3) * 2), b, idesc, i > 0);
             else tc_mma_ts(tb, tb + 256 + (i & 7) * 8, b, idesc, i > 0);
         }
@@ -44,6 +50,28 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int bu
         mbar_wait(bar, 0);
         unsigned long long t1 = clock64();
         if (blockIdx.x == 0) out[0] = t1 - t0;
+        if (blockIdx.x == 0) out[1] = 0;
+    } else if (warp == 2 && (mode & 2)) {
+        // TMA-like traffic: 32 KB bulk copies into smem[131072..) back to back
+        if (lane == 0) {
+            uint32_t ph = 0;
+            for (int i = 0; i < iters / 8; ++i) {
+                mbar_arrive_expect_tx(bar + 1, 65536);
+                bulk_g2s(smem + 131072, gsrc + (static_cast<size_t>(blockIdx.x * 7 + i) % 64) * 32768, 32768,
+                         bar + 1, policy_evict_first());
+                bulk_g2s(smem + 131072 + 32768, gsrc + (static_cast<size_t>(blockIdx.x * 5 + i + 9) % 64) * 32768, 32768,
+                         bar + 1, policy_evict_first());
+                mbar_wait(bar + 1, ph);
+                ph ^= 1;
+            }
+        }
+    } else if (warp >= 4 && warp < 8 && (mode & 4)) {
+        uint32_t v[16];
+        for (int j = 0; j < 16; ++j) v[j] = 0x3C003C00u;
+        for (int i = 0; i < iters / 4; ++i) {
+            for (int w = 0; w < 4; ++w) tc_st_x16(tb + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 256 + 64 * (i & 3) + 16 * w, v);
+            tc_wait_st();
+        }
     } else if (warp >= 2 && warp < 2 + busy) {
         float a = threadIdx.x, b = 1.0001f;
         for (int i = 0; i < iters * 16; ++i) a = a * b + 0.5f;
@@ -57,17 +85,22 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int bu
 int main(int argc, char** argv) {
     unsigned long long* d;
     cudaMalloc(&d, 16);
-    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+    cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+    uint8_t* gsrc;
+    cudaMalloc(&gsrc, 64 << 20);
+    cudaMemset(gsrc, 0, 64 << 20);
     const int iters = 4096;
+    for (int mode : {0, 1, 3, 5, 7})
     for (int ss = 0; ss < 2; ++ss)
-        for (int n : {64, 128, 256})
-            for (int busy : {0, 12}) {
-                bench<<<148, 512, 70000>>>(iters, n, ss, busy, d);
+        for (int n : {128, 256})
+            for (int busy : {0}) {
+                if (ss && mode) continue;
+                bench<<<148, 512, 200000>>>(iters, n, ss, busy, d, mode, gsrc);
                 cudaEvent_t e0, e1;
                 cudaEventCreate(&e0);
                 cudaEventCreate(&e1);
                 cudaEventRecord(e0);
-                bench<<<148, 512, 70000>>>(iters, n, ss, busy, d);
+                bench<<<148, 512, 200000>>>(iters, n, ss, busy, d, mode, gsrc);
                 cudaEventRecord(e1);
                 cudaError_t err = cudaDeviceSynchronize();
                 float ms = 0;
@@ -75,7 +108,7 @@ int main(int argc, char** argv) {
                 unsigned long long cyc = 0;
                 cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
                 const double flops = 2.0 * 128 * n * 16 * iters * 148;
-                printf("%s N=%3d busy=%2d: %6.1f cyc/mma  %7.1f TFLOP/s  (%s)\n", ss ? "SS" : "TS", n, busy,
+                printf("mode=%d %s N=%3d busy=%2d: %6.1f cyc/mma  %7.1f TFLOP/s  (%s)\n", mode, ss ? "SS" : "TS", n, busy,
                        double(cyc) / iters, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(err));
             }
     return 0;
