@@ -60,7 +60,8 @@ constexpr int kPlaneBytes = 128 * 16;     // one plane of a unit
 constexpr int kDeqWarps = 8;              // dequant warps: 4 TMEM lane quarters x kKS K-splits
 constexpr int kKS = kDeqWarps / 4;        // K splits of a 128-column unit among dequant warps
 constexpr int kWords = 4 / kKS;           // 32-weight words per dequant thread per unit
-constexpr int kThreads = (6 + kDeqWarps) * 32;
+constexpr int kEpiWarps = 16;             // epilogue warps: 4 lane quarters x 4 column groups
+constexpr int kThreads = (2 + kEpiWarps + kDeqWarps) * 32;
 constexpr int kMaxN = 256;                // tokens per tile
 constexpr int kTmemCols = 512;
 constexpr int kAccCol = 0;                // accumulator: columns [0, N)
@@ -79,6 +80,7 @@ struct GemmParams {
     int SX, SW;              // X / W ring stages
     int C;                   // cluster size: CTAs sharing (multicasting) one X tile
     uint32_t stage_w;        // W stage bytes (one unit)
+    uint32_t bar_bytes;      // barrier + offset area (multiple of 1024)
     uint32_t idesc;
     int dbg;  // SFMP_GEMM_DEBUG bits: 1 skip dequant math, 2 skip MMAs, 4 skip y stores, 8 xprep only, 16 no xprep
 };
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             mbar_init(&aempty[a], 1);
         }
         mbar_init(accfull, 1);
-        mbar_init(accempty, 4);
+        mbar_init(accempty, kEpiWarps);
         fence_mbar_init();
         fence_proxy_async();
     }
@@ -341,43 +343,49 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 accph ^= 1;
             }
         }
-    } else if (warp < 6) {
-        // ---------------- epilogue: TMEM -> coalesced y rows ----------------
-        const int q = warp & 3;
+    } else if (warp < 2 + kEpiWarps) {
+        // ---------------- epilogue: TMEM -> registers -> coalesced y rows ----------------
+        // kEpiWarps/4 warps per TMEM lane quarter, each owning 256/(kEpiWarps/4)
+        // accumulator columns: every warp loads its whole share into registers
+        // and releases the accumulator at once, so the y stores overlap the
+        // next tile's MMAs instead of stalling them.
+        constexpr int kCols = 256 / (kEpiWarps / 4);
+        const int ew = warp - 2, q = warp & 3, cg = ew >> 2;
         int accph = 0, ecount = 0;
         for (int ct = cid; ct < nct; ct += ncl) {
             const int rg = ct / p.TT, tt = ct - rg * p.TT, rt = rg * C + rank;
             mbar_wait(accfull, accph);
-            if ((p.dbg & 32) && blockIdx.x < 2 && q == 2 && lane == 0)
-                g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + (ecount++ & 255)] = gtimer_ns();
+            if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
+                g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + (ecount++ & 127)] = gtimer_ns();
             accph ^= 1;
             tc_fence_after();
-            const int t0 = tt * N;
-            const uint64_t row = static_cast<uint64_t>(rt) * 128 + q * 32 + lane;
-            const bool row_ok = row < p.out_rows;
-#pragma unroll 1
-            for (int c0 = 0; c0 < N; c0 += 32) {
-                uint32_t v[32];
-                tc_ld_x32(tbase + (static_cast<uint32_t>(q * 32) << 16) + kAccCol + c0, v);
-                tc_wait_ld();
-                if (c0 + 32 >= N) {
-                    // accumulator drained: the next tile's MMAs may start
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(accempty);
-                }
-                if (row_ok && !(p.dbg & 4)) {
-                    float* yp = p.y + static_cast<size_t>(t0 + c0) * p.out_rows + row;
-                    const int lim = min(32, min(N - c0, p.M - t0 - c0));
+            const int c_begin = cg * kCols;
+            uint32_t v[kCols / 32][32];
+            if (c_begin < N) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < lim) yp[static_cast<size_t>(j) * p.out_rows] = __uint_as_float(v[j]);
-                }
+                for (int c = 0; c < kCols / 32; ++c)
+                    tc_ld_x32(tbase + (static_cast<uint32_t>(q * 32) << 16) + kAccCol + c_begin + 32 * c, v[c]);
+                tc_wait_ld();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty);
+            if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
+                g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + 128 + ((ecount - 1) & 127)] = gtimer_ns();
+            if (p.dbg & 4) continue;
+            const int t0 = tt * N + c_begin;
+            const uint64_t row = static_cast<uint64_t>(rt) * 128 + q * 32 + lane;
+            const int lim = min(kCols, min(N - c_begin, p.M - t0));
+            if (row < p.out_rows && lim > 0) {
+                float* yp = p.y + static_cast<size_t>(t0) * p.out_rows + row;
+#pragma unroll
+                for (int j = 0; j < kCols; ++j)
+                    if (j < lim) yp[static_cast<size_t>(j) * p.out_rows] = __uint_as_float(v[j >> 5][j & 31]);
             }
         }
     } else {
         // ---------------- dequant: bit-planes -> f16 A operand in TMEM ----------------
-        const int dw = warp - 6, q = warp & 3, kh = dw >> 2;
+        const int dw = warp - 2 - kEpiWarps, q = warp & 3, kh = dw >> 2;
         const int r = q * 32 + lane;  // row within the unit = TMEM lane
         const uint32_t woff = static_cast<uint32_t>(kh * kWords * 4);  // byte offset of this warp's words in a row
         int ws = 0, wph = 0, ab = 0, aph = 0;
@@ -421,30 +429,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
 #pragma unroll
                     for (int i = 0; i < NP; ++i) ldrow(i, u + kUnitHdr + i * kPlaneBytes + r * 16 + woff);
                 }
-                // all math before the TMEM buffer is needed: after aempty only
-                // the tcgen05.st stores sit on the MMA's critical path
-                uint32_t H[kWords][16];
-#pragma unroll
-                for (int w = 0; w < kWords; ++w) {
-                    uint32_t pw[NP];
-#pragma unroll
-                    for (int i = 0; i < NP; ++i) pw[i] = pl[i][w];
-                    if (p.dbg & 1) {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) H[w][j] = 0x3C003C00u;
-                    } else {
-                        dequant_word<NP>(pw, s2, z2, H[w]);
-                    }
-                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&wempty[ws]);  // shared-memory reads of this stage are done
                 if (tl) tl[1 * 256 + (tcount & 255)] = gtimer_ns();
+                // 4 A buffers let dequant run ahead of the MMA, so waiting for the
+                // buffer before the math costs little and keeps registers low
                 mbar_wait(&aempty[ab], aph ^ 1);
                 if (tl) tl[2 * 256 + (tcount & 255)] = gtimer_ns();
                 tc_fence_after();
                 const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + ab * 64 + kh * kWords * 16;
 #pragma unroll
-                for (int w = 0; w < kWords; ++w) tc_st_x16(ta + w * 16, H[w]);
+                for (int w = 0; w < kWords; ++w) {
+                    uint32_t pw[NP];
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) pw[i] = pl[i][w];
+                    uint32_t H[16];
+                    if (p.dbg & 1) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) H[j] = 0x3C003C00u;
+                    } else {
+                        dequant_word<NP>(pw, s2, z2, H);
+                    }
+                    tc_st_x16(ta + w * 16, H);
+                }
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -616,9 +623,11 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     if (const char* e = getenv("SFMP_GEMM_DEBUG")) p.dbg = atoi(e);
     p.stage_w = (unit_max_bytes(m) + 127) / 128 * 128;
     const uint32_t xstage = static_cast<uint32_t>(p.N) * 128;
-    const size_t bar_bytes = 256 + (static_cast<size_t>(p.KC) + 1) * 8;
+    const size_t bar_bytes = (256 + (static_cast<size_t>(p.KC) + 1) * 8 + 1023) / 1024 * 1024;
+    p.bar_bytes = static_cast<uint32_t>(bar_bytes);
+    constexpr size_t kStageBytes = 0;
     // W ring: 4 units; X ring: as many 64-column atoms as the rest holds (<= 8)
-    const size_t avail = kSmemLimit - 1024 - bar_bytes;
+    const size_t avail = kSmemLimit - 1024 - bar_bytes - kStageBytes;
     p.SW = 4;
     p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
     if (p.SX < 2) {
@@ -626,7 +635,7 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
         p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
     }
     if (p.SX < 2) return cudaErrorInvalidConfiguration;
-    const size_t smem = 1024 + p.SX * xstage + p.SW * p.stage_w + bar_bytes;
+    const size_t smem = 1024 + p.SX * xstage + p.SW * p.stage_w + bar_bytes + kStageBytes;
     // K4 (prefill flavour): gather + convert + swizzle X
     const int cols = static_cast<int>(m.cols);
     const int Mpad = p.TT * p.N;

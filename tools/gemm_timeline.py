@@ -40,4 +40,7 @@ for i, nm in enumerate(names[1:4], 1):
 print(f"  deq afull -> mma afull: median {np.median(t[4, :n] - t[3, :n]) / 1e3:.3f} us")
 print(f"  mma commit(k) -> deq aempty(k+2): median {np.median(t[2, 2:n] - t[6, :n-2]) / 1e3:.3f} us")
 print(f"  mma afull -> mma commit: median {np.median(t[6, :n] - t[4, :n]) / 1e3:.3f} us")
-print("epilogue accfull:", (t[7][t[7] > 0] - t0) / 1e3)
+ef = t[7][:128]; er = t[7][128:]
+n_t = int((ef > 0).sum())
+print("epilogue accfull:", (ef[:n_t] - t0) / 1e3)
+print("epilogue acc released after (us):", (er[:n_t] - ef[:n_t]) / 1e3)
