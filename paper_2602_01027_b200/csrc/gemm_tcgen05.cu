@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         int accph = 0, ecount = 0;
         for (int ct = cid; ct < nct; ct += ncl) {
             const int rg = ct / p.TT, tt = ct - rg * p.TT, rt = rg * C + rank;
-            mbar_wait(accfull, accph);
+            mbar_wait_sleep(accfull, accph, 2000);  // a whole tile of MMAs away
             if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
                 g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + (ecount++ & 127)] = gtimer_ns();
             accph ^= 1;
@@ -663,7 +663,9 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (p.dbg & 8) return cudaSuccess;
-    p.C = 4;
+    // Clusters of 4 sharing X by multicast measured no faster and cap the grid
+    // at the co-resident cluster count (132 of 148 SMs): default to 1.
+    p.C = 1;
     if (const char* e = getenv("SFMP_GEMM_CLUSTER")) p.C = std::max(1, std::min(4, atoi(e)));
     while (p.RT % p.C) p.C >>= 1;
     const int nct = (p.RT / p.C) * p.TT;
