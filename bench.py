@@ -505,14 +505,18 @@ def main():
         for M in MS:
             b = algo_bytes(info_local, M, rows_local, SHAPES[p][1])
             step_bytes += b
-    n_gemv = len(MS) * len(PROJS)
+    n_launch = len(MS) if grouped else len(MS) * len(PROJS)  # GEMV launches per step
     t_us = t_ms * 1e3
-    achieved = step_bytes / (t_us * 1e-6) / 1e9  # GB/s (includes launch gaps: conservative)
+    # achieved = algorithmic bytes of one GEMV launch / its share of the step
+    # (each launch's time includes its x pre-pass: a lower bound on the kernel)
+    achieved = step_bytes / (t_us * 1e-6) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemv_grouped_8b_M1.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch_gate_m1")
+            mb = json.load(open(prof))["metrics"]["dram__bytes_read.sum"].split()[0]
+            wb = json.load(open(prof))["metrics"]["dram__bytes_write.sum"].split()[0]
+            traffic = round((float(mb) + float(wb)) * 1e6)  # ncu --set full, grouped M=1 launch
         except Exception:
             traffic = None
     out = {
@@ -535,7 +539,10 @@ def main():
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                      "algorithmic_bytes_per_step": step_bytes,
-                     "avg_launch_us": round(t_us / n_gemv, 3)},
+                     "algorithmic_bytes_per_launch": step_bytes // n_launch,
+                     "traffic_note": "dram read+write of one grouped M=1 gemv_kernel launch "
+                                     "(profiles/r01_ncu_gemv_grouped_8b_M1.json)",
+                     "avg_launch_us": round(t_us / n_launch, 3), "launches_per_step": n_launch},
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": ("pinned host x -> one H2D, sfmp_gemm_grouped per M, one D2H -> pinned host y; "
                        "CUDA graph per step, host synchronises on y every step")},
