@@ -78,7 +78,9 @@ struct GemmParams {
     uint64_t out_rows;
     int floor_bits, has_extra;
     int SX, SW;              // X / W ring stages
-    int C;                   // cluster size: CTAs sharing (multicasting) one X tile
+    int64_t work, Q;         // (tile, kc) steps in all, per CTA (stream-K)
+    int rr;                  // 1: whole tiles round-robin over the grid
+    float* part;             // [grid][2][N][128] f32 stream-K partial tiles
     uint32_t stage_w;        // W stage bytes (one unit)
     uint32_t bar_bytes;      // barrier + offset area (multiple of 1024)
     uint32_t idesc;
@@ -172,6 +174,99 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
     return t;
 }
 
+struct GSeg {
+    int tile, kc0, kc1;
+    bool first;  // first segment of this CTA's range
+};
+// Segments of this CTA: round-robin whole tiles (b, b+G, ...) when p.rr, else
+// the contiguous stream-K range [b*Q, (b+1)*Q) cut at tile boundaries.
+struct SegIter {
+    int64_t w, wend;
+    bool first;
+    __device__ __forceinline__ bool next(const GemmParams& p, GSeg& g) {
+        if (p.rr) {
+            if (w >= p.work) return false;
+            g.tile = static_cast<int>(w / p.KC);
+            g.kc0 = 0;
+            g.kc1 = p.KC;
+            g.first = first;
+            w += static_cast<int64_t>(gridDim.x) * p.KC;
+        } else {
+            if (w >= wend) return false;
+            g.tile = static_cast<int>(w / p.KC);
+            g.kc0 = static_cast<int>(w - static_cast<int64_t>(g.tile) * p.KC);
+            g.kc1 = static_cast<int>(min(static_cast<int64_t>(p.KC), g.kc0 + (wend - w)));
+            g.first = first;
+            w += g.kc1 - g.kc0;
+        }
+        first = false;
+        return true;
+    }
+};
+__device__ __forceinline__ SegIter seg_begin(const GemmParams& p) {
+    SegIter it;
+    it.w = p.rr ? static_cast<int64_t>(blockIdx.x) * p.KC : static_cast<int64_t>(blockIdx.x) * p.Q;
+    it.wend = min(p.work, it.w + p.Q);
+    it.first = true;
+    return it;
+}
+
+// Stream-K fix-up: a tile shared by CTAs c0..c1 gets the sum of their partial
+// tiles in CTA order (deterministic).  CTA c0's part is in slot 1 when its
+// range began in an earlier tile, slot 0 otherwise; the others' parts are
+// their first segments (slot 0).  grid = (N/32, CTA boundaries); boundary b
+// (end of CTA b's range) reduces the tile it falls in if it is that tile's
+// first boundary.
+__global__ void __launch_bounds__(128) gemm_reduce_kernel(const GemmParams p) {
+    const int64_t b = blockIdx.y;
+    const int64_t w = (b + 1) * p.Q;
+    if (w >= p.work) return;
+    const int64_t tile = w / p.KC;
+    const int64_t ts = tile * p.KC;
+    if (w == ts || b != ts / p.Q) return;
+    const int c0 = static_cast<int>(ts / p.Q), c1 = static_cast<int>((ts + p.KC - 1) / p.Q);
+    const int s0 = (static_cast<int64_t>(c0) * p.Q < ts) ? 1 : 0;
+    const int rt = static_cast<int>(tile / p.TT), tt = static_cast<int>(tile - static_cast<int64_t>(rt) * p.TT);
+    const int N = p.N;
+    // warp wi handles tokens j0 + wi + 4k (k < 8); lane l rows 4l..4l+3 (float4)
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j0 = blockIdx.x * 32 + wi;
+    const size_t pstride = static_cast<size_t>(N) * 128;
+    float4 acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = c0; c <= c1; ++c) {  // CTA order: deterministic
+        const float4* src = reinterpret_cast<const float4*>(
+                                p.part + (static_cast<size_t>(c) * 2 + (c == c0 ? s0 : 0)) * pstride +
+                                static_cast<size_t>(j0) * 128) + lane;
+        float4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = (j0 + 4 * k < N) ? __ldcg(src + k * 4 * 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            acc[k].x += v[k].x;
+            acc[k].y += v[k].y;
+            acc[k].z += v[k].z;
+            acc[k].w += v[k].w;
+        }
+    }
+    const uint64_t grow = static_cast<uint64_t>(rt) * 128 + 4 * lane;
+    const bool vec = (p.out_rows % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.y) & 15) == 0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int j = j0 + 4 * k, t = tt * N + j;
+        if (j >= N || t >= p.M) continue;
+        float* yp = p.y + static_cast<size_t>(t) * p.out_rows + grow;
+        if (vec && grow + 4 <= p.out_rows) {
+            *reinterpret_cast<float4*>(yp) = acc[k];
+        } else {
+            const float a[4] = {acc[k].x, acc[k].y, acc[k].z, acc[k].w};
+            for (int e = 0; e < 4; ++e)
+                if (grow + e < p.out_rows) yp[e] = a[e];
+        }
+    }
+}
+
 // Dequantise one 32-weight word of this thread's row into 16 f16x2.
 template <int NP>
 __device__ __forceinline__ void dequant_word(const uint32_t (&p)[NP], __half2 s2, __half2 z2, uint32_t (&H)[16]) {
@@ -209,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < SX; ++s) {
             mbar_init(&xfull[s], 1);
-            mbar_init(&xempty[s], p.C);  // one MMA commit from every CTA of the cluster
+            mbar_init(&xempty[s], 1);
         }
         for (int s = 0; s < SW; ++s) {
             mbar_init(&wfull[s], 1);
@@ -230,19 +325,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     }
     tc_fence_before();
     __syncthreads();
-    if (p.C > 1) cluster_sync_all();  // peers' barriers are initialised before any multicast
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
-    // Work: cluster tiles ct = (row-tile group, token tile); CTA `rank` of a
-    // cluster takes row tile group*C + rank, all ranks walk the same (tt, kc)
-    // sequence so each X atom is fetched once and multicast to all of them.
-    const int C = p.C;
-    const int rank = C > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-    const int cid = blockIdx.x / C, ncl = gridDim.x / C;
-    const int nct = (p.RT / C) * p.TT;
+    // Work: the sequence of (tile, kc) steps, tile = rt * TT + tt, kc inner,
+    // cut into ranges [b*Q, (b+1)*Q), one per CTA.  With enough tiles Q is a
+    // whole number of tiles (plain persistent tiles); when the tiles cannot
+    // fill the SMs, ranges split tiles along K (stream-K): a segment that
+    // covers a whole tile stores y, the others store a partial tile that
+    // gemm_reduce_kernel sums in CTA order (deterministic) afterwards.
     const int KC = p.KC;
-    const uint16_t cmask = static_cast<uint16_t>((1u << C) - 1u);
 
     if (warp == 0) {
         // ---------------- producer ----------------
@@ -251,19 +343,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         const uint64_t pol_w = policy_evict_first();
         int xs = 0, xph = 0, ws = 0, wph = 0;
         bool waited = false;
-        const uint32_t xslice = xstage / C;
-        for (int ct = cid; ct < nct; ct += ncl) {
-            const int rg = ct / p.TT, tt = ct - rg * p.TT, rt = rg * C + rank;
-            const uint64_t* off0 = p.woff + static_cast<size_t>(rt) * KC;
+        SegIter it = seg_begin(p);
+        for (GSeg sg; it.next(p, sg);) {
+            const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
+            const uint64_t* off0 = p.woff + static_cast<size_t>(rt) * KC + sg.kc0;
             __syncwarp();
-            for (int i = lane; i <= KC; i += 32) offs[i] = __ldg(off0 + i);
+            for (int i = lane; i <= sg.kc1 - sg.kc0; i += 32) offs[i] = __ldg(off0 + i);
             __syncwarp();
             if (lane == 0) {
-                for (int kc = 0; kc < KC; ++kc) {
+                for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                     // weights (independent of the X pre-pass)
                     mbar_wait(&wempty[ws], wph ^ 1);
-                    const uint64_t a0 = offs[kc];
-                    const uint32_t n0 = static_cast<uint32_t>(offs[kc + 1] - a0);
+                    const uint64_t a0 = offs[kc - sg.kc0];
+                    const uint32_t n0 = static_cast<uint32_t>(offs[kc - sg.kc0 + 1] - a0);
                     mbar_arrive_expect_tx(&wfull[ws], n0);
                     bulk_g2s(wbuf + static_cast<size_t>(ws) * p.stage_w, p.wl + a0, n0, &wfull[ws], pol_w);
                     if (++ws == SW) { ws = 0; wph ^= 1; }
@@ -273,24 +365,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                         waited = true;
                     }
                     for (int h = 0; h < 2; ++h) {
-                        // slot free in every CTA of the cluster (xempty counts C commits)
                         mbar_wait(&xempty[xs], xph ^ 1);
                         mbar_arrive_expect_tx(&xfull[xs], xstage);
-                        const uint32_t xdst = smem_u32(xbuf + static_cast<size_t>(xs) * xstage) + rank * xslice;
-                        const uint8_t* xsrc = p.xs + ((static_cast<size_t>(tt) * KC + kc) * 2 + h) * xstage + rank * xslice;
-                        if (C > 1) {
-                            asm volatile(
-                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-                                "[%0], [%1], %2, [%3], %4;" ::"r"(xdst),
-                                "l"(xsrc), "r"(xslice), "r"(smem_u32(&xfull[xs])), "h"(cmask)
-                                : "memory");
-                        } else {
-                            asm volatile(
-                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-                                "[%3];" ::"r"(xdst),
-                                "l"(xsrc), "r"(xslice), "r"(smem_u32(&xfull[xs]))
-                                : "memory");
-                        }
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                smem_u32(xbuf + static_cast<size_t>(xs) * xstage)),
+                            "l"(p.xs + ((static_cast<size_t>(tt) * KC + kc) * 2 + h) * xstage), "r"(xstage),
+                            "r"(smem_u32(&xfull[xs]))
+                            : "memory");
                         if (++xs == SX) { xs = 0; xph ^= 1; }
                     }
                 }
@@ -307,10 +389,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             int tcount = 0;
             const uint32_t idesc = p.idesc;
             const bool do_mma = !(p.dbg & 2);
-            for (int ct = cid; ct < nct; ct += ncl) {
+            SegIter it = seg_begin(p);
+            for (GSeg sg; it.next(p, sg);) {
                 mbar_wait(accempty, accph ^ 1);
                 tc_fence_after();
-                for (int kc = 0; kc < KC; ++kc, ++tcount) {
+                for (int kc = sg.kc0; kc < sg.kc1; ++kc, ++tcount) {
                     mbar_wait(&afull[ab], aph);
                     if (tl) tl[4 * 256 + (tcount & 255)] = gtimer_ns();
                     tc_fence_after();
@@ -325,10 +408,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
                                     tc_mma_ts(tbase + kAccCol, a0 + (h * 4 + kk) * 8, bdesc + 2 * kk, idesc,
-                                              (kc | h | kk) != 0);
+                                              ((kc - sg.kc0) | h | kk) != 0);
                             }
-                            if (C > 1) tc_commit_mc(&xempty[xs], cmask);  // frees the slot in every CTA's view
-                            else tc_commit(&xempty[xs]);
+                            tc_commit(&xempty[xs]);
                         }
                         __syncwarp();
                         if (++xs == SX) { xs = 0; xph ^= 1; }
@@ -352,8 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         constexpr int kCols = 256 / (kEpiWarps / 4);
         const int ew = warp - 2, q = warp & 3, cg = ew >> 2;
         int accph = 0, ecount = 0;
-        for (int ct = cid; ct < nct; ct += ncl) {
-            const int rg = ct / p.TT, tt = ct - rg * p.TT, rt = rg * C + rank;
+        SegIter it = seg_begin(p);
+        for (GSeg sg; it.next(p, sg);) {
+            const int slot = sg.first ? 0 : 1;  // partial slot: first / last segment of the range
+            const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
             mbar_wait_sleep(accfull, accph, 2000);  // a whole tile of MMAs away
             if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
                 g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + (ecount++ & 127)] = gtimer_ns();
@@ -375,13 +459,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             if (p.dbg & 4) continue;
             const int t0 = tt * N + c_begin;
             const uint64_t row = static_cast<uint64_t>(rt) * 128 + q * 32 + lane;
-            const int lim = min(kCols, min(N - c_begin, p.M - t0));
-            if (row < p.out_rows && lim > 0) {
-                float* yp = p.y + static_cast<size_t>(t0) * p.out_rows + row;
-#pragma unroll
-                for (int j = 0; j < kCols; ++j)
-                    if (j < lim) yp[static_cast<size_t>(j) * p.out_rows] = __uint_as_float(v[j >> 5][j & 31]);
+            int lim = min(kCols, min(N - c_begin, p.M - t0));
+            // whole-tile segment -> y[t][row]; else partial [t][128 rows] of this CTA's slot
+            const bool full = sg.kc0 == 0 && sg.kc1 == KC;
+            float* yp;
+            size_t ld;
+            if (full) {
+                yp = p.y + static_cast<size_t>(t0) * p.out_rows + row;
+                ld = p.out_rows;
+                if (row >= p.out_rows) lim = 0;
+            } else {
+                yp = p.part + (static_cast<size_t>(blockIdx.x) * 2 + slot) * (static_cast<size_t>(N) * 128) +
+                     static_cast<size_t>(c_begin) * 128 + q * 32 + lane;
+                ld = 128;
             }
+#pragma unroll
+            for (int j = 0; j < kCols; ++j)
+                if (j < lim) yp[static_cast<size_t>(j) * ld] = __uint_as_float(v[j >> 5][j & 31]);
         }
     } else {
         // ---------------- dequant: bit-planes -> f16 A operand in TMEM ----------------
@@ -392,8 +486,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         unsigned long long* tl = ((p.dbg & 32) && blockIdx.x < 2 && dw == 0 && lane == 0)
                                      ? g_gemm_tl + blockIdx.x * 8 * 256 : nullptr;
         int tcount = 0;
-        for (int ct = cid; ct < nct; ct += ncl) {
-            for (int kc = 0; kc < KC; ++kc) {
+        SegIter it = seg_begin(p);
+        for (GSeg sg; it.next(p, sg);) {
+            for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                 mbar_wait(&wfull[ws], wph);
                 if (tl) tl[0 * 256 + (tcount & 255)] = gtimer_ns();
                 const uint32_t u = smem_u32(wbuf + static_cast<size_t>(ws) * p.stage_w);
@@ -465,8 +560,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     }
     tc_fence_before();
     __syncthreads();
-    // no CTA may leave while a peer can still multicast into it / arrive on it
-    if (p.C > 1) cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
         tc_dealloc(tbase, kTmemCols);
@@ -488,10 +581,9 @@ uint32_t unit_max_bytes(const DevModel& m) {
 }
 
 template <int NP>
-cudaError_t launch_np(const GemmParams& p, size_t smem, int nct, int num_sms, cudaStream_t st) {
+cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
     auto k = gemm_kernel<NP>;
     static int configured[64] = {0};
-    static int max_clusters[64][5] = {{0}};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !configured[dev]) {
@@ -500,33 +592,22 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int nct, int num_sms, cu
         configured[dev] = 1;
     }
     cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = static_cast<unsigned>(p.C);
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    // persistent grid: as many clusters as can be co-resident (GPC packing
-    // may allow fewer than num_sms / C)
-    int& mc = max_clusters[dev < 64 ? dev : 0][p.C];
-    if (mc == 0) {
-        cfg.gridDim = dim3(p.C * (num_sms / p.C));
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
-            cudaGetLastError();
-            n = num_sms / p.C;
-        }
-        mc = n;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, p);
+    if (e != cudaSuccess) return e;
+    if (!p.rr && p.Q % p.KC != 0) {  // some tiles are split along K: stream-K fix-up
+        gemm_reduce_kernel<<<dim3((p.N + 31) / 32, grid), 128, 0, st>>>(p);
+        e = cudaGetLastError();
     }
-    const int ncl = std::max(1, std::min(nct, mc));
-    cfg.gridDim = dim3(ncl * p.C);
-    return cudaLaunchKernelEx(&cfg, k, p);
+    return e;
 }
 
 }  // namespace
@@ -543,8 +624,7 @@ extern "C" int sfmp_debug_gemm_timeline(unsigned long long* host, size_t n) {
 bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const std::vector<uint32_t>& out_map,
                        std::vector<uint8_t>& wl, std::vector<uint64_t>& woff) {
     if (d.n_b % 128 != 0 || d.cols % 128 != 0 || d.out_rows == 0) return false;
-    // row tiles padded to a multiple of 4 so clusters of up to 4 CTAs tile them
-    const uint64_t KC = d.cols / 128, RT2 = (d.out_rows + 511) / 512 * 4;
+    const uint64_t KC = d.cols / 128, RT2 = (d.out_rows + 127) / 128;
     const uint32_t TR = d.TR, nb8 = d.n_b / 8;
     const uint64_t plane_unit = static_cast<uint64_t>(TR) * nb8;
     std::vector<uint32_t> inv(RT2 * 128, 0xFFFFFFFFu);
@@ -598,10 +678,14 @@ bool gemm_supported(const DevModel& m) {
     return m.d_gl != nullptr && m.d_xslot != nullptr && m.cols * 2 <= static_cast<uint64_t>(kSmemLimit) && m.ceil_bits >= 1 && m.ceil_bits <= 8 && m.cols < (1ull << 31);
 }
 
-size_t gemm_workspace_bytes(const DevModel& m, int64_t M) {
+// Workspace: swizzled X images | stream-K partial tiles [grid <= num_sms][2][N][128] f32.
+size_t gemm_x_bytes(const DevModel& m, int64_t M) {
     const int N = tile_n(M);
     const int64_t TT = (M + N - 1) / N;
-    return static_cast<size_t>(TT) * N * m.cols * 2;
+    return (static_cast<size_t>(TT) * N * m.cols * 2 + 255) / 256 * 256;
+}
+size_t gemm_workspace_bytes(const DevModel& m, int64_t M) {
+    return gemm_x_bytes(m, M) + static_cast<size_t>(m.num_sms) * 2 * tile_n(M) * 128 * 4;
 }
 
 cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y, void* ws,
@@ -615,6 +699,7 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     p.wl = m.d_gl;
     p.woff = m.d_gl_off;
     p.xs = static_cast<const uint8_t*>(ws);
+    p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + gemm_x_bytes(m, M));
     p.y = y;
     p.out_rows = m.out_rows;
     p.floor_bits = m.floor_bits;
@@ -663,22 +748,31 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (p.dbg & 8) return cudaSuccess;
-    // Clusters of 4 sharing X by multicast measured no faster and cap the grid
-    // at the co-resident cluster count (132 of 148 SMs): default to 1.
-    p.C = 1;
-    if (const char* e = getenv("SFMP_GEMM_CLUSTER")) p.C = std::max(1, std::min(4, atoi(e)));
-    while (p.RT % p.C) p.C >>= 1;
-    const int nct = (p.RT / p.C) * p.TT;
-    const int S = m.num_sms;
+    // (Clusters of 4 sharing X by TMA multicast measured no faster and capped the
+    // grid at the co-resident cluster count, 132 of 148 SMs: not used.)
+    // Whole tiles per CTA when they fill the SMs (measured: splitting big
+    // tile counts along K costs more than the wave it saves); stream-K when
+    // there are fewer tiles than SMs (small M, k/v): >= 8 steps per CTA.
+    const int64_t ntiles = static_cast<int64_t>(p.RT) * p.TT;
+    p.work = ntiles * p.KC;
+    const int sms = m.num_sms;
+    p.rr = ntiles * 4 > sms ? 1 : 0;  // measured: stream-K pays off only when tiles << SMs
+    if (const char* e = getenv("SFMP_GEMM_SK")) p.rr = atoi(e) ? 0 : 1;
+    p.Q = p.KC;
+    int S = static_cast<int>(std::min<int64_t>(ntiles, sms));
+    if (!p.rr) {
+        p.Q = std::max<int64_t>(std::min<int64_t>(p.KC, 8), (p.work + sms - 1) / sms);
+        S = static_cast<int>((p.work + p.Q - 1) / p.Q);
+    }
     switch (m.ceil_bits) {
-        case 1: return launch_np<1>(p, smem, nct, S, st);
-        case 2: return launch_np<2>(p, smem, nct, S, st);
-        case 3: return launch_np<3>(p, smem, nct, S, st);
-        case 4: return launch_np<4>(p, smem, nct, S, st);
-        case 5: return launch_np<5>(p, smem, nct, S, st);
-        case 6: return launch_np<6>(p, smem, nct, S, st);
-        case 7: return launch_np<7>(p, smem, nct, S, st);
-        default: return launch_np<8>(p, smem, nct, S, st);
+        case 1: return launch_np<1>(p, smem, S, st);
+        case 2: return launch_np<2>(p, smem, S, st);
+        case 3: return launch_np<3>(p, smem, S, st);
+        case 4: return launch_np<4>(p, smem, S, st);
+        case 5: return launch_np<5>(p, smem, S, st);
+        case 6: return launch_np<6>(p, smem, S, st);
+        case 7: return launch_np<7>(p, smem, S, st);
+        default: return launch_np<8>(p, smem, S, st);
     }
 }
 
