@@ -45,7 +45,7 @@ namespace sfmpk {
 namespace {
 
 constexpr int kTR = 128;  // rows per unit
-constexpr int kMT = 1;            // m16 tiles (16 rows each) per compute warp
+constexpr int kMT = 2;            // m16 tiles (16 rows each) per compute warp
 constexpr int kNCW = 8 / kMT;     // compute warps per 128-row tile
 constexpr int kThreads = 32 * (1 + kNCW);
 constexpr int kHdrBytes = 1280;  // barriers | zeros | stage bit-widths | out_map
