@@ -756,7 +756,11 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     const int64_t ntiles = static_cast<int64_t>(p.RT) * p.TT;
     p.work = ntiles * p.KC;
     const int sms = m.num_sms;
-    p.rr = ntiles * 4 > sms ? 1 : 0;  // measured: stream-K pays off only when tiles << SMs
+    // measured (tools/sweep.py, prof_gemm.py): stream-K pays off when the tiles
+    // leave most SMs idle (<= 1/4 busy) or leave SMs idle while each CTA still
+    // gets a long K range (>= 32 steps); otherwise whole tiles round-robin
+    const bool sk = ntiles * 4 <= sms || (ntiles < sms && (p.work + sms - 1) / sms >= 32);
+    p.rr = sk ? 0 : 1;
     if (const char* e = getenv("SFMP_GEMM_SK")) p.rr = atoi(e) ? 0 : 1;
     p.Q = p.KC;
     int S = static_cast<int>(std::min<int64_t>(ntiles, sms));
