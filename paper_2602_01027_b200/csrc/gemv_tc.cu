@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
 // 32-bit shared addresses; all other offsets are compile-time immediates.
 template <int B, int NT, int CH>
 __device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[NT], int chunk_bytes, int c,
-                                           float (&cacc)[2 * kMT][NT][4]) {
+                                           float (&cacc)[kMT][NT][4]) {
     constexpr int NB8 = CH * 16;   // bytes of one row of one plane
     constexpr int PS = kTR * NB8;  // bytes of one plane of the unit
     // rows r0 + 8*r: (r0, r0+8) is m-tile 0, (r0+16, r0+24) m-tile 1
@@ -262,7 +262,7 @@ __device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[N
             const uint2 b = lds_v2(xb[nt] + c * chunk_bytes + s * 32);
 #pragma unroll
             for (int m = 0; m < kMT; ++m)
-                mma_16816(cacc[2 * m + (s & 1)][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
+                mma_16816(cacc[m][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
                           A[2 * m + 1][2 * s + 1], b.x, b.y);
         }
     }
@@ -435,9 +435,9 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + s * xstep[nt];
                 const uint32_t prow = prow0 + s * stage_w;
-                float cacc[2 * kMT][NT][4];
+                float cacc[kMT][NT][4];
 #pragma unroll
-                for (int h = 0; h < 2 * kMT; ++h)
+                for (int h = 0; h < kMT; ++h)
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -462,12 +462,11 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                     for (int nt = 0; nt < NT; ++nt) {
                         const float2 xg01 = lds_f2(xg + 32 * nt);
                         const float2 b01 = lds_f2(xg + boff + 32 * nt);
-                        const float* c0 = cacc[2 * m][nt];
-                        const float* c1 = cacc[2 * m + 1][nt];
-                        yacc[m][nt][0] += sa * ((c0[0] + c1[0]) - b01.x) + za * xg01.x;
-                        yacc[m][nt][1] += sa * ((c0[1] + c1[1]) - b01.y) + za * xg01.y;
-                        yacc[m][nt][2] += sb * ((c0[2] + c1[2]) - b01.x) + zb * xg01.x;
-                        yacc[m][nt][3] += sb * ((c0[3] + c1[3]) - b01.y) + zb * xg01.y;
+                        const float* c0 = cacc[m][nt];
+                        yacc[m][nt][0] += sa * (c0[0] - b01.x) + za * xg01.x;
+                        yacc[m][nt][1] += sa * (c0[1] - b01.y) + za * xg01.y;
+                        yacc[m][nt][2] += sb * (c0[2] - b01.x) + zb * xg01.x;
+                        yacc[m][nt][3] += sb * (c0[3] - b01.y) + zb * xg01.y;
                     }
                 }
                 __syncwarp();
