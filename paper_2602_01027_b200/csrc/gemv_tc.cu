@@ -47,10 +47,17 @@ namespace {
 constexpr int kTR = 128;  // rows per unit
 constexpr int kMT = 2;            // m16 tiles (16 rows each) per compute warp
 constexpr int kNCW = 8 / kMT;     // compute warps per 128-row tile
+#ifndef SFMP_GEMV_CTAS1
+#define SFMP_GEMV_CTAS1 4
+#endif
+#ifndef SFMP_GEMV_CTAS2
+#define SFMP_GEMV_CTAS2 3
+#endif
+constexpr int kCtasNT1 = SFMP_GEMV_CTAS1, kCtasNT2 = SFMP_GEMV_CTAS2;  // resident CTAs per SM
 constexpr int kThreads = 32 * (1 + kNCW);
 constexpr int kHdrBytes = 1280;  // barriers | zeros | stage bit-widths | out_map
 // resident CTAs per SM: 4 for M<=8 (NT=1), 3 for M<=16 (NT=2, more registers)
-__host__ __device__ constexpr int ctas_per_sm(int NT) { return kMT == 2 ? (NT == 1 ? 4 : 3) : (NT == 1 ? 3 : 2); }
+__host__ __device__ constexpr int ctas_per_sm(int NT) { return kMT == 2 ? (NT == 1 ? kCtasNT1 : kCtasNT2) : (NT == 1 ? 3 : 2); }
 __host__ __device__ constexpr int smem_per_cta(int NT) { return (225 * 1024) / ctas_per_sm(NT); }
 
 // One linear of a (possibly grouped) launch: independent matrices -- e.g. the
