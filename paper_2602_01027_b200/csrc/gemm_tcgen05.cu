@@ -111,7 +111,7 @@ __device__ __forceinline__ float ldx(const void* x, size_t i) {
 // (xslot[kc*128 + s] = col_perm[kc*128 + slot_col(s)], built at upload).
 // Tokens M..TT*N-1 of the last tile are written as zeros.
 template <sfmp_dtype DT>
-__global__ void __launch_bounds__(256) xprep_gemm_kernel(const void* __restrict__ x, const uint32_t* __restrict__ xslot,
+__global__ void __launch_bounds__(1024) xprep_gemm_kernel(const void* __restrict__ x, const uint32_t* __restrict__ xslot,
                                                          uint8_t* __restrict__ xs, int M, int N, int KC, int cols,
                                                          int Mpad) {
     extern __shared__ __align__(16) __half xrow[];
@@ -724,7 +724,11 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     // K4 (prefill flavour): gather + convert + swizzle X
     const int cols = static_cast<int>(m.cols);
     const int Mpad = p.TT * p.N;
-    const int xgrid = std::min(Mpad, m.num_sms * 8);
+    // one token per CTA (all resident at once for the usual shapes): the pass
+    // costs about one token's load-gather-store latency instead of a loop
+    int xthreads = 128;
+    if (const char* e = getenv("SFMP_XPREP_THREADS")) xthreads = std::max(32, std::min(1024, atoi(e)));
+    const int xgrid = Mpad;
     const size_t xsm = static_cast<size_t>(cols) * 2;
     uint8_t* xs = static_cast<uint8_t*>(ws);
     if (!(p.dbg & 16)) {
@@ -732,15 +736,15 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
         switch (dt) {
             case SFMP_F32:
                 e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                xprep_gemm_kernel<SFMP_F32><<<xgrid, 256, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                xprep_gemm_kernel<SFMP_F32><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
                 break;
             case SFMP_F16:
                 e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                xprep_gemm_kernel<SFMP_F16><<<xgrid, 256, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                xprep_gemm_kernel<SFMP_F16><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
                 break;
             default:
                 e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                xprep_gemm_kernel<SFMP_BF16><<<xgrid, 256, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                xprep_gemm_kernel<SFMP_BF16><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
                 break;
         }
         if (e0 != cudaSuccess) return e0;
