@@ -298,7 +298,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     uint64_t* accfull = aempty + kNA;  // [1]
     uint64_t* accempty = accfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
-    uint64_t* offs = accempty + 2;  // [KC + 1] unit offsets of the producer's current row tile
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -337,33 +336,37 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     const int KC = p.KC;
 
     if (warp == 0) {
-        // ---------------- producer ----------------
-        // Unit offsets of the current row tile are staged in shared memory by
-        // the whole warp, so lane 0 never waits on a global load between copies.
+        // ---------------- producers ----------------
+        // Lane 0 streams the weight units, lane 1 the X atoms, each gated only
+        // by its own ring: the weights no longer wait for X slots (which free
+        // only as MMAs complete), so dequantisation can run ahead.  Lane 0
+        // reads each segment's unit offsets straight from global memory, the
+        // loads for a segment issued together (one latency per segment).
         const uint64_t pol_w = policy_evict_first();
-        int xs = 0, xph = 0, ws = 0, wph = 0;
-        bool waited = false;
-        SegIter it = seg_begin(p);
-        for (GSeg sg; it.next(p, sg);) {
-            const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
-            const uint64_t* off0 = p.woff + static_cast<size_t>(rt) * KC + sg.kc0;
-            __syncwarp();
-            for (int i = lane; i <= sg.kc1 - sg.kc0; i += 32) offs[i] = __ldg(off0 + i);
-            __syncwarp();
-            if (lane == 0) {
+        if (lane == 0) {
+            int ws = 0, wph = 0;
+            SegIter it = seg_begin(p);
+            for (GSeg sg; it.next(p, sg);) {
+                const int rt = sg.tile / p.TT;
+                const uint64_t* off0 = p.woff + static_cast<size_t>(rt) * KC + sg.kc0;
+                uint64_t a_next = __ldg(off0);
                 for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
-                    // weights (independent of the X pre-pass)
+                    const uint64_t a0 = a_next;
+                    a_next = __ldg(off0 + (kc - sg.kc0) + 1);
+                    const uint32_t n0 = static_cast<uint32_t>(a_next - a0);
                     mbar_wait(&wempty[ws], wph ^ 1);
-                    const uint64_t a0 = offs[kc - sg.kc0];
-                    const uint32_t n0 = static_cast<uint32_t>(offs[kc - sg.kc0 + 1] - a0);
                     mbar_arrive_expect_tx(&wfull[ws], n0);
                     bulk_g2s(wbuf + static_cast<size_t>(ws) * p.stage_w, p.wl + a0, n0, &wfull[ws], pol_w);
                     if (++ws == SW) { ws = 0; wph ^= 1; }
-                    // activations: the two 64-column atoms of this chunk
-                    if (!waited) {
-                        pdl_wait();
-                        waited = true;
-                    }
+                }
+            }
+        } else if (lane == 1) {
+            int xs = 0, xph = 0;
+            pdl_wait();  // X is written by the pre-pass (programmatic dependent launch)
+            SegIter it = seg_begin(p);
+            for (GSeg sg; it.next(p, sg);) {
+                const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
+                for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                     for (int h = 0; h < 2; ++h) {
                         mbar_wait(&xempty[xs], xph ^ 1);
                         mbar_arrive_expect_tx(&xfull[xs], xstage);
@@ -713,8 +716,13 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     constexpr size_t kStageBytes = 0;
     // W ring: 4 units; X ring: as many 64-column atoms as the rest holds (<= 8)
     const size_t avail = kSmemLimit - 1024 - bar_bytes - kStageBytes;
-    p.SW = 4;
+    p.SW = 8;
+    if (const char* e = getenv("SFMP_GEMM_SW")) p.SW = std::max(2, std::min(8, atoi(e)));
     p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
+    while (p.SX < 4 && p.SW > 4) {
+        --p.SW;
+        p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
+    }
     if (p.SX < 2) {
         p.SW = 2;
         p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));

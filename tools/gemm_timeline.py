@@ -31,7 +31,7 @@ n = int((t[4] > 0).sum())
 t0 = t[0, 0]
 names = ["deq wfull", "deq math", "deq aempty", "deq afull", "mma afull", "mma xfull", "mma commit"]
 print(f"{proj} M={M}: {n} units on CTA 0; times rel. to first wfull (us)")
-for k in list(range(0, min(n, 6))) + list(range(max(6, n - 3), n)):
+for k in list(range(0, min(n, 4))) + list(range(28, min(n, 38))) + list(range(max(6, n - 3), n)):
     print(f"unit {k:3d}: " + " ".join(f"{nm}={(t[i, k] - t0) / 1e3:7.2f}" for i, nm in enumerate(names)))
 d = np.diff(t[4, :n]) / 1e3
 print(f"mma afull-to-afull interval us: median {np.median(d):.3f} p90 {np.percentile(d, 90):.3f}")
