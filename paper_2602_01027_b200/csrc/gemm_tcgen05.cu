@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                     const uint64_t a0 = a_next;
                     a_next = __ldg(off0 + (kc - sg.kc0) + 1);
                     const uint32_t n0 = static_cast<uint32_t>(a_next - a0);
-                    mbar_wait(&wempty[ws], wph ^ 1);
+                    mbar_wait_sleep(&wempty[ws], wph ^ 1, 500);
                     mbar_arrive_expect_tx(&wfull[ws], n0);
                     bulk_g2s(wbuf + static_cast<size_t>(ws) * p.stage_w, p.wl + a0, n0, &wfull[ws], pol_w);
                     if (++ws == SW) { ws = 0; wph ^= 1; }
@@ -368,7 +368,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
                 for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                     for (int h = 0; h < 2; ++h) {
-                        mbar_wait(&xempty[xs], xph ^ 1);
+                        mbar_wait_sleep(&xempty[xs], xph ^ 1, 200);
+                        if (p.dbg & 256) {  // probe: no X traffic
+                            mbar_arrive(&xfull[xs]);
+                            if (++xs == SX) { xs = 0; xph ^= 1; }
+                            continue;
+                        }
                         mbar_arrive_expect_tx(&xfull[xs], xstage);
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         SegIter it = seg_begin(p);
         for (GSeg sg; it.next(p, sg);) {
             for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
-                mbar_wait(&wfull[ws], wph);
+                mbar_wait_sleep(&wfull[ws], wph, 200);
                 if (tl) tl[0 * 256 + (tcount & 255)] = gtimer_ns();
                 const uint32_t u = smem_u32(wbuf + static_cast<size_t>(ws) * p.stage_w);
                 const __half2 s2 = __half2half2(__ushort_as_half(lds_u16(u + 2 * r)));
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 if (tl) tl[1 * 256 + (tcount & 255)] = gtimer_ns();
                 // 4 A buffers let dequant run ahead of the MMA, so waiting for the
                 // buffer before the math costs little and keeps registers low
-                mbar_wait(&aempty[ab], aph ^ 1);
+                mbar_wait_sleep(&aempty[ab], aph ^ 1, 300);
                 if (tl) tl[2 * 256 + (tcount & 255)] = gtimer_ns();
                 tc_fence_after();
                 const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + ab * 64 + kh * kWords * 16;

@@ -44,3 +44,10 @@ ef = t[7][:128]; er = t[7][128:]
 n_t = int((ef > 0).sum())
 print("epilogue accfull:", (ef[:n_t] - t0) / 1e3)
 print("epilogue acc released after (us):", (er[:n_t] - ef[:n_t]) / 1e3)
+# per position-in-tile intervals (KC units per tile assumed 32)
+iv = np.diff(t[4, :n]) / 1e3
+pos = np.arange(1, n) % 32
+for kpos in range(32):
+    sel = iv[pos == kpos]
+    if len(sel):
+        print(f"  kc={kpos:2d}: afull interval median {np.median(sel):.3f} us; wfull-lead {np.median((t[4, 1:n][pos == kpos] - t[0, 1:n][pos == kpos]) / 1e3):.2f} us")

@@ -21,7 +21,16 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int bu
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 196608);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3C003C00u;  // 1.0h
+    // mode bit 3: random f16 data (|v| in ~[0.01, 2], random signs) instead of 1.0
+    for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) {
+        uint32_t v = 0x3C003C00u;
+        if (mode & 8) {
+            uint32_t h = (i * 2654435761u) ^ (blockIdx.x * 97u);
+            h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+            v = (h & 0x83FF83FFu) | 0x30003000u;  // exponent 12: values ~[0.125, 0.25) with random sign/mantissa
+        }
+        reinterpret_cast<uint32_t*>(smem)[i] = v;
+    }
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         mbar_init(bar + 1, 1);
@@ -35,6 +44,19 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int bu
     __syncthreads();
     tc_fence_after();
     const uint32_t tb = *slot;
+    if ((mode & 8) && warp >= 4 && warp < 8) {  // random A in TMEM columns 256..511
+        uint32_t v[16];
+        for (int j = 0; j < 16; ++j) {
+            uint32_t h = (threadIdx.x * 31u + j * 7919u) * 2654435761u;
+            h ^= h >> 15;
+            v[j] = (h & 0x83FF83FFu) | 0x2C002C00u;
+        }
+        for (int c = 0; c < 256; c += 16) tc_st_x16(tb + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 256 + c, v);
+        tc_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
     if (warp == 1 && lane == 0) {
         const uint32_t idesc = tc_idesc_f16(128, n);
         const uint64_t bdesc = tc_desc_sw128(smem_u32(smem));
@@ -90,7 +112,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&gsrc, 64 << 20);
     cudaMemset(gsrc, 0, 64 << 20);
     const int iters = 4096;
-    for (int mode : {0, 1, 3, 5, 7})
+    for (int mode : {0, 8, 15})
     for (int ss = 0; ss < 2; ++ss)
         for (int n : {128, 256})
             for (int busy : {0}) {
