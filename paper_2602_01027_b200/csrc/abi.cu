@@ -594,9 +594,11 @@ sfmp_status sfmp_workspace_size(const sfmp_dev_model* model, int64_t M, sfmp_pat
     if (!model || !bytes) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
     const DevModel& d = *reinterpret_cast<const DevModel*>(model);
     size_t b = 0;
+    // (AUTO may still pick the GEMV for M > 16 when x is misaligned: size for both)
     const bool gemm = (path == SFMP_PATH_GEMM) || (path == SFMP_PATH_AUTO && M > 16 && d.gemm_ok);
     if (gemm) b = sfmpk::gemm_workspace_bytes(d, M);
-    else if (path != SFMP_PATH_GENERIC && d.gemv_ok) b = sfmpk::gemv_workspace_bytes(d, 16);
+    if (path != SFMP_PATH_GENERIC && path != SFMP_PATH_GEMM && d.gemv_ok)
+        b = std::max(b, sfmpk::gemv_workspace_bytes(d, 16));
     *bytes = b;
     return SFMP_OK;
 }
@@ -613,7 +615,12 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
     const DevModel& d = *reinterpret_cast<const DevModel*>(model);
     DeviceGuard guard(d.device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (path == SFMP_PATH_AUTO) path = (M > 16 && d.gemm_ok) ? SFMP_PATH_GEMM : (d.gemv_ok ? SFMP_PATH_GEMV : SFMP_PATH_GENERIC);
+    // the tensor-core pre-pass reads x rows with 16-byte vector loads
+    const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    if (path == SFMP_PATH_AUTO)
+        path = (M > 16 && d.gemm_ok && x_aligned) ? SFMP_PATH_GEMM : (d.gemv_ok ? SFMP_PATH_GEMV : SFMP_PATH_GENERIC);
+    if (path == SFMP_PATH_GEMM && !x_aligned)
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "GEMM path needs x 16-byte aligned");
     cudaError_t e = cudaSuccess;
     const size_t esz = dtype == SFMP_F32 ? 4 : 2;
     switch (path) {

@@ -101,3 +101,19 @@ def test_llama8b_prefill_parity(gpu, port, proj):
     ref = port.matmul(np.ascontiguousarray(x[sample]), port.load(data).dequantize(), threads=8)
     e_max, e_l2 = errors(y[sample], ref)
     assert e_max <= TOL, (proj, e_max, e_l2)
+
+
+def test_gemm_misaligned_x_routes_to_gemv(gpu, port):
+    """AUTO with a non-16-byte-aligned x takes the decode path (same result);
+    forcing the tensor-core path on it is an argument error, not a fault."""
+    import torch
+    data = model_bytes(port, 1024, 512, 3.5)
+    dm = gpu.DeviceModel(data)
+    buf = torch.from_numpy(activations(port, 40, 512 + 1, seed=2)).cuda()
+    x = buf.reshape(-1)[1:1 + 40 * 512].view(40, 512)  # 4-byte offset: misaligned for 16 B loads
+    assert x.data_ptr() % 16 != 0
+    ref = port.matmul(x.cpu().numpy(), port.load(data).dequantize(), threads=8)
+    y = dm.gemm(x).cpu().numpy()
+    assert errors(y, ref)[0] <= TOL
+    with pytest.raises(gpu.SfmpError):
+        dm.gemm(x, path=gpu.PATH_GEMM)
