@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         for (GSeg sg; it.next(p, sg);) {
             const int slot = sg.first ? 0 : 1;  // partial slot: first / last segment of the range
             const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
-            mbar_wait_sleep(accfull, accph, 2000);  // a whole tile of MMAs away
+            mbar_wait_sleep(accfull, accph, 200);  // a whole tile of MMAs away: sleep between polls
             if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
                 g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + (ecount++ & 127)] = gtimer_ns();
             accph ^= 1;
