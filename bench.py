@@ -196,6 +196,48 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# dense cuBLAS comparison (the paper's kernel comparison):
+# the same decode step with dense bf16 weights through torch.matmul (cuBLAS)
+# ---------------------------------------------------------------------------
+def dense_leg(dev, stream, xs, args):
+    import torch
+    copies = 2  # 2 x 436 MB of dense weights >> L2
+    W = [{p: torch.randn(SHAPES[p][0], SHAPES[p][1], device=dev, dtype=torch.bfloat16) * 0.02 for p in PROJS}
+         for _ in range(copies)]
+    ys = {(p, M): torch.empty(M, SHAPES[p][0], device=dev, dtype=torch.bfloat16) for p in PROJS for M in MS}
+
+    def step(i):
+        for mi, M in enumerate(MS):
+            c = (i * len(MS) + mi) % copies
+            for p in PROJS:
+                torch.matmul(xs[(p, M)], W[c][p].t(), out=ys[(p, M)])
+
+    with torch.cuda.stream(stream):
+        step(0)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(copies):
+            step(i)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (reps * copies)
+    del W
+    torch.cuda.empty_cache()
+    byts = sum(2 * SHAPES[p][0] * SHAPES[p][1] for p in PROJS) * len(MS)
+    return {"what": "same decode step, dense bf16 weights, torch.matmul (cuBLAS), CUDA graph",
+            "us": round(us, 1), "GBps": round(byts / us / 1e3, 1)}
+
+
+# ---------------------------------------------------------------------------
 # prefill leg (configs[2]): the 7 linears at M=2048 through K2 (tcgen05 GEMM)
 # ---------------------------------------------------------------------------
 def prefill_leg(sfmp, port, models, dev, stream, args):
@@ -576,6 +618,7 @@ def main():
     }
     if world == 1 and not args.no_prefill:
         out["prefill"] = prefill_leg(sfmp, port, models, dev, stream, args)
+        out["dense_cublas_bf16_step"] = dense_leg(dev, stream, xs, args)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_sample(port, blobs)
     print(json.dumps(out), flush=True)

@@ -15,6 +15,7 @@ from oracle.oracle import Port  # noqa: E402
 from synth import LLAMA_8B, activations, model_bytes  # noqa: E402
 
 proj = sys.argv[1] if len(sys.argv) > 1 else "k_proj"
+import time as _time
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 P = Port()
 rows, cols = LLAMA_8B[proj]
@@ -24,6 +25,12 @@ y = dm.gemm(x, path=sfmp.PATH_GEMM)
 torch.cuda.synchronize()
 y = dm.gemm(x, path=sfmp.PATH_GEMM)
 torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record()
+y = dm.gemm(x, path=sfmp.PATH_GEMM)
+e1.record()
+torch.cuda.synchronize()
+print(f"call time (events, incl. pre-pass): {e0.elapsed_time(e1) * 1e3:.1f} us")
 buf = np.zeros(2 * 8 * 256, np.uint64)
 sfmp.lib().sfmp_debug_gemm_timeline(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_size_t(buf.size))
 t = buf.reshape(2, 8, 256).astype(np.int64)[0]
