@@ -749,14 +749,17 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
         switch (dt) {
             case SFMP_F32:
                 e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F32>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
                 xprep_gemm_kernel<SFMP_F32><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
                 break;
             case SFMP_F16:
                 e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F16>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
                 xprep_gemm_kernel<SFMP_F16><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
                 break;
             default:
                 e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_BF16>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
                 xprep_gemm_kernel<SFMP_BF16><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
                 break;
         }

@@ -94,7 +94,8 @@ struct XLin {
     const uint32_t* col_perm;
     uint8_t* xrec;
     int BC, cols, warp0;
-    int lo;  // floor bit-width: records carry the magic biases of lo and lo+1 bit units
+    int item0;  // first pre-pass CTA column (groups of 8 block columns) of this linear
+    int lo;     // floor bit-width: records carry the magic biases of lo and lo+1 bit units
 };
 struct XParams {
     XLin lin[kMaxLin];
@@ -155,21 +156,137 @@ __device__ __forceinline__ float load_x(const void* x, size_t i) {
         return __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(x) + i));
 }
 
+template <sfmp_dtype DT>
+struct XT;
+template <>
+struct XT<SFMP_F32> {
+    using T = float;
+    static __device__ __forceinline__ float f(float v) { return v; }
+};
+template <>
+struct XT<SFMP_F16> {
+    using T = __half;
+    static __device__ __forceinline__ float f(__half v) { return __half2float(v); }
+};
+template <>
+struct XT<SFMP_BF16> {
+    using T = __nv_bfloat16;
+    static __device__ __forceinline__ float f(__nv_bfloat16 v) { return __bfloat162float(v); }
+};
+constexpr int kXprepRowLimit = 192 * 1024;  // staged x row bytes (larger rows: xprep_kernel)
+
+// K4 (decode flavour, staged): one CTA per (token t, 8 block columns of one
+// linear).  It stages token t's x row and the 8 block columns' col_perm in
+// shared memory with coalesced 16 B loads, then each warp writes the record
+// piece of one block column for token t: lane (s, q) gathers the 4 k-slots
+// 32q + 8(s&1) + 4j + 16e + (s>>1) of each 128-column chunk from shared
+// memory and stores 8 B at frag_off(c, nt, s, n, q) -- the token's 256 B of a
+// chunk are one contiguous warp store.  The column sum X_g (lutgemm.cpp:
+// 113-115) uses the input values, the magic bias the f16-rounded ones.
+template <sfmp_dtype DT>
+__global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
+    using T = typename XT<DT>::T;
+    pdl_launch_dependents();  // let the GEMV start streaming weights right away
+    extern __shared__ __align__(16) uint8_t xsm[];
+    const int dbg = xp.dbg;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && dbg == 5) {
+        // previous launch's GEMV end (complete: stream order), then this start
+        g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 104] = g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102];
+        DBG_KSTAMP(100);
+    }
+    const int M = xp.M, n_b = xp.n_b, CH = n_b >> 7;
+    const int t = blockIdx.y;
+    int it = blockIdx.x, li = 0;
+    while (li + 1 < xp.nlin && it >= xp.lin[li + 1].item0) ++li;
+    const XLin& XL = xp.lin[li];
+    it -= XL.item0;
+    const int bc0 = it * 8, nbc = min(8, XL.BC - bc0), cols = XL.cols;
+    uint32_t* cp = reinterpret_cast<uint32_t*>(xsm);  // [nbc][n_b] column indices
+    T* xr = reinterpret_cast<T*>(xsm + 8 * n_b * 4);  // x[t][0..cols)
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(XL.col_perm + static_cast<size_t>(bc0) * n_b);
+        const uint64_t keep = policy_evict_last();
+        for (int i = threadIdx.x; i < nbc * n_b / 4; i += 256) reinterpret_cast<uint4*>(cp)[i] = ldg_keep_v4(src + i, keep);
+        const T* xrow = static_cast<const T*>(XL.x) + static_cast<size_t>(t) * cols;
+        if ((reinterpret_cast<uintptr_t>(xrow) & 15) == 0) {
+            const int nv = cols * static_cast<int>(sizeof(T)) / 16;  // cols % 128 == 0
+            for (int i = threadIdx.x; i < nv; i += 256)
+                reinterpret_cast<uint4*>(xr)[i] = __ldg(reinterpret_cast<const uint4*>(xrow) + i);
+        } else {
+            for (int i = threadIdx.x; i < cols; i += 256) xr[i] = xrow[i];
+        }
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= nbc) return;
+    const int bc = bc0 + warp, s8 = lane >> 2, q = lane & 3;
+    const RecGeom G{M};
+    uint8_t* rec = XL.xrec + static_cast<size_t>(bc) * xp.rec_bytes;
+    const uint32_t* cpw = cp + warp * n_b;
+    const int lo = XL.lo;
+    auto mag = [](int B, int j) { return B <= 4 ? rp_magic(B, j) : 0.f; };
+    const float mlx = mag(lo, 2 * s8), mly = mag(lo, 2 * s8 + 1);
+    const float mhx = mag(lo + 1, 2 * s8), mhy = mag(lo + 1, 2 * s8 + 1);
+    const int kb = 32 * q + 8 * (s8 & 1) + (s8 >> 1);
+    float xs = 0.f, bias_lo = 0.f, bias_hi = 0.f;
+    for (int c = 0; c < CH; ++c) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) v[j * 2 + e] = XT<DT>::f(xr[cpw[c * 128 + kb + 4 * j + 16 * e]]);
+        uint2 st;
+        st.x = h2_as_u32(__floats2half2_rn(v[0], v[1]));  // pairs with A register 2*s8
+        st.y = h2_as_u32(__floats2half2_rn(v[2], v[3]));  // ... and 2*s8+1
+        *reinterpret_cast<uint2*>(rec + G.frag_off(c, t >> 3, s8, t & 7, q)) = st;
+        const float sx = __low2float(u32_as_h2(st.x)) + __high2float(u32_as_h2(st.x));
+        const float sy = __low2float(u32_as_h2(st.y)) + __high2float(u32_as_h2(st.y));
+        bias_lo += mlx * sx + mly * sy;
+        bias_hi += mhx * sx + mhy * sy;
+        xs += (v[0] + v[1]) + (v[2] + v[3]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, o);
+        bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, o);
+    }
+    if (lane == 0) {
+        float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
+        xg[t] = xs;
+        xg[16 + t] = bias_lo;
+        xg[32 + t] = bias_hi;
+        if (t == M - 1)  // token columns the GEMV computes but never stores
+            for (int u = M; u < 8 * G.nt_count(); ++u) xg[u] = xg[16 + u] = xg[32 + u] = 0.f;
+    }
+    if (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
+}
+
+// Fallback for x rows above kXprepRowLimit bytes.
 // K4 (decode flavour): gather x[t][col_perm[.]] once per call into per-block-
 // column records laid out exactly as the MMA B fragments the GEMV consumes,
 // plus per-token column sums X_g (lutgemm.cpp:113-115) and the magic-offset
-// bias.  One warp per (block column, n-tile); lane (n,q) owns token nt*8+n
-// and k-slots 32q + 4h + a (+16) of each 128-column chunk.
+// bias.  One item per (block column, n-tile); its CH 128-column chunks go to
+// CH warps of one CTA (so the col_perm -> x dependent loads of the chunks are
+// in flight together), whose sums are combined in chunk order through shared
+// memory.  Lane (n,q) owns token nt*8+n and k-slots 32q + 4h + a (+16).
 template <sfmp_dtype DT>
 __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     pdl_launch_dependents();  // let the GEMV start streaming weights right away
+    __shared__ float red[8][3][8];
     const int dbg = xp.dbg;
-    if (blockIdx.x == 0 && threadIdx.x == 0) DBG_KSTAMP(100);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && dbg == 5) {
+        // previous launch's GEMV end (complete: stream order), then this start
+        g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 104] = g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102];
+        DBG_KSTAMP(100);
+    }
     const int M = xp.M, n_b = xp.n_b;
     const uint32_t rec_bytes = xp.rec_bytes;
     const RecGeom G{M};
     const int NT = G.nt_count();
-    int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int CH = n_b >> 7;  // 1..8 (host: 8 % CH == 0)
+    const int warp = threadIdx.x >> 5, c = warp % CH;
+    int w = blockIdx.x * (8 / CH) + warp / CH;  // item
     int li = 0;
     while (li + 1 < xp.nlin && w >= xp.lin[li + 1].warp0) ++li;
     const XLin& XL = xp.lin[li];
@@ -179,16 +296,16 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     const uint32_t* col_perm = XL.col_perm;
     uint8_t* xrec = XL.xrec;
     const int lo = XL.lo;
-    if (w >= BC * NT) return;
+    const bool item_ok = w < BC * NT;
     const int bc = w / NT, nt = w - bc * NT;
     const int lane = threadIdx.x & 31, q = lane & 3, n = lane >> 2;
-    const int CH = n_b >> 7;
     const int t = nt * 8 + n;
-    const bool live = n < G.mnt(nt);
+    const bool live = item_ok && n < G.mnt(nt);
     uint8_t* rec = xrec + static_cast<size_t>(bc) * rec_bytes;
     float xs = 0.f, bias_lo = 0.f, bias_hi = 0.f;
-    for (int c = 0; c < CH; ++c) {
-        const uint4 idx4 = __ldg(reinterpret_cast<const uint4*>(col_perm + bc * n_b + c * 128) + lane);
+    if (item_ok) {
+        const uint4 idx4 =
+            ldg_keep_v4(reinterpret_cast<const uint4*>(col_perm + bc * n_b + c * 128) + lane, policy_evict_last());
         uint32_t gi[32];
 #pragma unroll
         for (int s8 = 0; s8 < 8; ++s8) {
@@ -226,14 +343,31 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
 #pragma unroll
             for (int e = 0; e < 32; ++e) xs += v[e];
         }
+        xs += __shfl_xor_sync(0xffffffffu, xs, 1);
+        xs += __shfl_xor_sync(0xffffffffu, xs, 2);
+        bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 1);
+        bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 2);
+        bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 1);
+        bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 2);
     }
-    xs += __shfl_xor_sync(0xffffffffu, xs, 1);
-    xs += __shfl_xor_sync(0xffffffffu, xs, 2);
-    bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 1);
-    bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 2);
-    bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 1);
-    bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 2);
-    if (q == 0) {
+    if (CH > 1) {
+        if (q == 0) {
+            red[warp][0][n] = xs;
+            red[warp][1][n] = bias_lo;
+            red[warp][2][n] = bias_hi;
+        }
+        __syncthreads();
+        if (c != 0) return;
+        if (q == 0) {
+            xs = bias_lo = bias_hi = 0.f;
+            for (int k = 0; k < CH; ++k) {
+                xs += red[warp + k][0][n];
+                bias_lo += red[warp + k][1][n];
+                bias_hi += red[warp + k][2][n];
+            }
+        }
+    }
+    if (item_ok && q == 0) {
         float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
         xg[nt * 8 + n] = live ? xs : 0.f;
         xg[16 + nt * 8 + n] = live ? bias_lo : 0.f;
@@ -340,6 +474,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         // ---------------- producer: one bulk copy per unit (+ its activation record) ----
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
+            const uint64_t keep = policy_evict_last();
             const uint32_t pbytes = kTR * nb8;
             int gi = 0;  // unit counter of this CTA (debug stamps)
             auto issue_w = [&](int s, const Lin& L, uint64_t d) {
@@ -375,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                     uint64_t dpre[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
-                        if (i < pre) dpre[i] = __ldg(gdesc + i);
+                        if (i < pre) dpre[i] = ldg_keep_u64(gdesc + i, keep);
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
                         if (i < pre) {
@@ -389,10 +524,10 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                     i0 = pre;
                     first = false;
                 }
-                uint64_t dnext = i0 < nunits ? __ldg(gdesc + i0) : 0;
+                uint64_t dnext = i0 < nunits ? ldg_keep_u64(gdesc + i0, keep) : 0;
                 for (int i = i0; i < nunits; ++i) {
                     const uint64_t d = dnext;
-                    if (i + 1 < nunits) dnext = __ldg(gdesc + i + 1);
+                    if (i + 1 < nunits) dnext = ldg_keep_u64(gdesc + i + 1, keep);
                     mbar_wait(&empty[s], ph ^ 1);
                     issue_w(s, L, d);
                     issue_x(s, L, I.bc0 + i);
@@ -511,25 +646,55 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
             // sums the partials in split order and stores them un-permuted.
             // Compute warps only (the producer streams on): named barrier 1.
             named_bar_sync(1, kNCW * 32);  // every partial store precedes the release below
+            if (threadIdx.x == 32) DBG_STAMP(124);
             if (threadIdx.x == 32) {
                 const unsigned old = atomic_add_acq_rel_gpu(L.counters + rt, 1u);
                 *flag = (old == static_cast<unsigned>(C - 1)) ? 1u : 0u;
             }
             named_bar_sync(1, kNCW * 32);
+            if (threadIdx.x == 32) DBG_STAMP(125);
             if (*flag) {
-                __threadfence();
-                const float* pp = L.part + static_cast<size_t>(rt) * kMaxSplit * (16 * kTR);
-                for (int v = threadIdx.x - 32; v < p.M * kTR; v += kNCW * 32) {
-                    const int t = v / kTR, row = v - t * kTR;
-                    float acc = 0.f;
-                    for (int r = 0; r < C; ++r) acc += __ldcg(pp + static_cast<size_t>(r) * (16 * kTR) + v);
-                    L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = acc;
+                // Acquire by thread 32 + the barrier orders these loads after
+                // every partial store (the semaphore pattern; no extra fence).
+                // One row per thread, all tokens; RB splits per round so that
+                // RB*8*NT loads are in flight together (latency, not bandwidth).
+                static_assert(kNCW * 32 == kTR, "fixup maps one compute thread per row");
+                constexpr int RB = NT == 1 ? 4 : 2;
+                const int row = threadIdx.x - 32;
+                const float* pp = L.part + static_cast<size_t>(rt) * kMaxSplit * (16 * kTR) + row;
+                const uint32_t orow = __ldg(L.out_map + rt * kTR + row);
+                float acc[8 * NT];
+#pragma unroll
+                for (int t = 0; t < 8 * NT; ++t) acc[t] = 0.f;
+                for (int r0 = 0; r0 < C; r0 += RB) {
+                    float v[RB][8 * NT];
+#pragma unroll
+                    for (int r = 0; r < RB; ++r)
+#pragma unroll
+                        for (int t = 0; t < 8 * NT; ++t)
+                            v[r][t] = (r0 + r < C && t < p.M)
+                                          ? __ldcg(pp + static_cast<size_t>(r0 + r) * (16 * kTR) + t * kTR)
+                                          : 0.f;
+#pragma unroll
+                    for (int r = 0; r < RB; ++r)
+#pragma unroll
+                        for (int t = 0; t < 8 * NT; ++t)
+                            if (r0 + r < C) acc[t] += v[r][t];  // split order, as the partials were cut
                 }
+#pragma unroll
+                for (int t = 0; t < 8 * NT; ++t)
+                    if (t < p.M) L.y[t * L.out_rows + orow] = acc[t];
                 if (threadIdx.x == 32) L.counters[rt] = 0u;  // ready for the next call (stream-ordered)
+                if (threadIdx.x == 32) DBG_STAMP(126);
             }
         }
     }
     if (threadIdx.x == 0) DBG_STAMP(1);
+    if (threadIdx.x == 32) DBG_STAMP(127);
+    if (dbg == 5 && threadIdx.x == 32) {  // kernel-level: max end over all CTAs (compute warps)
+        atomicMax(&g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102], gtimer());
+        if (blockIdx.x == gridDim.x - 1) g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 103] = gridDim.x;
+    }
 }
 
 template <int NT, int CH, int LO>
@@ -561,13 +726,43 @@ cudaError_t launch_nc(cudaLaunchConfig_t& cfg, const Params& p, int lo) {
 }
 
 template <sfmp_dtype DT>
-cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int grid, size_t smem, int lo, cudaStream_t st) {
+cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems, int max_cols, int grid, size_t smem, int lo,
+                     cudaStream_t st) {
+    const size_t elem = DT == SFMP_F32 ? 4 : 2;
     // K4: activation records (normal launch: it overwrites the workspace the
     // previous call may still read, and x may be that call's output, so it
     // follows it in stream order).  Measured: chaining it programmatically
     // lets the next GEMV's CTAs occupy slots early and slows both calls.
     const int NT = p.M > 8 ? 2 : 1;
-    xprep_kernel<DT><<<(xwarps + 7) / 8, 256, 0, st>>>(xp);
+    {
+        // Same shared-memory carveout as the GEMV: an SM running a pre-pass CTA
+        // then needs no reconfiguration (which waits for the SM to drain)
+        // before the GEMV's CTAs can join it.
+        static int configured[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && !configured[dev]) {
+            cudaFuncSetAttribute(xprep_kernel<DT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+            configured[dev] = 1;
+        }
+    }
+    const size_t row_smem = static_cast<size_t>(8) * p.n_b * 4 + static_cast<size_t>(max_cols) * elem;
+    if (row_smem <= static_cast<size_t>(kXprepRowLimit)) {
+        static int configured_rows[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 64 && !configured_rows[dev]) {
+            cudaFuncSetAttribute(xprep_rows_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXprepRowLimit);
+            cudaFuncSetAttribute(xprep_rows_kernel<DT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+            configured_rows[dev] = 1;
+        }
+        xprep_rows_kernel<DT><<<dim3(xitems, p.M), 256, row_smem, st>>>(xp);
+    } else {
+        const int per_cta = 8 / (p.n_b / 128);  // items per pre-pass CTA
+        xprep_kernel<DT><<<(xwarps + per_cta - 1) / per_cta, 256, 0, st>>>(xp);
+    }
     {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -646,7 +841,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     int64_t Q = std::max<int64_t>({2, (units + slots - 1) / slots, (max_bc + kMaxSplit - 2) / (kMaxSplit - 1)});
     if (const char* e = getenv("SFMP_GEMV_Q")) Q = std::max<int64_t>(Q, atoi(e));
     int64_t unit0 = 0;
-    int xwarps = 0;
+    int xwarps = 0, xitems = 0, max_cols = 0;
     for (int i = 0; i < n; ++i) {
         const DevModel& m = *ms[i];
         Lin& L = p.lin[i];
@@ -669,8 +864,11 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         X.BC = BC;
         X.cols = static_cast<int>(m.cols);
         X.warp0 = xwarps;
+        X.item0 = xitems;
         X.lo = m.floor_bits;
         xwarps += BC * NT;
+        xitems += (BC + 7) / 8;
+        max_cols = std::max(max_cols, X.cols);
     }
     p.stage_w = static_cast<uint32_t>((4 * kTR + ceil_bits * kTR * (m0.n_b / 8) + 127) / 128 * 128);
     int max_stages = 4;
@@ -684,9 +882,9 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     p.Q = Q;
     const int grid = static_cast<int>((unit0 + Q - 1) / Q);
     switch (dt) {
-        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, grid, smem, m0.floor_bits, st);
-        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, grid, smem, m0.floor_bits, st);
-        default: return launch_t<SFMP_BF16>(p, xp, xwarps, grid, smem, m0.floor_bits, st);
+        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st);
+        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st);
+        default: return launch_t<SFMP_BF16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st);
     }
 }
 

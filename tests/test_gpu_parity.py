@@ -112,3 +112,31 @@ def test_bit_sweep_parity(gpu, port, bits):
     for path in (gpu.PATH_GEMV, gpu.PATH_GENERIC):
         y = dm.gemm(torch.from_numpy(x).cuda(), path=path).cpu().numpy()
         assert errors(y, ref)[0] <= TOL
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_gemv_wide_rows(gpu, port, dtype):
+    """Decode pre-pass on a 53248-column linear: the bf16 row (104 KB) is
+    staged in shared memory, the f32 row (208 KB) exceeds the staging limit
+    and takes the gather pre-pass; both within the parity bar."""
+    import torch
+    data = model_bytes(port, 512, 53248, 3.0)
+    dm = gpu.DeviceModel(data)
+    x = activations(port, 5, 53248, seed=11)
+    xt = torch.from_numpy(x).cuda().to(getattr(torch, dtype))
+    ref = port.matmul(xt.float().cpu().numpy(), port.load(data).dequantize(), threads=8)
+    y = dm.gemm(xt, path=gpu.PATH_GEMV).cpu().numpy()
+    assert errors(y, ref)[0] <= TOL
+
+
+def test_gemv_misaligned_rows_f16(gpu, port):
+    """x rows at a 2-byte offset: the staged pre-pass copies them element-wise."""
+    import torch
+    data = model_bytes(port, 1024, 1024, 3.5)
+    dm = gpu.DeviceModel(data)
+    buf = torch.from_numpy(activations(port, 7, 1025, seed=5)).cuda().to(torch.float16)
+    x = buf.reshape(-1)[1:1 + 7 * 1024].view(7, 1024)
+    assert x.data_ptr() % 16 != 0
+    ref = port.matmul(x.float().cpu().numpy(), port.load(data).dequantize(), threads=8)
+    y = dm.gemm(x, path=gpu.PATH_GEMV).cpu().numpy()
+    assert errors(y, ref)[0] <= TOL

@@ -80,6 +80,18 @@ if os.environ.get("SFMP_GEMV_DEBUG") == "5":
     print("  last done  ", pct(np.concatenate([last, [0]])))
     print("  end        ", pct(t[:, 1]))
     print("  units/CTA  ", np.percentile(nun[sel], [0, 50, 100]))
+    print("  xprep first CTA start / last CTA end (us, rel. to first GEMV CTA start): %.2f / %.2f" %
+          ((t[511, 100] - t0) / 1e3, (t[511, 101] - t0) / 1e3))
+    print("  GEMV grid %d, last CTA end (all CTAs) %.2f us; launch period %.2f us; prev GEMV end -> xprep start %.2f us" %
+          (t[511, 103], (t[511, 102] - t0) / 1e3, e0.elapsed_time(e1) * 1e3 / (5 * args.launches),
+           (t[511, 100] - t[511, 104]) / 1e3))
+    ce = (t[:511, 127] - t0) / 1e3
+    order = np.argsort(-np.where(sel, ce, -1))[:8]
+    print("  latest compute ends (cta: end, last unit done, last seam barrier, flag, fixup end):")
+    for c in order:
+        n = nun[c]
+        print("    %4d: %6.2f %6.2f %6.2f %6.2f %6.2f" % (c, ce[c], (t[c, 4 + 3 * (n - 1)] - t0) / 1e3,
+              (t[c, 124] - t0) / 1e3, (t[c, 125] - t0) / 1e3, (t[c, 126] - t0) / 1e3 if t[c, 126] > t0 else -1))
     # per-unit processing interval (compute warp 0) median over CTAs
     iv = []
     for c in np.where(sel)[0]:
