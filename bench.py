@@ -309,6 +309,7 @@ def main():
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-group", action="store_true", help="one launch per linear instead of per decoder layer")
     ap.add_argument("--prefill-M", type=int, default=2048)
+    ap.add_argument("--e2e-order", default="", help="comma list: order of the M groups in the e2e step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -481,20 +482,26 @@ def main():
     gy = {M: (yoff[(PROJS[0], M)], yoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][0]) for M in MS}
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
+    # Group order of the e2e step: a small group first (short exposed H2D), the
+    # largest second (its H2D hides under the first group's compute, its D2H
+    # under the later groups'), a small group last (short exposed D2H).
+    E2E_MS = [int(v) for v in args.e2e_order.split(",")] if args.e2e_order else [1, 16, 8, 4, 2]
+    assert sorted(E2E_MS) == sorted(MS)
+
     def e2e_body(i):
         # copies of group k+1 (H2D) and k-1 (D2H) overlap the compute of group k
         cur = torch.cuda.current_stream()
         h2d_s.wait_stream(cur)
         d2h_s.wait_stream(cur)
         ready = []
-        for M in MS:
+        for M in E2E_MS:
             with torch.cuda.stream(h2d_s):
                 a, b = gx[M]
                 dxb[a:b].copy_(hxb[a:b], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d_s)
                 ready.append(ev)
-        for mi, M in enumerate(MS):
+        for mi, M in enumerate(E2E_MS):
             c = (i * len(MS) + mi) % COPIES
             cur.wait_event(ready[mi])
             if world == 1:
@@ -612,7 +619,7 @@ def main():
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": ("pinned host x -> H2D per M group on a copy stream, sfmp_gemm_grouped per M, "
                        "D2H per group on a second copy stream (copies overlap compute); CUDA graph "
-                       "per step, host synchronises on y every step")},
+                       "per step, host synchronises on y every step"), "group_order": E2E_MS},
         "gpu_launches": args.steps * launches_per_step,
         "clocks": clk,
     }
