@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(1024) xprep_gemm_kernel(const void* __restrict
 // 0 dequant wfull seen, 1 dequant math done, 2 aempty seen, 3 afull arrived,
 // 4 MMA afull seen, 5 MMA xfull seen, 6 MMA issued+committed, 7 epilogue accfull seen (per tile).
 __device__ unsigned long long g_gemm_tl[2 * 8 * 256];
+// kernel phases of CTAs < 512 (SFMP_GEMM_DEBUG & 32): entry, setup done, first
+// W issue, griddepcontrol.wait returned, first X issue, exit
+constexpr int kPhCtas = 512;
+__device__ unsigned long long g_gemm_ph[kPhCtas * 16];  // + role ends: 6 W, 7 X, 8 MMA, 9 epilogue, 10 dequant
 __device__ __forceinline__ unsigned long long gtimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -232,16 +236,27 @@ __global__ void __launch_bounds__(128) gemm_reduce_kernel(const GemmParams p) {
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j0 = blockIdx.x * 32 + wi;
     const size_t pstride = static_cast<size_t>(N) * 128;
+    const bool full = blockIdx.x * 32 + 32 <= N;
     float4 acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // partials come from the previous kernel: read-only path (a strong ld.cg
+    // here was issued one at a time, 32 serial HBM round trips)
     for (int c = c0; c <= c1; ++c) {  // CTA order: deterministic
         const float4* src = reinterpret_cast<const float4*>(
                                 p.part + (static_cast<size_t>(c) * 2 + (c == c0 ? s0 : 0)) * pstride +
                                 static_cast<size_t>(j0) * 128) + lane;
         float4 v[8];
+        if (full) {  // unconditional loads: all 8 in flight together
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = (j0 + 4 * k < N) ? __ldcg(src + k * 4 * 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < 8; ++k) v[k] = __ldg(src + k * 4 * 32);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldg(src + (j0 + 4 * k < N ? k : 0) * 4 * 32);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (j0 + 4 * k >= N) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             acc[k].x += v[k].x;
@@ -300,6 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool ph = (p.dbg & 32) && blockIdx.x < kPhCtas;
+    if (ph && threadIdx.x == 0) g_gemm_ph[blockIdx.x * 16 + 0] = gtimer_ns();
     if (threadIdx.x == 0) {
         for (int s = 0; s < SX; ++s) {
             mbar_init(&xfull[s], 1);
@@ -326,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    if (ph && threadIdx.x == 0) g_gemm_ph[blockIdx.x * 16 + 1] = gtimer_ns();
 
     // Work: the sequence of (tile, kc) steps, tile = rt * TT + tt, kc inner,
     // cut into ranges [b*Q, (b+1)*Q), one per CTA.  With enough tiles Q is a
@@ -357,12 +375,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                     mbar_wait_sleep(&wempty[ws], wph ^ 1, 500);
                     mbar_arrive_expect_tx(&wfull[ws], n0);
                     bulk_g2s(wbuf + static_cast<size_t>(ws) * p.stage_w, p.wl + a0, n0, &wfull[ws], pol_w);
+                    if (ph && sg.first && kc == sg.kc0) g_gemm_ph[blockIdx.x * 16 + 2] = gtimer_ns();
                     if (++ws == SW) { ws = 0; wph ^= 1; }
                 }
             }
+            if (ph) g_gemm_ph[blockIdx.x * 16 + 6] = gtimer_ns();
         } else if (lane == 1) {
             int xs = 0, xph = 0;
             pdl_wait();  // X is written by the pre-pass (programmatic dependent launch)
+            if (ph) g_gemm_ph[blockIdx.x * 16 + 3] = gtimer_ns();
             SegIter it = seg_begin(p);
             for (GSeg sg; it.next(p, sg);) {
                 const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
@@ -381,10 +402,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                             "l"(p.xs + ((static_cast<size_t>(tt) * KC + kc) * 2 + h) * xstage), "r"(xstage),
                             "r"(smem_u32(&xfull[xs]))
                             : "memory");
+                        if (ph && sg.first && kc == sg.kc0 && h == 0) g_gemm_ph[blockIdx.x * 16 + 4] = gtimer_ns();
                         if (++xs == SX) { xs = 0; xph ^= 1; }
                     }
                 }
             }
+            if (ph) g_gemm_ph[blockIdx.x * 16 + 7] = gtimer_ns();
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
@@ -432,13 +455,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 __syncwarp();
                 accph ^= 1;
             }
+            if (ph && lane == 0) g_gemm_ph[blockIdx.x * 16 + 8] = gtimer_ns();
         }
     } else if (warp < 2 + kEpiWarps) {
         // ---------------- epilogue: TMEM -> registers -> coalesced y rows ----------------
         // kEpiWarps/4 warps per TMEM lane quarter, each owning 256/(kEpiWarps/4)
-        // accumulator columns: every warp loads its whole share into registers
-        // and releases the accumulator at once, so the y stores overlap the
-        // next tile's MMAs instead of stalling them.
+        // accumulator columns, loaded 32 at a time; the accumulator is
+        // released after the last load, so the last stores overlap the next
+        // tile's MMAs.
         constexpr int kCols = 256 / (kEpiWarps / 4);
         const int ew = warp - 2, q = warp & 3, cg = ew >> 2;
         int accph = 0, ecount = 0;
@@ -452,22 +476,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             accph ^= 1;
             tc_fence_after();
             const int c_begin = cg * kCols;
-            uint32_t v[kCols / 32][32];
-            if (c_begin < N) {
-#pragma unroll
-                for (int c = 0; c < kCols / 32; ++c)
-                    tc_ld_x32(tbase + (static_cast<uint32_t>(q * 32) << 16) + kAccCol + c_begin + 32 * c, v[c]);
-                tc_wait_ld();
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(accempty);
-            if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
-                g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + 128 + ((ecount - 1) & 127)] = gtimer_ns();
-            if (p.dbg & 4) continue;
             const int t0 = tt * N + c_begin;
             const uint64_t row = static_cast<uint64_t>(rt) * 128 + q * 32 + lane;
-            int lim = min(kCols, min(N - c_begin, p.M - t0));
+            int lim = (p.dbg & 4) ? 0 : min(kCols, min(N - c_begin, p.M - t0));
             // whole-tile segment -> y[t][row]; else partial [t][128 rows] of this CTA's slot
             const bool full = sg.kc0 == 0 && sg.kc1 == KC;
             float* yp;
@@ -481,10 +492,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                      static_cast<size_t>(c_begin) * 128 + q * 32 + lane;
                 ld = 128;
             }
+            // 32 columns at a time (a 64-register array would spill: 832
+            // threads leave 72 registers each, and local memory misses L1);
+            // the accumulator is released after the last load, before the
+            // last chunk's stores
 #pragma unroll
-            for (int j = 0; j < kCols; ++j)
-                if (j < lim) yp[static_cast<size_t>(j) * ld] = __uint_as_float(v[j >> 5][j & 31]);
+            for (int c = 0; c < kCols / 32; ++c) {
+                uint32_t v[32];
+                if (c_begin + 32 * c < N) {
+                    tc_ld_x32(tbase + (static_cast<uint32_t>(q * 32) << 16) + kAccCol + c_begin + 32 * c, v);
+                    tc_wait_ld();
+                }
+                if (c == kCols / 32 - 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(accempty);
+                    if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
+                        g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + 128 + ((ecount - 1) & 127)] = gtimer_ns();
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (32 * c + j < lim) yp[static_cast<size_t>(32 * c + j) * ld] = __uint_as_float(v[j]);
+            }
         }
+        if (ph && ew == 0 && lane == 0) g_gemm_ph[blockIdx.x * 16 + 9] = gtimer_ns();
     } else {
         // ---------------- dequant: bit-planes -> f16 A operand in TMEM ----------------
         const int dw = warp - 2 - kEpiWarps, q = warp & 3, kh = dw >> 2;
@@ -565,9 +596,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 if (++ab == kNA) { ab = 0; aph ^= 1; }
             }
         }
+        if (ph && dw == 0 && lane == 0) g_gemm_ph[blockIdx.x * 16 + 10] = gtimer_ns();
     }
     tc_fence_before();
     __syncthreads();
+    if (ph && threadIdx.x == 0) g_gemm_ph[blockIdx.x * 16 + 5] = gtimer_ns();
     if (warp == 1) {
         tc_fence_after();
         tc_dealloc(tbase, kTmemCols);
@@ -620,6 +653,14 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t s
 
 }  // namespace
 
+extern "C" int sfmp_debug_gemm_phases(unsigned long long* host, size_t n) {
+    if (n > static_cast<size_t>(kPhCtas) * 16) n = static_cast<size_t>(kPhCtas) * 16;
+    cudaError_t e = cudaMemcpyFromSymbol(host, g_gemm_ph, n * sizeof(unsigned long long));
+    void* d = nullptr;
+    cudaGetSymbolAddress(&d, g_gemm_ph);
+    cudaMemset(d, 0, sizeof(unsigned long long) * kPhCtas * 16);
+    return static_cast<int>(e);
+}
 extern "C" int sfmp_debug_gemm_timeline(unsigned long long* host, size_t n) {
     if (n > 2 * 8 * 256) n = 2 * 8 * 256;
     return static_cast<int>(cudaMemcpyFromSymbol(host, g_gemm_tl, n * sizeof(unsigned long long)));

@@ -654,8 +654,10 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
             named_bar_sync(1, kNCW * 32);
             if (threadIdx.x == 32) DBG_STAMP(125);
             if (*flag) {
-                // Acquire by thread 32 + the barrier orders these loads after
-                // every partial store (the semaphore pattern; no extra fence).
+                // Acquire by thread 32 (it also invalidates this SM's L1) + the
+                // barrier order these plain loads after every partial store
+                // (the semaphore pattern).  Weak loads: a strong ld.cg is
+                // issued one at a time.
                 // One row per thread, all tokens; RB splits per round so that
                 // RB*8*NT loads are in flight together (latency, not bandwidth).
                 static_assert(kNCW * 32 == kTR, "fixup maps one compute thread per row");
@@ -673,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                         for (int t = 0; t < 8 * NT; ++t)
                             v[r][t] = (r0 + r < C && t < p.M)
-                                          ? __ldcg(pp + static_cast<size_t>(r0 + r) * (16 * kTR) + t * kTR)
+                                          ? pp[static_cast<size_t>(r0 + r) * (16 * kTR) + t * kTR]
                                           : 0.f;
 #pragma unroll
                     for (int r = 0; r < RB; ++r)

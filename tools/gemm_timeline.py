@@ -25,6 +25,12 @@ y = dm.gemm(x, path=sfmp.PATH_GEMM)
 torch.cuda.synchronize()
 y = dm.gemm(x, path=sfmp.PATH_GEMM)
 torch.cuda.synchronize()
+_ph = np.zeros(512 * 16, np.uint64)
+sfmp.lib().sfmp_debug_gemm_phases(_ph.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_size_t(_ph.size))  # clears
+if os.environ.get("FLUSH"):
+    _fl = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    _fl.zero_()
+    torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record()
 y = dm.gemm(x, path=sfmp.PATH_GEMM)
@@ -38,6 +44,18 @@ n = int((t[4] > 0).sum())
 t0 = t[0, 0]
 names = ["deq wfull", "deq math", "deq aempty", "deq afull", "mma afull", "mma xfull", "mma commit"]
 print(f"{proj} M={M}: {n} units on CTA 0; times rel. to first wfull (us)")
+ph = np.zeros(512 * 16, np.uint64)
+sfmp.lib().sfmp_debug_gemm_phases(ph.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_size_t(ph.size))
+ph = ph.astype(np.int64).reshape(512, 16)
+print("CTA 0 phases (us rel. to first wfull): entry %.2f setup %.2f firstW %.2f pdl_wait %.2f firstX %.2f exit %.2f"
+      % tuple((ph[0, i] - t0) / 1e3 for i in range(6)))
+live = ph[:, 0] > 0
+e0_ = ph[live, 0].min()
+for i, nm in enumerate(["entry", "setup", "firstW", "pdl_wait", "firstX", "exit", "W end", "X end", "MMA end",
+                        "epi end", "deq end"]):
+    v = (ph[live, i] - e0_) / 1e3
+    print("  all %d CTAs %-8s (us rel. to first entry) p0 %.2f p50 %.2f p90 %.2f p100 %.2f" %
+          (live.sum(), nm, *np.percentile(v, [0, 50, 90, 100])))
 for k in list(range(0, min(n, 4))) + list(range(28, min(n, 38))) + list(range(max(6, n - 3), n)):
     print(f"unit {k:3d}: " + " ".join(f"{nm}={(t[i, k] - t0) / 1e3:7.2f}" for i, nm in enumerate(names)))
 d = np.diff(t[4, :n]) / 1e3

@@ -19,10 +19,11 @@ ap.add_argument("--M", type=int, default=2048)
 ap.add_argument("--bits", type=float, default=3.25)
 ap.add_argument("--launches", type=int, default=8)
 ap.add_argument("--eager", action="store_true")
+ap.add_argument("--m_b", type=int, default=0, help="row block (0: synth default; the bench uses 128 for k/v)")
 args = ap.parse_args()
 P = Port()
 rows, cols = (LLAMA_8B if args.model == "8b" else LLAMA_70B)[args.proj]
-data = model_bytes(P, rows, cols, args.bits)
+data = model_bytes(P, rows, cols, args.bits, **({'m_b': args.m_b} if args.m_b else {}))
 dm = sfmp.DeviceModel(data)
 x = torch.from_numpy(activations(P, args.M, cols)).cuda().to(torch.bfloat16)
 y = torch.empty(args.M, rows, device="cuda")
