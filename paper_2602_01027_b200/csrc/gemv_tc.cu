@@ -456,6 +456,11 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int dbg = p.debug_mode;
     if (threadIdx.x == 0) DBG_STAMP(0);
+    if (threadIdx.x == 0 && dbg == 5 && blockIdx.x < kDbgCtas - 1) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_dbg_timeline[blockIdx.x * kDbgSlots + 123] = smid;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);

@@ -18,9 +18,10 @@ ap.add_argument("--M", type=int, default=1)
 ap.add_argument("--copies", type=int, default=4)
 ap.add_argument("--launches", type=int, default=8)
 ap.add_argument("--eager", action="store_true")
+ap.add_argument("--order", default="", help="comma list of projections (default: LLAMA_8B order)")
 args = ap.parse_args()
 P = Port()
-projs = list(LLAMA_8B)
+projs = args.order.split(",") if args.order else list(LLAMA_8B)
 datas = {p: model_bytes(P, *LLAMA_8B[p], 3.25, m_b=128 if p in ("k_proj", "v_proj") else 512,
                         seed={"up_proj": 4, "v_proj": 1}.get(p, 0)) for p in projs}
 models = [[sfmp.DeviceModel(datas[p]) for p in projs] for _ in range(args.copies)]
@@ -92,6 +93,14 @@ if os.environ.get("SFMP_GEMV_DEBUG") == "5":
         n = nun[c]
         print("    %4d: %6.2f %6.2f %6.2f %6.2f %6.2f" % (c, ce[c], (t[c, 4 + 3 * (n - 1)] - t0) / 1e3,
               (t[c, 124] - t0) / 1e3, (t[c, 125] - t0) / 1e3, (t[c, 126] - t0) / 1e3 if t[c, 126] > t0 else -1))
+    sm = t[:511, 123]
+    ends = {}
+    for c in np.where(sel)[0]:
+        ends.setdefault(int(sm[c]), []).append(ce[c])
+    sm_last = np.array([max(v) for v in ends.values()])
+    sm_first = np.array([min(v) for v in ends.values()])
+    print("  per-SM (%d SMs) latest compute end p0/p10/p50/p90/p100: %s" % (len(ends), " ".join("%.2f" % np.percentile(sm_last, q) for q in (0, 10, 50, 90, 100))))
+    print("  per-SM earliest CTA end p0/p50/p100: %s" % " ".join("%.2f" % np.percentile(sm_first, q) for q in (0, 50, 100)))
     # per-unit processing interval (compute warp 0) median over CTAs
     iv = []
     for c in np.where(sel)[0]:
