@@ -818,9 +818,11 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     p.work = ntiles * p.KC;
     const int sms = m.num_sms;
     // measured (tools/sweep.py, prof_gemm.py): stream-K pays off when the tiles
-    // leave most SMs idle (<= 1/4 busy) or leave SMs idle while each CTA still
-    // gets a long K range (>= 32 steps); otherwise whole tiles round-robin
-    const bool sk = ntiles * 4 <= sms || (ntiles < sms && (p.work + sms - 1) / sms >= 32);
+    // leave at least half the SMs idle (k/v at M <= 2048: 64 tiles, 35 vs 38 us;
+    // q at M=512: 29 vs 33 us) or leave SMs idle while each CTA still gets a
+    // long K range (>= 32 steps); otherwise whole tiles round-robin (k/v at
+    // M=4096, 128 tiles: 49 vs 59 us)
+    const bool sk = ntiles * 2 <= sms || (ntiles < sms && (p.work + sms - 1) / sms >= 32);
     p.rr = sk ? 0 : 1;
     if (const char* e = getenv("SFMP_GEMM_SK")) p.rr = atoi(e) ? 0 : 1;
     p.Q = p.KC;

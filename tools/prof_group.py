@@ -101,6 +101,13 @@ if os.environ.get("SFMP_GEMV_DEBUG") == "5":
     sm_first = np.array([min(v) for v in ends.values()])
     print("  per-SM (%d SMs) latest compute end p0/p10/p50/p90/p100: %s" % (len(ends), " ".join("%.2f" % np.percentile(sm_last, q) for q in (0, 10, 50, 90, 100))))
     print("  per-SM earliest CTA end p0/p50/p100: %s" % " ".join("%.2f" % np.percentile(sm_first, q) for q in (0, 50, 100)))
+    rank = np.arange(511) // 148
+    for rk in range(4):
+        m = sel & (rank == rk)
+        if m.any():
+            print("  CTA rank %d (blockIdx//148): last done mean %.2f p90 %.2f; first full mean %.2f" %
+                  (rk, ((last[:511] - t0)[m] / 1e3).mean(), np.percentile((last[:511] - t0)[m] / 1e3, 90),
+                   ((t[:511, 3] - t0)[m] / 1e3).mean()))
     # per-unit processing interval (compute warp 0) median over CTAs
     iv = []
     for c in np.where(sel)[0]:
