@@ -98,9 +98,21 @@ if os.environ.get("SFMP_GEMV_DEBUG") == "5":
     for c in np.where(sel)[0]:
         ends.setdefault(int(sm[c]), []).append(ce[c])
     sm_last = np.array([max(v) for v in ends.values()])
+    if os.environ.get("SM_DUMP"):
+        np.save(os.environ["SM_DUMP"], np.array([[k, max(v), min(v), len(v)] for k, v in sorted(ends.items())]))
     sm_first = np.array([min(v) for v in ends.values()])
     print("  per-SM (%d SMs) latest compute end p0/p10/p50/p90/p100: %s" % (len(ends), " ".join("%.2f" % np.percentile(sm_last, q) for q in (0, 10, 50, 90, 100))))
     print("  per-SM earliest CTA end p0/p50/p100: %s" % " ".join("%.2f" % np.percentile(sm_first, q) for q in (0, 50, 100)))
+    hb = t[:511, 122]
+    busy = (last[:511] - t[:511, 3]) / 1e3
+    ok = sel & (nun > 0)
+    if hb[ok].any():  # (needs a build that counts ceil-bit units in slot 122)
+      A = np.stack([nun[ok], hb[ok], np.ones(ok.sum())], 1)
+      coef, *_ = np.linalg.lstsq(A, busy[ok], rcond=None)
+      pred = A @ coef
+      print("  busy(us) ~ %.3f*units + %.3f*ceil_units + %.2f; R2 %.3f; ceil units/CTA p0/p50/p100 %s" %
+          (coef[0], coef[1], coef[2], 1 - ((busy[ok] - pred) ** 2).sum() / ((busy[ok] - busy[ok].mean()) ** 2).sum(),
+           np.percentile(hb[ok], [0, 50, 100])))
     rank = np.arange(511) // 148
     for rk in range(4):
         m = sel & (rank == rk)
