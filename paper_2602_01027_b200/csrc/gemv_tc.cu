@@ -146,6 +146,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do {                                                                                      \
         if (dbg == 5) g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + (slot)] = gtimer();         \
     } while (0)
+// Per-unit stamps cost ~12 issue slots per unit even when off: compiled in
+// only with -DSFMP_GEMV_TIMELINE=1 (tools/prof_group.py's timeline).
+#ifndef SFMP_GEMV_TIMELINE
+#define SFMP_GEMV_TIMELINE 0
+#endif
+#if SFMP_GEMV_TIMELINE
+#define DBG_USTAMP(slot) DBG_STAMP(slot)
+#else
+#define DBG_USTAMP(slot) \
+    do {                 \
+    } while (0)
+#endif
 
 template <sfmp_dtype DT>
 __device__ __forceinline__ float load_x(const void* x, size_t i) {
@@ -485,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
             auto issue_w = [&](int s, const Lin& L, uint64_t d) {
                 const int bits = static_cast<int>((d >> 48) & 0xF);
                 sbits[s] = static_cast<uint32_t>(bits);  // published by the arrive below
-                DBG_STAMP(2 + 3 * gi);
+                DBG_USTAMP(2 + 3 * gi);
                 const uint32_t wbytes = 4 * kTR + bits * pbytes;
                 mbar_arrive_expect_tx(&full[s], wbytes + p.rec_bytes);
                 bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
@@ -560,7 +572,9 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         }
         const uint32_t xg0 = smem_u32(xbase) + G.xg_off(CH) + 8 * q;
         const uint32_t sbits_a = smem_u32(sbits);
+        const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
         int s = 0, ph = 0, gi = 0;
+        uint32_t wo = 0, xo = 0;  // byte offsets of stage s in the weight / record rings
         const int64_t uend = min(p.units, (static_cast<int64_t>(blockIdx.x) + 1) * p.Q);
         for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.Q; u < uend;) {
             const Seg I = seg_at(p, u, uend);
@@ -575,13 +589,13 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                     for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
             for (int i = 0; i < nunits; ++i, ++gi) {
-                mbar_wait(&full[s], ph);
-                if (cw == 0 && lane == 0) DBG_STAMP(3 + 3 * gi);
+                mbar_wait_a(full_a + 8 * s, ph);
+                if (cw == 0 && lane == 0) DBG_USTAMP(3 + 3 * gi);
                 const int bits = static_cast<int>(lds_u32(sbits_a + 4 * s));
                 uint32_t xb[NT];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + s * xstep[nt];
-                const uint32_t prow = prow0 + s * stage_w;
+                for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + (xstep[nt] ? xo : 0u);
+                const uint32_t prow = prow0 + wo;
                 float cacc[kMT][NT][4];
 #pragma unroll
                 for (int h = 0; h < kMT; ++h)
@@ -598,8 +612,8 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                     }
                 }
                 // per-row affine of this block: y += s*(C - bias) + z*Xg
-                const uint32_t sz = sz0 + s * stage_w;
-                const uint32_t xg = xg0 + s * rec_bytes;
+                const uint32_t sz = sz0 + wo;
+                const uint32_t xg = xg0 + xo;
                 const uint32_t boff = bits == LO ? 64u : 128u;  // bias of this unit's layout (0 for > 4 bits)
 #pragma unroll
                 for (int m = 0; m < kMT; ++m) {
@@ -610,16 +624,19 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                         const float2 xg01 = lds_f2(xg + 32 * nt);
                         const float2 b01 = lds_f2(xg + boff + 32 * nt);
                         const float* c0 = cacc[m][nt];
-                        yacc[m][nt][0] += sa * (c0[0] - b01.x) + za * xg01.x;
-                        yacc[m][nt][1] += sa * (c0[1] - b01.y) + za * xg01.y;
-                        yacc[m][nt][2] += sb * (c0[2] - b01.x) + zb * xg01.x;
-                        yacc[m][nt][3] += sb * (c0[3] - b01.y) + zb * xg01.y;
+                        // 3 ops per element: FFMA(z, Xg, y), FADD(C - b), FFMA(s, ., .)
+                        yacc[m][nt][0] = fmaf(sa, c0[0] - b01.x, fmaf(za, xg01.x, yacc[m][nt][0]));
+                        yacc[m][nt][1] = fmaf(sa, c0[1] - b01.y, fmaf(za, xg01.y, yacc[m][nt][1]));
+                        yacc[m][nt][2] = fmaf(sb, c0[2] - b01.x, fmaf(zb, xg01.x, yacc[m][nt][2]));
+                        yacc[m][nt][3] = fmaf(sb, c0[3] - b01.y, fmaf(zb, xg01.y, yacc[m][nt][3]));
                     }
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-                if (cw == 0 && lane == 0) DBG_STAMP(4 + 3 * gi);
-                if (++s == S) { s = 0; ph ^= 1; }
+                if (lane == 0) mbar_arrive_a(empty_a + 8 * s);
+                if (cw == 0 && lane == 0) DBG_USTAMP(4 + 3 * gi);
+                wo += stage_w;
+                xo += rec_bytes;
+                if (++s == S) { s = 0; ph ^= 1; wo = 0; xo = 0; }
             }
             if (C == 1) {
                 // whole row tile in this item: un-permuted store straight to y

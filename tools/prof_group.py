@@ -1,5 +1,7 @@
 """Grouped decode (the bench step for one M): the 7 Llama-3.1-8B linears in one launch.
---eager: plain launches for ncu; else graph + events timing."""
+--eager: plain launches for ncu; else graph + events timing.
+SFMP_GEMV_DEBUG=5 prints the per-CTA timeline; its per-unit stamps need a build with
+`make -C paper_2602_01027_b200 EXTRA=-DSFMP_GEMV_TIMELINE=1`."""
 import argparse
 import os
 import sys
