@@ -107,10 +107,17 @@ struct XParams {
 // Activation record of one block column (n_b columns), for M tokens:
 //   for chunk c (128 columns), n-tile nt (8 tokens), token n < Mnt, k-step s:
 //     4 lanes x 8 B of f16 B fragments  (tokens >= M omitted)
-//   then Xg[16] (f32 column sums), bias[16] of floor-bit units, bias[16] of
-//   ceil-bit units (f32 magic offsets of the repacked layout, repack.cuh).
+//   then Xg[16] (f32 column sums), then for the floor-bit and the ceil-bit
+//   layout the NEGATED per-token magic offset (repack.cuh) as MMA accumulator
+//   fragments [nt][lane quad q][4] = {-b(2q), -b(2q+1), -b(2q), -b(2q+1)} of
+//   n-tile nt: one 16-byte load initialises an accumulator, so C - bias comes
+//   out of the MMA itself.
 // Within a (c, nt, n) run the 8 k-steps are contiguous (stride 32 B), so a
 // lane's fragment addresses are compile-time offsets from one base.
+// float index (from xg_off) of token t's accumulator-init slots, layout hi=0/1
+__host__ __device__ __forceinline__ int bias_slot(int t, int hi) {
+    return 16 + hi * 32 + ((t >> 3) * 4 + ((t & 7) >> 1)) * 4 + (t & 1);
+}
 struct RecGeom {
     int M;
     __host__ __device__ int mnt(int nt) const { return nt == 0 ? (M < 8 ? M : 8) : M - 8; }
@@ -123,7 +130,7 @@ struct RecGeom {
         return lane_off(c, nt, n, q) + s * 32;
     }
     __host__ __device__ int xg_off(int CH) const { return CH * chunk_bytes(); }
-    __host__ __device__ int bytes(int CH) const { return (xg_off(CH) + 192 + 127) / 128 * 128; }
+    __host__ __device__ int bytes(int CH) const { return (xg_off(CH) + 320 + 127) / 128 * 128; }
 };
 
 // Debug timeline (SFMP_GEMV_DEBUG=5): [cta][slot] globaltimer stamps for the
@@ -266,10 +273,11 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     if (lane == 0) {
         float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
         xg[t] = xs;
-        xg[16 + t] = bias_lo;
-        xg[32 + t] = bias_hi;
+        xg[bias_slot(t, 0)] = xg[bias_slot(t, 0) + 2] = -bias_lo;
+        xg[bias_slot(t, 1)] = xg[bias_slot(t, 1) + 2] = -bias_hi;
         if (t == M - 1)  // token columns the GEMV computes but never stores
-            for (int u = M; u < 8 * G.nt_count(); ++u) xg[u] = xg[16 + u] = xg[32 + u] = 0.f;
+            for (int u = M; u < 8 * G.nt_count(); ++u)
+                xg[u] = xg[bias_slot(u, 0)] = xg[bias_slot(u, 0) + 2] = xg[bias_slot(u, 1)] = xg[bias_slot(u, 1) + 2] = 0.f;
     }
     if (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
 }
@@ -381,9 +389,10 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     }
     if (item_ok && q == 0) {
         float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
-        xg[nt * 8 + n] = live ? xs : 0.f;
-        xg[16 + nt * 8 + n] = live ? bias_lo : 0.f;
-        xg[32 + nt * 8 + n] = live ? bias_hi : 0.f;
+        const int tt = nt * 8 + n;
+        xg[tt] = live ? xs : 0.f;
+        xg[bias_slot(tt, 0)] = xg[bias_slot(tt, 0) + 2] = live ? -bias_lo : 0.f;
+        xg[bias_slot(tt, 1)] = xg[bias_slot(tt, 1) + 2] = live ? -bias_hi : 0.f;
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
 }
@@ -571,6 +580,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
             xstep[nt] = live ? rec_bytes : 0u;
         }
         const uint32_t xg0 = smem_u32(xbase) + G.xg_off(CH) + 8 * q;
+        const uint32_t bc_a = smem_u32(xbase) + G.xg_off(CH) + 64 + 16 * q;  // accumulator inits
         const uint32_t sbits_a = smem_u32(sbits);
         const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
         int s = 0, ph = 0, gi = 0;
@@ -596,13 +606,21 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + (xstep[nt] ? xo : 0u);
                 const uint32_t prow = prow0 + wo;
+                // accumulators start at -bias (this unit's layout): C - bias from the MMA
+                const uint32_t xg = xg0 + xo;
+                const uint32_t binit = bc_a + xo + (bits == LO ? 0u : 128u);
                 float cacc[kMT][NT][4];
 #pragma unroll
-                for (int h = 0; h < kMT; ++h)
+                for (int nt = 0; nt < NT; ++nt) {
+                    const uint4 b4 = lds_v4(binit + 64 * nt);
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) cacc[h][nt][e] = 0.f;
+                    for (int h = 0; h < kMT; ++h) {
+                        cacc[h][nt][0] = __uint_as_float(b4.x);
+                        cacc[h][nt][1] = __uint_as_float(b4.y);
+                        cacc[h][nt][2] = __uint_as_float(b4.z);
+                        cacc[h][nt][3] = __uint_as_float(b4.w);
+                    }
+                }
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
                     if (bits == LO) {
@@ -613,8 +631,6 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 }
                 // per-row affine of this block: y += s*(C - bias) + z*Xg
                 const uint32_t sz = sz0 + wo;
-                const uint32_t xg = xg0 + xo;
-                const uint32_t boff = bits == LO ? 64u : 128u;  // bias of this unit's layout (0 for > 4 bits)
 #pragma unroll
                 for (int m = 0; m < kMT; ++m) {
                     const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
@@ -622,13 +638,11 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) {
                         const float2 xg01 = lds_f2(xg + 32 * nt);
-                        const float2 b01 = lds_f2(xg + boff + 32 * nt);
-                        const float* c0 = cacc[m][nt];
-                        // 3 ops per element: FFMA(z, Xg, y), FADD(C - b), FFMA(s, ., .)
-                        yacc[m][nt][0] = fmaf(sa, c0[0] - b01.x, fmaf(za, xg01.x, yacc[m][nt][0]));
-                        yacc[m][nt][1] = fmaf(sa, c0[1] - b01.y, fmaf(za, xg01.y, yacc[m][nt][1]));
-                        yacc[m][nt][2] = fmaf(sb, c0[2] - b01.x, fmaf(zb, xg01.x, yacc[m][nt][2]));
-                        yacc[m][nt][3] = fmaf(sb, c0[3] - b01.y, fmaf(zb, xg01.y, yacc[m][nt][3]));
+                        const float* c0 = cacc[m][nt];  // = C - bias
+                        yacc[m][nt][0] = fmaf(sa, c0[0], fmaf(za, xg01.x, yacc[m][nt][0]));
+                        yacc[m][nt][1] = fmaf(sa, c0[1], fmaf(za, xg01.y, yacc[m][nt][1]));
+                        yacc[m][nt][2] = fmaf(sb, c0[2], fmaf(zb, xg01.x, yacc[m][nt][2]));
+                        yacc[m][nt][3] = fmaf(sb, c0[3], fmaf(zb, xg01.y, yacc[m][nt][3]));
                     }
                 }
                 __syncwarp();
