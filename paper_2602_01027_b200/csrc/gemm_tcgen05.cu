@@ -105,6 +105,88 @@ __device__ __forceinline__ float ldx(const void* x, size_t i) {
         return __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(x) + i));
 }
 
+// Persistent pre-pass (cols < 65536): each CTA keeps the slot table as u16 in
+// shared memory (loaded once, instead of once per token) and streams its
+// tokens' x rows through two shared buffers with 1-D bulk copies, so the next
+// row lands while the current one is gathered into the swizzled B image.
+// Tokens M..TT*N-1 of the last tile are written as zeros.
+template <sfmp_dtype DT>
+__global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __restrict__ x,
+                                                              const uint32_t* __restrict__ xslot,
+                                                              uint8_t* __restrict__ xs, int M, int N, int KC,
+                                                              int cols, int Mpad) {
+    using T = std::conditional_t<DT == SFMP_F32, float, uint16_t>;
+    extern __shared__ __align__(16) uint8_t xsm[];
+    pdl_launch_dependents();
+    uint64_t* bar = reinterpret_cast<uint64_t*>(xsm);            // [2] row buffer full
+    uint16_t* idx = reinterpret_cast<uint16_t*>(xsm + 16);        // [cols] slot table
+    const uint32_t row_bytes = static_cast<uint32_t>(cols) * sizeof(T);
+    uint8_t* rowbuf = xsm + 16 + ((static_cast<size_t>(cols) * 2 + 15) / 16) * 16;  // [2][row_bytes]
+    const int G = gridDim.x;
+    auto row_of = [&](int k) { return static_cast<int>(blockIdx.x) + k * G; };  // k-th token of this CTA
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+        const uint64_t pol = policy_evict_first();
+        for (int k = 0; k < 2; ++k) {
+            const int t = row_of(k);
+            if (t < M) {
+                mbar_arrive_expect_tx(&bar[k], row_bytes);
+                bulk_g2s(rowbuf + k * static_cast<size_t>(row_bytes),
+                         static_cast<const uint8_t*>(x) + static_cast<size_t>(t) * row_bytes, row_bytes, &bar[k], pol);
+            }
+        }
+    }
+    for (int i = threadIdx.x; i < cols / 4; i += blockDim.x) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(xslot) + i);
+        reinterpret_cast<uint2*>(idx)[i] = make_uint2(v.x | (v.y << 16), v.z | (v.w << 16));
+    }
+    __syncthreads();
+    for (int k = 0;; ++k) {
+        const int t = row_of(k);
+        if (t >= Mpad) break;
+        const int buf = k & 1;
+        const int tt = t / N, r = t - tt * N;
+        uint8_t* dst = xs + static_cast<size_t>(tt) * KC * 2 * N * 128 + r * 128;
+        const T* xr = reinterpret_cast<const T*>(rowbuf + buf * static_cast<size_t>(row_bytes));
+        if (t < M) mbar_wait(&bar[buf], static_cast<uint32_t>(k >> 1) & 1u);
+        for (int c = threadIdx.x; c < KC * 16; c += blockDim.x) {
+            const int kc = c >> 4, a = (c >> 3) & 1, j = c & 7;
+            uint4 out = make_uint4(0u, 0u, 0u, 0u);
+            if (t < M) {
+                const uint4 ii = *reinterpret_cast<const uint4*>(idx + kc * 128 + 64 * a + 8 * j);
+                const uint32_t iv[4] = {ii.x, ii.y, ii.z, ii.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const T lo = xr[iv[e] & 0xFFFFu], hi = xr[iv[e] >> 16];
+                    if constexpr (DT == SFMP_F32) {
+                        o[e] = h2_as_u32(__floats2half2_rn(lo, hi));
+                    } else if constexpr (DT == SFMP_BF16) {
+                        o[e] = h2_as_u32(__floats2half2_rn(__bfloat162float(__ushort_as_bfloat16(lo)),
+                                                          __bfloat162float(__ushort_as_bfloat16(hi))));
+                    } else {
+                        o[e] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+                    }
+                }
+                out = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            *reinterpret_cast<uint4*>(dst + (static_cast<size_t>(kc) * 2 + a) * N * 128 + ((j ^ (r & 7)) << 4)) = out;
+        }
+        __syncthreads();  // buffer `buf` is free again
+        if (threadIdx.x == 0) {
+            const int t2 = row_of(k + 2);
+            if (t2 < M) {
+                mbar_arrive_expect_tx(&bar[buf], row_bytes);
+                bulk_g2s(rowbuf + buf * static_cast<size_t>(row_bytes),
+                         static_cast<const uint8_t*>(x) + static_cast<size_t>(t2) * row_bytes, row_bytes, &bar[buf],
+                         policy_evict_first());
+            }
+        }
+    }
+}
+
 // One CTA per token (grid-stride): the x row is staged in shared memory as
 // f16 with coalesced 16-byte loads, then every 16-byte chunk of the swizzled
 // B image is gathered from shared memory through the slot table xslot
@@ -785,7 +867,31 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     const int xgrid = Mpad;
     const size_t xsm = static_cast<size_t>(cols) * 2;
     uint8_t* xs = static_cast<uint8_t*>(ws);
-    if (!(p.dbg & 16)) {
+    // persistent pre-pass when the u16 slot table + two rows fit (>= 2 CTAs per SM)
+    const size_t elem = dt == SFMP_F32 ? 4 : 2;
+    const size_t rsm = 16 + (static_cast<size_t>(cols) * 2 + 15) / 16 * 16 + 2 * static_cast<size_t>(cols) * elem;
+    const bool rows_ok = cols < 65536 && rsm <= 110 * 1024 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                         !getenv("SFMP_XPREP_LEGACY");
+    if (!(p.dbg & 16) && rows_ok) {
+        const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / rsm)));
+        const int rgrid = static_cast<int>(std::min<int64_t>(Mpad, static_cast<int64_t>(per_sm) * m.num_sms));
+        cudaError_t e0 = cudaSuccess;
+        switch (dt) {
+            case SFMP_F32:
+                e0 = cudaFuncSetAttribute(xprep_gemm_rows_kernel<SFMP_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                xprep_gemm_rows_kernel<SFMP_F32><<<rgrid, 512, rsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                break;
+            case SFMP_F16:
+                e0 = cudaFuncSetAttribute(xprep_gemm_rows_kernel<SFMP_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                xprep_gemm_rows_kernel<SFMP_F16><<<rgrid, 512, rsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                break;
+            default:
+                e0 = cudaFuncSetAttribute(xprep_gemm_rows_kernel<SFMP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+                xprep_gemm_rows_kernel<SFMP_BF16><<<rgrid, 512, rsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
+                break;
+        }
+        if (e0 != cudaSuccess) return e0;
+    } else if (!(p.dbg & 16)) {
         cudaError_t e0 = cudaSuccess;
         switch (dt) {
             case SFMP_F32:
