@@ -79,7 +79,8 @@ struct GemmParams {
     int floor_bits, has_extra;
     int SX, SW;              // X / W ring stages
     int64_t work, Q;         // (tile, kc) steps in all, per CTA (stream-K)
-    int rr;                  // 1: whole tiles round-robin over the grid
+    int64_t w0;              // steps [0, w0): whole tiles round-robin; [w0, work): stream-K ranges of Q
+    int rr;                  // 1: whole tiles only (w0 == work)
     float* part;             // [grid][2][N][128] f32 stream-K partial tiles
     uint32_t stage_w;        // W stage bytes (one unit)
     uint32_t bar_bytes;      // barrier + offset area (multiple of 1024)
@@ -262,37 +263,44 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
 
 struct GSeg {
     int tile, kc0, kc1;
-    bool first;  // first segment of this CTA's range
+    bool first;  // first segment of this CTA's stream-K range
 };
-// Segments of this CTA: round-robin whole tiles (b, b+G, ...) when p.rr, else
-// the contiguous stream-K range [b*Q, (b+1)*Q) cut at tile boundaries.
+// Segments of this CTA: whole tiles b, b+G, ... of the round-robin part
+// [0, w0), then its stream-K range [w0 + b*Q, w0 + (b+1)*Q) cut at tile
+// boundaries (hybrid: the last, partial wave of tiles is spread over all CTAs
+// instead of leaving most SMs idle while a few finish whole tiles).
 struct SegIter {
     int64_t w, wend;
-    bool first;
+    bool sk, first;
     __device__ __forceinline__ bool next(const GemmParams& p, GSeg& g) {
-        if (p.rr) {
-            if (w >= p.work) return false;
-            g.tile = static_cast<int>(w / p.KC);
-            g.kc0 = 0;
-            g.kc1 = p.KC;
-            g.first = first;
-            w += static_cast<int64_t>(gridDim.x) * p.KC;
-        } else {
-            if (w >= wend) return false;
-            g.tile = static_cast<int>(w / p.KC);
-            g.kc0 = static_cast<int>(w - static_cast<int64_t>(g.tile) * p.KC);
-            g.kc1 = static_cast<int>(min(static_cast<int64_t>(p.KC), g.kc0 + (wend - w)));
-            g.first = first;
-            w += g.kc1 - g.kc0;
+        if (!sk) {
+            if (w < p.w0) {
+                g.tile = static_cast<int>(w / p.KC);
+                g.kc0 = 0;
+                g.kc1 = p.KC;
+                g.first = false;
+                w += static_cast<int64_t>(gridDim.x) * p.KC;
+                return true;
+            }
+            sk = true;
+            w = p.w0 + static_cast<int64_t>(blockIdx.x) * p.Q;
+            wend = min(p.work, w + p.Q);
         }
+        if (w >= wend) return false;
+        g.tile = static_cast<int>(w / p.KC);
+        g.kc0 = static_cast<int>(w - static_cast<int64_t>(g.tile) * p.KC);
+        g.kc1 = static_cast<int>(min(static_cast<int64_t>(p.KC), g.kc0 + (wend - w)));
+        g.first = first;
+        w += g.kc1 - g.kc0;
         first = false;
         return true;
     }
 };
 __device__ __forceinline__ SegIter seg_begin(const GemmParams& p) {
     SegIter it;
-    it.w = p.rr ? static_cast<int64_t>(blockIdx.x) * p.KC : static_cast<int64_t>(blockIdx.x) * p.Q;
-    it.wend = min(p.work, it.w + p.Q);
+    it.w = static_cast<int64_t>(blockIdx.x) * p.KC;
+    it.wend = 0;
+    it.sk = false;
     it.first = true;
     return it;
 }
@@ -305,13 +313,13 @@ __device__ __forceinline__ SegIter seg_begin(const GemmParams& p) {
 // first boundary.
 __global__ void __launch_bounds__(128) gemm_reduce_kernel(const GemmParams p) {
     const int64_t b = blockIdx.y;
-    const int64_t w = (b + 1) * p.Q;
+    const int64_t w = p.w0 + (b + 1) * p.Q;  // end of CTA b's stream-K range
     if (w >= p.work) return;
     const int64_t tile = w / p.KC;
-    const int64_t ts = tile * p.KC;
-    if (w == ts || b != ts / p.Q) return;
-    const int c0 = static_cast<int>(ts / p.Q), c1 = static_cast<int>((ts + p.KC - 1) / p.Q);
-    const int s0 = (static_cast<int64_t>(c0) * p.Q < ts) ? 1 : 0;
+    const int64_t ts = tile * p.KC;  // >= w0: w0 is a tile boundary
+    if (w == ts || b != (ts - p.w0) / p.Q) return;
+    const int c0 = static_cast<int>((ts - p.w0) / p.Q), c1 = static_cast<int>((ts + p.KC - 1 - p.w0) / p.Q);
+    const int s0 = (p.w0 + static_cast<int64_t>(c0) * p.Q < ts) ? 1 : 0;
     const int rt = static_cast<int>(tile / p.TT), tt = static_cast<int>(tile - static_cast<int64_t>(rt) * p.TT);
     const int N = p.N;
     // warp wi handles tokens j0 + wi + 4k (k < 8); lane l rows 4l..4l+3 (float4)
@@ -727,7 +735,8 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t s
     cudaError_t e = cudaLaunchKernelEx(&cfg, k, p);
     if (e != cudaSuccess) return e;
     if (!p.rr && p.Q % p.KC != 0) {  // some tiles are split along K: stream-K fix-up
-        gemm_reduce_kernel<<<dim3((p.N + 31) / 32, grid), 128, 0, st>>>(p);
+        const int nb = static_cast<int>((p.work - p.w0 + p.Q - 1) / p.Q);  // CTAs with a stream-K range
+        gemm_reduce_kernel<<<dim3((p.N + 31) / 32, nb), 128, 0, st>>>(p);
         e = cudaGetLastError();
     }
     return e;
@@ -932,10 +941,27 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     p.rr = sk ? 0 : 1;
     if (const char* e = getenv("SFMP_GEMM_SK")) p.rr = atoi(e) ? 0 : 1;
     p.Q = p.KC;
+    p.w0 = p.work;
     int S = static_cast<int>(std::min<int64_t>(ntiles, sms));
     if (!p.rr) {
+        p.w0 = 0;
         p.Q = std::max<int64_t>(std::min<int64_t>(p.KC, 8), (p.work + sms - 1) / sms);
         S = static_cast<int>((p.work + p.Q - 1) / p.Q);
+    } else if (ntiles > sms) {
+        // Hybrid: full rounds of whole tiles, the remainder (a partial wave)
+        // as stream-K ranges of >= 8 steps over all CTAs -- when the remainder
+        // is small (measured: gate/up 896 tiles = 6 x 148 + 8: 195 -> 190 us;
+        // with a large remainder the partial tiles' reduction costs more than
+        // the idle SMs: q 256 = 148 + 108 tiles, 63 -> 68 us).
+        const int64_t rounds = ntiles / sms, rem = ntiles - rounds * sms;
+        bool hybrid = rem > 0 && rem * 4 <= static_cast<int64_t>(sms);
+        if (const char* e = getenv("SFMP_GEMM_HYBRID")) hybrid = hybrid && atoi(e) != 0;
+        if (hybrid) {
+            p.rr = 0;
+            p.w0 = rounds * sms * p.KC;
+            p.Q = std::max<int64_t>(8, (rem * p.KC + sms - 1) / sms);
+            S = sms;
+        }
     }
     switch (m.ceil_bits) {
         case 1: return launch_np<1>(p, smem, S, st);
