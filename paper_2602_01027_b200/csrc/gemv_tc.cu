@@ -113,7 +113,12 @@ struct XParams {
 //   n-tile nt: one 16-byte load initialises an accumulator, so C - bias comes
 //   out of the MMA itself.
 // Within a (c, nt, n) run the 8 k-steps are contiguous (stride 32 B), so a
-// lane's fragment addresses are compile-time offsets from one base.
+// lane's fragment addresses are compile-time offsets from one base.  Runs are
+// kRun = 288 B apart (256 B + 32 B pad): a warp's k-step load then spreads the
+// 8 tokens over all 32 banks (2 wavefronts for 256 B) instead of hitting one
+// bank pair 8 times (at 256 B stride the B loads were 59 % bank conflicts and
+// the shared-memory pipe the M=16 bottleneck).
+constexpr int kRun = 288;
 // float index (from xg_off) of token t's accumulator-init slots, layout hi=0/1
 __host__ __device__ __forceinline__ int bias_slot(int t, int hi) {
     return 16 + hi * 32 + ((t >> 3) * 4 + ((t & 7) >> 1)) * 4 + (t & 1);
@@ -122,9 +127,9 @@ struct RecGeom {
     int M;
     __host__ __device__ int mnt(int nt) const { return nt == 0 ? (M < 8 ? M : 8) : M - 8; }
     __host__ __device__ int nt_count() const { return M > 8 ? 2 : 1; }
-    __host__ __device__ int chunk_bytes() const { return 256 * M; }  // all n-tiles
+    __host__ __device__ int chunk_bytes() const { return kRun * M; }  // all n-tiles
     __host__ __device__ int lane_off(int c, int nt, int n, int q) const {
-        return c * chunk_bytes() + nt * 2048 + n * 256 + q * 8;
+        return c * chunk_bytes() + nt * 8 * kRun + n * kRun + q * 8;
     }
     __host__ __device__ int frag_off(int c, int nt, int s, int n, int q) const {
         return lane_off(c, nt, n, q) + s * 32;
