@@ -483,9 +483,11 @@ def main():
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
     # Group order of the e2e step: a small group first (short exposed H2D), the
-    # largest second (its H2D hides under the first group's compute, its D2H
-    # under the later groups'), a small group last (short exposed D2H).
-    E2E_MS = [int(v) for v in args.e2e_order.split(",")] if args.e2e_order else [1, 16, 8, 4, 2]
+    # largest late enough that its H2D (2.5 MB, the slowest copy) hides under
+    # three groups' compute, a small group last (short exposed D2H).  Measured
+    # (200 steps each, noisy): 1,4,8,16,2 -> 247-283 us; 1,16,8,4,2 -> 270-350;
+    # 1,2,4,8,16 -> 290-348.
+    E2E_MS = [int(v) for v in args.e2e_order.split(",")] if args.e2e_order else [1, 4, 8, 16, 2]
     assert sorted(E2E_MS) == sorted(MS)
 
     def e2e_body(i):
