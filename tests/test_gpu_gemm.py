@@ -85,10 +85,11 @@ def test_gemm_deterministic_linear_zero(gpu, port):
     assert torch.equal(y2, 2 * a)
 
 
-@pytest.mark.parametrize("proj", ["q_proj", "k_proj", "down_proj"])
+@pytest.mark.parametrize("proj", ["q_proj", "k_proj", "gate_proj", "down_proj"])
 def test_llama8b_prefill_parity(gpu, port, proj):
-    """configs[2]: Llama-3.1-8B linears at avg 3.25 bits, prefill M=2048;
-    checked on a seeded sample of token rows (first/last included)."""
+    """configs[2]: Llama-3.1-8B linears at avg 3.25 bits, prefill M=2048
+    (q/down: whole tiles; k: stream-K; gate: whole-tile rounds + stream-K over
+    the last partial wave); checked on a seeded sample of token rows."""
     import torch
     rows, cols = LLAMA_8B[proj]
     M = 2048
@@ -117,3 +118,20 @@ def test_gemm_misaligned_x_routes_to_gemv(gpu, port):
     assert errors(y, ref)[0] <= TOL
     with pytest.raises(gpu.SfmpError):
         dm.gemm(x, path=gpu.PATH_GEMM)
+
+
+@pytest.mark.parametrize("dtype,legacy", [("bfloat16", False), ("bfloat16", True), ("float32", False)])
+def test_gemm_prepass_variants(gpu, port, dtype, legacy, monkeypatch):
+    """Both prefill pre-passes: the persistent row-streaming one (bf16 rows of
+    a 14336-column linear) and the one-token-per-CTA one (forced, and taken
+    by f32 rows whose two staging buffers exceed its shared-memory budget)."""
+    import torch
+    if legacy:
+        monkeypatch.setenv("SFMP_XPREP_LEGACY", "1")
+    rows, cols, M = 512, 14336, 300
+    data = model_bytes(port, rows, cols, 3.0)
+    dm = gpu.DeviceModel(data)
+    xt = torch.from_numpy(activations(port, M, cols, seed=21)).cuda().to(getattr(torch, dtype))
+    y = dm.gemm(xt, path=gpu.PATH_GEMM).cpu().numpy()
+    ref = port.matmul(xt.float().cpu().numpy(), port.load(data).dequantize(), threads=8)
+    assert errors(y, ref)[0] <= TOL
