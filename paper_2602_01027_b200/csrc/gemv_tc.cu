@@ -45,19 +45,22 @@ namespace sfmpk {
 namespace {
 
 constexpr int kTR = 128;  // rows per unit
-constexpr int kMT = 2;            // m16 tiles (16 rows each) per compute warp
-constexpr int kNCW = 8 / kMT;     // compute warps per 128-row tile
+#ifndef SFMP_GEMV_MT
+#define SFMP_GEMV_MT 2
+#endif
+constexpr int kMT = SFMP_GEMV_MT;  // m16 tiles (16 rows each) per compute warp
+constexpr int kNCW = 8 / kMT;      // compute warps per 128-row tile
 #ifndef SFMP_GEMV_CTAS1
-#define SFMP_GEMV_CTAS1 4
+#define SFMP_GEMV_CTAS1 (SFMP_GEMV_MT == 2 ? 4 : 3)
 #endif
 #ifndef SFMP_GEMV_CTAS2
-#define SFMP_GEMV_CTAS2 3
+#define SFMP_GEMV_CTAS2 (SFMP_GEMV_MT == 2 ? 3 : 2)
 #endif
 constexpr int kCtasNT1 = SFMP_GEMV_CTAS1, kCtasNT2 = SFMP_GEMV_CTAS2;  // resident CTAs per SM
 constexpr int kThreads = 32 * (1 + kNCW);
 constexpr int kHdrBytes = 1280;  // barriers | zeros | stage bit-widths | out_map
 // resident CTAs per SM: 4 for M<=8 (NT=1), 3 for M<=16 (NT=2, more registers)
-__host__ __device__ constexpr int ctas_per_sm(int NT) { return kMT == 2 ? (NT == 1 ? kCtasNT1 : kCtasNT2) : (NT == 1 ? 3 : 2); }
+__host__ __device__ constexpr int ctas_per_sm(int NT) { return NT == 1 ? kCtasNT1 : kCtasNT2; }
 __host__ __device__ constexpr int smem_per_cta(int NT) { return (225 * 1024) / ctas_per_sm(NT); }
 
 // One linear of a (possibly grouped) launch: independent matrices -- e.g. the
@@ -701,9 +704,10 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 // issued one at a time.
                 // One row per thread, all tokens; RB splits per round so that
                 // RB*8*NT loads are in flight together (latency, not bandwidth).
-                static_assert(kNCW * 32 == kTR, "fixup maps one compute thread per row");
+                static_assert(kNCW * 32 >= kTR, "fixup maps one compute thread per row");
                 constexpr int RB = NT == 1 ? 4 : 2;
                 const int row = threadIdx.x - 32;
+                if (row < kTR) {
                 const float* pp = L.part + static_cast<size_t>(rt) * kMaxSplit * (16 * kTR) + row;
                 const uint32_t orow = __ldg(L.out_map + rt * kTR + row);
                 float acc[8 * NT];
@@ -727,6 +731,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                 for (int t = 0; t < 8 * NT; ++t)
                     if (t < p.M) L.y[t * L.out_rows + orow] = acc[t];
+                }
                 if (threadIdx.x == 32) L.counters[rt] = 0u;  // ready for the next call (stream-ordered)
                 if (threadIdx.x == 32) DBG_STAMP(126);
             }
