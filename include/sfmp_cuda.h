@@ -169,6 +169,13 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
 sfmp_status sfmp_gemm_grouped(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
                               int64_t M, float* const* ys, void* const* workspaces, const size_t* workspace_bytes,
                               int count, void* stream);
+/* Same with a token count per problem (Ms[i] rows of xs[i] / ys[i]), e.g. the
+ * experts of a mixture-of-experts layer.  Consecutive decode problems (M <= 16)
+ * that are groupable, fall in the same class (M <= 8 or 9..16) and use distinct
+ * workspaces share one launch (up to 40 per launch). */
+sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                                const int64_t* Ms, float* const* ys, void* const* workspaces,
+                                const size_t* workspace_bytes, int count, void* stream);
 /* Host-buffer convenience with the reference's calling convention: x and y
  * are HOST arrays; copies, kernel and synchronisation happen inside. */
 sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M,

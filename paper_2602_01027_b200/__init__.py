@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = (
     "sfmp_model_create_from_parts", "sfmp_model_create_shard", "sfmp_model_destroy",
     "sfmp_model_get_info", "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
     "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered", "sfmp_shard_plan",
-    "sfmp_shard_extract", "sfmp_gemm_grouped",
+    "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v",
 )
 
 
@@ -127,12 +127,13 @@ def lib() -> C.CDLL:
     L.sfmp_unpermute_gathered.argtypes = [vp, vp, i64, vp, vp]
     L.sfmp_shard_plan.argtypes = [vp, sz, C.c_uint32, vp, C.POINTER(C.c_uint64)]
     L.sfmp_gemm_grouped.argtypes = [vp, vp, C.c_int, i64, vp, vp, vp, C.c_int, vp]
+    L.sfmp_gemm_grouped_v.argtypes = [vp, vp, C.c_int, vp, vp, vp, vp, C.c_int, vp]
     L.sfmp_shard_extract.argtypes = [vp, sz, C.c_uint32, C.c_uint32, vp, C.POINTER(C.c_size_t)]
     for name in ("sfmp_parse_header", "sfmp_block_offsets", "sfmp_model_create",
                  "sfmp_model_create_shard", "sfmp_model_destroy", "sfmp_model_get_info",
                  "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
                  "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered",
-                 "sfmp_shard_plan", "sfmp_shard_extract", "sfmp_gemm_grouped"):
+                 "sfmp_shard_plan", "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -316,27 +317,30 @@ class DeviceModel:
 
 
 def gemm_grouped(models, xs, outs=None, workspaces=None, stream=None):
-    """Independent linears in one call (sfmp_gemm_grouped): y_i = x_i . W_i^T.
-    For decode M the whole group is one activation pre-pass + one GEMV launch."""
+    """Independent linears in one call: y_i = x_i . W_i^T, x_i [M_i, cols_i] of one
+    dtype (M_i may differ: sfmp_gemm_grouped_v).  Decode problems (M_i <= 16) of
+    one n-tile class (M <= 8 or 9..16) with distinct workspaces share one
+    activation pre-pass + one GEMV launch."""
     import torch
     n = len(models)
     xs = [x.contiguous() for x in xs]
-    M = xs[0].shape[0]
     dt = _dtype_code(xs[0])
     for m, x in zip(models, xs):
-        if x.shape != (M, m.cols) or _dtype_code(x) != dt:
+        if x.dim() != 2 or x.shape[1] != m.cols or _dtype_code(x) != dt:
             raise ShapeError("gemm_grouped: every x must be [M, cols] of one dtype")
+    Ms = [x.shape[0] for x in xs]
     if outs is None:
-        outs = [torch.empty(M, m.out_rows, dtype=torch.float32, device=x.device) for m, x in zip(models, xs)]
+        outs = [torch.empty(M, m.out_rows, dtype=torch.float32, device=x.device) for m, x, M in zip(models, xs, Ms)]
     if workspaces is None:
-        workspaces = [m.workspace(min(M, 16) if M <= 16 else M) for m in models]
+        workspaces = [m.workspace(min(M, 16) if M <= 16 else M) for m, M in zip(models, Ms)]
     P = C.c_void_p * n
     hs = P(*[m.handle for m in models])
     xp = P(*[x.data_ptr() for x in xs])
     yp = P(*[y.data_ptr() for y in outs])
     wp = P(*[(w.data_ptr() if w is not None else None) for w in workspaces])
     wb = (C.c_size_t * n)(*[(w.numel() if w is not None else 0) for w in workspaces])
-    check(lib().sfmp_gemm_grouped(hs, xp, dt, M, yp, wp, wb, n, _stream_ptr(stream)))
+    mp = (C.c_int64 * n)(*Ms)
+    check(lib().sfmp_gemm_grouped_v(hs, xp, dt, mp, yp, wp, wb, n, _stream_ptr(stream)))
     return outs
 
 

@@ -655,38 +655,64 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
 sfmp_status sfmp_gemm_grouped(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
                               int64_t M, float* const* ys, void* const* workspaces, const size_t* workspace_bytes,
                               int count, void* stream) {
-    if (count < 0 || (count && (!models || !xs || !ys || !workspaces)))
-        return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    if (count < 0) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
     if (M < 0) return fail(SFMP_ERR_SHAPE, "negative M");
-    if (M == 0 || count == 0) return SFMP_OK;
+    std::vector<int64_t> Ms(count > 0 ? count : 1, M);
+    return sfmp_gemm_grouped_v(models, xs, dtype, Ms.data(), ys, workspaces, workspace_bytes, count, stream);
+}
+
+sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                                const int64_t* Ms, float* const* ys, void* const* workspaces,
+                                const size_t* workspace_bytes, int count, void* stream) {
+    if (count < 0 || (count && (!models || !xs || !ys || !workspaces || !Ms)))
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    if (count == 0) return SFMP_OK;
     if (dtype != SFMP_F32 && dtype != SFMP_F16 && dtype != SFMP_BF16)
         return fail(SFMP_ERR_INVALID_ARGUMENT, "bad dtype");
     std::vector<const DevModel*> ms(count);
     for (int i = 0; i < count; ++i) {
-        if (!models[i] || !xs[i] || !ys[i]) return fail(SFMP_ERR_INVALID_ARGUMENT, "null model/x/y");
+        if (Ms[i] < 0) return fail(SFMP_ERR_SHAPE, "negative M");
+        if (!models[i] || (Ms[i] && (!xs[i] || !ys[i]))) return fail(SFMP_ERR_INVALID_ARGUMENT, "null model/x/y");
         ms[i] = reinterpret_cast<const DevModel*>(models[i]);
     }
-    // Runs of groupable decode linears go out as one launch; anything else
+    // Runs of groupable decode problems go out as one launch; anything else
     // (prefill M, odd geometry) falls to the per-model entry point.
-    const bool decode = M <= 16;
+    auto decode_ok = [&](int k) {
+        if (Ms[k] < 1 || Ms[k] > 16 || !ms[k]->gemv_ok || !workspaces[k]) return false;
+        return !workspace_bytes || workspace_bytes[k] >= sfmpk::gemv_workspace_bytes(*ms[k], 16);
+    };
     int i = 0;
     while (i < count) {
         int j = i + 1;
-        if (decode && ms[i]->gemv_ok) {
-            const size_t need = sfmpk::gemv_workspace_bytes(*ms[i], 16);
-            if (!workspaces[i] || (workspace_bytes && workspace_bytes[i] < need))
+        if (Ms[i] == 0) {
+            i = j;
+            continue;
+        }
+        if (Ms[i] <= 16 && ms[i]->gemv_ok) {
+            if (!decode_ok(i))
                 return fail(SFMP_ERR_CONFIG, "grouped decode needs a workspace per model (sfmp_workspace_size)");
-            while (j < count && j - i < 16 && sfmpk::gemv_groupable(*ms[i], *ms[j]) && workspaces[j] &&
-                   (!workspace_bytes || workspace_bytes[j] >= sfmpk::gemv_workspace_bytes(*ms[j], 16)))
+            const bool wide = Ms[i] > 8;
+            // same n-tile class, groupable geometry, and a workspace of its own
+            // (the records / partials / counters of one launch must not alias)
+            while (j < count && j - i < 40 && decode_ok(j) && (Ms[j] > 8) == wide &&
+                   sfmpk::gemv_groupable(*ms[i], *ms[j])) {
+                bool distinct = true;
+                for (int k = i; k < j; ++k) distinct = distinct && workspaces[k] != workspaces[j];
+                if (!distinct) break;
                 ++j;
+            }
             DeviceGuard guard(ms[i]->device);
             std::vector<uint8_t*> wss(j - i);
-            for (int k = i; k < j; ++k) wss[k - i] = static_cast<uint8_t*>(workspaces[k]);
-            cudaError_t e = sfmpk::launch_gemv_group(ms.data() + i, xs + i, ys + i, wss.data(), j - i, dtype,
-                                                     static_cast<int>(M), static_cast<cudaStream_t>(stream));
+            std::vector<int> mi(j - i);
+            for (int k = i; k < j; ++k) {
+                wss[k - i] = static_cast<uint8_t*>(workspaces[k]);
+                mi[k - i] = static_cast<int>(Ms[k]);
+            }
+            cudaError_t e = sfmpk::launch_gemv_group(ms.data() + i, xs + i, ys + i, wss.data(), mi.data(), j - i, dtype,
+                                                     static_cast<cudaStream_t>(stream));
             if (e != cudaSuccess) return cuda_fail(e, "grouped GEMV launch");
         } else {
-            sfmp_status s = sfmp_gemm(models[i], xs[i], dtype, M, ys[i], workspaces[i],
+            sfmp_status s = sfmp_gemm(models[i], xs[i], dtype, Ms[i], ys[i], workspaces[i],
                                       workspace_bytes ? workspace_bytes[i] : 0, stream);
             if (s) return s;
         }

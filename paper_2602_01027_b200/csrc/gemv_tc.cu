@@ -66,7 +66,7 @@ __host__ __device__ constexpr int smem_per_cta(int NT) { return (225 * 1024) / c
 // One linear of a (possibly grouped) launch: independent matrices -- e.g. the
 // seven linears of a decoder layer -- share one launch so the fixed per-call
 // latencies (launch, first HBM bytes, split-K tail) are paid once.
-constexpr int kMaxLin = 16;
+constexpr int kMaxLin = 40;
 constexpr int kMaxSplit = 32;  // CTAs that may share one row tile
 struct Lin {
     const uint8_t* payload;
@@ -78,6 +78,8 @@ struct Lin {
     unsigned* counters;         // [RT] completion counters (zero between calls)
     uint64_t out_rows;
     int BC;
+    int M;                      // tokens of this linear (problems of one launch may differ)
+    uint32_t rec_bytes;         // its activation record bytes (RecGeom{M})
     int64_t unit0;              // first unit of this linear in the group's unit sequence
 };
 struct Params {
@@ -85,11 +87,11 @@ struct Params {
     int nlin;
     int64_t units;  // units of all linears
     int64_t Q;      // units per CTA
-    int M;
+    int M;          // max tokens over the linears (all <= 8 or all in 9..16)
     int n_b;
     int stages;
     uint32_t stage_w;    // bytes per weight stage (smem)
-    uint32_t rec_bytes;  // bytes per activation record (smem and global)
+    uint32_t rec_bytes;  // max activation record bytes (shared-memory stage stride)
     int debug_mode;      // 0 normal; 5 timeline stamps
 };
 struct XLin {
@@ -99,6 +101,8 @@ struct XLin {
     int BC, cols, warp0;
     int item0;  // first pre-pass CTA column (groups of 8 block columns) of this linear
     int lo;     // floor bit-width: records carry the magic biases of lo and lo+1 bit units
+    int M;      // tokens of this linear
+    uint32_t rec_bytes;
 };
 struct XParams {
     XLin lin[kMaxLin];
@@ -221,11 +225,13 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
         g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 104] = g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102];
         DBG_KSTAMP(100);
     }
-    const int M = xp.M, n_b = xp.n_b, CH = n_b >> 7;
+    const int n_b = xp.n_b, CH = n_b >> 7;
     const int t = blockIdx.y;
     int it = blockIdx.x, li = 0;
     while (li + 1 < xp.nlin && it >= xp.lin[li + 1].item0) ++li;
     const XLin& XL = xp.lin[li];
+    const int M = XL.M;
+    if (t >= M) return;  // grid.y = the launch's largest M
     it -= XL.item0;
     const int bc0 = it * 8, nbc = min(8, XL.BC - bc0), cols = XL.cols;
     uint32_t* cp = reinterpret_cast<uint32_t*>(xsm);  // [nbc][n_b] column indices
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     if (warp >= nbc) return;
     const int bc = bc0 + warp, s8 = lane >> 2, q = lane & 3;
     const RecGeom G{M};
-    uint8_t* rec = XL.xrec + static_cast<size_t>(bc) * xp.rec_bytes;
+    uint8_t* rec = XL.xrec + static_cast<size_t>(bc) * XL.rec_bytes;
     const uint32_t* cpw = cp + warp * n_b;
     const int lo = XL.lo;
     auto mag = [](int B, int j) { return B <= 4 ? rp_magic(B, j) : 0.f; };
@@ -308,10 +314,8 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
         g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 104] = g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102];
         DBG_KSTAMP(100);
     }
-    const int M = xp.M, n_b = xp.n_b;
-    const uint32_t rec_bytes = xp.rec_bytes;
-    const RecGeom G{M};
-    const int NT = G.nt_count();
+    const int n_b = xp.n_b;
+    const int NT = RecGeom{xp.M}.nt_count();  // per launch (its linears share the n-tile count)
     const int CH = n_b >> 7;  // 1..8 (host: 8 % CH == 0)
     const int warp = threadIdx.x >> 5, c = warp % CH;
     int w = blockIdx.x * (8 / CH) + warp / CH;  // item
@@ -319,6 +323,9 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     while (li + 1 < xp.nlin && w >= xp.lin[li + 1].warp0) ++li;
     const XLin& XL = xp.lin[li];
     w -= XL.warp0;
+    const int M = XL.M;
+    const uint32_t rec_bytes = XL.rec_bytes;
+    const RecGeom G{M};
     const int BC = XL.BC, cols = XL.cols;
     const void* x = XL.x;
     const uint32_t* col_perm = XL.col_perm;
@@ -502,7 +509,6 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     __syncthreads();
 
     constexpr int nb8 = CH * 16;
-    const RecGeom G{p.M};
 
     if (warp == 0) {
         // ---------------- producer: one bulk copy per unit (+ its activation record) ----
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 sbits[s] = static_cast<uint32_t>(bits);  // published by the arrive below
                 DBG_USTAMP(2 + 3 * gi);
                 const uint32_t wbytes = 4 * kTR + bits * pbytes;
-                mbar_arrive_expect_tx(&full[s], wbytes + p.rec_bytes);
+                mbar_arrive_expect_tx(&full[s], wbytes + L.rec_bytes);
                 bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
                          &full[s], pol);
             };
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                         smem_u32(xbase + static_cast<size_t>(s) * p.rec_bytes)),
-                    "l"(L.xrec + static_cast<size_t>(bc_) * p.rec_bytes), "r"(p.rec_bytes), "r"(smem_u32(&full[s]))
+                    "l"(L.xrec + static_cast<size_t>(bc_) * L.rec_bytes), "r"(L.rec_bytes), "r"(smem_u32(&full[s]))
                     : "memory");
             };
             int s = 0, ph = 0;
@@ -575,20 +581,13 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         const int cw = warp - 1;
         const int g = lane >> 2, q = lane & 3;
         const int r0 = cw * 16 * kMT + g;  // rows r0 + 8*r of the tile
-        const int chunk_bytes = G.chunk_bytes();
         const uint32_t stage_w = p.stage_w, rec_bytes = p.rec_bytes;
         // per-lane shared addresses for stage 0; a stage adds s * stage_w / rec_bytes
         const uint32_t prow0 = smem_u32(wbase) + 4 * kTR + r0 * nb8 + q * 4;
         const uint32_t sz0 = smem_u32(wbase) + 2 * r0;
-        uint32_t xb0[NT], xstep[NT];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const bool live = g < G.mnt(nt);
-            xb0[nt] = live ? smem_u32(xbase) + G.lane_off(0, nt, g, q) : smem_u32(zeros) + q * 8;
-            xstep[nt] = live ? rec_bytes : 0u;
-        }
-        const uint32_t xg0 = smem_u32(xbase) + G.xg_off(CH) + 8 * q;
-        const uint32_t bc_a = smem_u32(xbase) + G.xg_off(CH) + 64 + 16 * q;  // accumulator inits
+        // record addresses depend on the linear's M: set per segment
+        int chunk_bytes = 0, cur_li = -1;
+        uint32_t xb0[NT], xstep[NT], xg0 = 0, bc_a = 0;
         const uint32_t sbits_a = smem_u32(sbits);
         const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
         int s = 0, ph = 0, gi = 0;
@@ -599,6 +598,19 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
             u += I.bc1 - I.bc0;
             const Lin& L = p.lin[I.li];
             const int C = I.C, rt = I.rt, nunits = I.bc1 - I.bc0;
+            if (I.li != cur_li) {
+                cur_li = I.li;
+                const RecGeom GL{L.M};
+                chunk_bytes = GL.chunk_bytes();
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const bool live = g < GL.mnt(nt);
+                    xb0[nt] = live ? smem_u32(xbase) + GL.lane_off(0, nt, g, q) : smem_u32(zeros) + q * 8;
+                    xstep[nt] = live ? rec_bytes : 0u;
+                }
+                xg0 = smem_u32(xbase) + GL.xg_off(CH) + 8 * q;
+                bc_a = smem_u32(xbase) + GL.xg_off(CH) + 64 + 16 * q;  // accumulator inits
+            }
             float yacc[kMT][NT][4];
 #pragma unroll
             for (int m = 0; m < kMT; ++m)
@@ -669,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int t = nt * 8 + 2 * q + (e & 1);
-                            if (t < p.M)
+                            if (t < L.M)
                                 L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + r0 + 16 * m + 8 * (e >> 1))] =
                                     yacc[m][nt][e];
                         }
@@ -684,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int t = nt * 8 + 2 * q + (e & 1);
-                        if (t < p.M) part[t * kTR + r0 + 16 * m + 8 * (e >> 1)] = yacc[m][nt][e];
+                        if (t < L.M) part[t * kTR + r0 + 16 * m + 8 * (e >> 1)] = yacc[m][nt][e];
                     }
             // Deterministic split-K: the last of the C items of this row tile
             // sums the partials in split order and stores them un-permuted.
@@ -719,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                     for (int r = 0; r < RB; ++r)
 #pragma unroll
                         for (int t = 0; t < 8 * NT; ++t)
-                            v[r][t] = (r0 + r < C && t < p.M)
+                            v[r][t] = (r0 + r < C && t < L.M)
                                           ? pp[static_cast<size_t>(r0 + r) * (16 * kTR) + t * kTR]
                                           : 0.f;
 #pragma unroll
@@ -730,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 }
 #pragma unroll
                 for (int t = 0; t < 8 * NT; ++t)
-                    if (t < p.M) L.y[t * L.out_rows + orow] = acc[t];
+                    if (t < L.M) L.y[t * L.out_rows + orow] = acc[t];
                 }
                 if (threadIdx.x == 32) L.counters[rt] = 0u;  // ready for the next call (stream-ordered)
                 if (threadIdx.x == 32) DBG_STAMP(126);
@@ -858,17 +870,24 @@ bool gemv_groupable(const DevModel& a, const DevModel& b) {
 }
 
 cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, float* const* ys, uint8_t* const* wss,
-                              int n, sfmp_dtype dt, int M, cudaStream_t st) {
+                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st) {
     if (n < 1 || n > kMaxLin) return cudaErrorInvalidValue;
     const DevModel& m0 = *ms[0];
+    int M = 0;
+    for (int i = 0; i < n; ++i) {
+        if (Ms[i] < 1 || Ms[i] > 16) return cudaErrorInvalidValue;
+        M = std::max(M, Ms[i]);
+    }
     const int NT = M > 8 ? 2 : 1;
+    for (int i = 0; i < n; ++i)
+        if ((Ms[i] > 8 ? 2 : 1) != NT) return cudaErrorInvalidValue;  // one n-tile count per launch
     const int CH = static_cast<int>(m0.n_b / 128);
     Params p{};
     XParams xp{};
     p.nlin = xp.nlin = n;
     p.M = xp.M = M;
     p.n_b = xp.n_b = static_cast<int>(m0.n_b);
-    p.rec_bytes = xp.rec_bytes = static_cast<uint32_t>(RecGeom{M}.bytes(CH));
+    p.rec_bytes = xp.rec_bytes = static_cast<uint32_t>(RecGeom{M}.bytes(CH));  // stage stride: the largest
     {
         const char* dbg = getenv("SFMP_GEMV_DEBUG");
         p.debug_mode = xp.dbg = dbg ? atoi(dbg) : 0;
@@ -903,6 +922,8 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         L.counters = reinterpret_cast<unsigned*>(wss[i] + gemv_rec_bytes(m) + gemv_part_bytes(m));
         L.out_rows = m.out_rows;
         L.BC = BC;
+        L.M = Ms[i];
+        L.rec_bytes = static_cast<uint32_t>(RecGeom{Ms[i]}.bytes(CH));
         L.unit0 = unit0;
         unit0 += static_cast<int64_t>(m.RT) * BC;
         XLin& X = xp.lin[i];
@@ -914,6 +935,8 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         X.warp0 = xwarps;
         X.item0 = xitems;
         X.lo = m.floor_bits;
+        X.M = Ms[i];
+        X.rec_bytes = L.rec_bytes;
         xwarps += BC * NT;
         xitems += (BC + 7) / 8;
         max_cols = std::max(max_cols, X.cols);
@@ -942,7 +965,8 @@ cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, 
     const void* xs[1] = {x};
     float* ys[1] = {y};
     uint8_t* wss[1] = {reinterpret_cast<uint8_t*>(ws)};
-    return launch_gemv_group(ms, xs, ys, wss, 1, dt, M, st);
+    const int Ms[1] = {M};
+    return launch_gemv_group(ms, xs, ys, wss, Ms, 1, dt, st);
 }
 
 }  // namespace sfmpk

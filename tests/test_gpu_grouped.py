@@ -38,3 +38,33 @@ def test_grouped_mixed_geometry_and_prefill(gpu, port):
         for d, x, y in zip(datas, xs_np, ys):
             ref = port.matmul(x, port.load(d).dequantize(), threads=8)
             assert errors(y.cpu().numpy(), ref)[0] <= 1e-3
+
+
+def test_grouped_per_problem_token_counts(gpu, port):
+    """sfmp_gemm_grouped_v: problems with different M in one call -- M <= 8 ones
+    share a launch, 9..16 another, M > 16 and M = 0 go their own way; a shared
+    workspace splits the launch instead of aliasing its records."""
+    import torch
+    datas = [model_bytes(port, r, c, 3.25, m_b=mb, seed=i) for i, (r, c, mb) in enumerate(SHAPES)]
+    models = [gpu.DeviceModel(d) for d in datas]
+    Ms = [1, 3, 8, 5, 2, 12, 16, 9, 40, 0]
+    picks = [i % len(models) for i in range(len(Ms))]
+    xs_np = [activations(port, max(M, 1), models[k].cols, seed=30 + i)[:M] for i, (M, k) in enumerate(zip(Ms, picks))]
+    xs = [torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16).reshape(M, models[k].cols)
+          for x, M, k in zip(xs_np, Ms, picks)]
+    sel = [models[k] for k in picks]
+    # every problem its own zeroed workspace, except problems 0 and 3 (both
+    # M <= 8) which share one: the M <= 8 run must split there
+    ws = [torch.zeros(m.workspace_bytes(max(M, 1)), dtype=torch.uint8, device="cuda") for m, M in zip(sel, Ms)]
+    ws[0] = ws[3] = torch.zeros(max(sel[0].workspace_bytes(16), sel[3].workspace_bytes(16)), dtype=torch.uint8,
+                                device="cuda")
+    ys = gpu.gemm_grouped(sel, xs, workspaces=ws)
+    for i, (M, k) in enumerate(zip(Ms, picks)):
+        assert ys[i].shape == (M, models[k].out_rows)
+        if M == 0:
+            continue
+        ref = port.matmul(xs[i].float().cpu().numpy(), port.load(datas[k]).dequantize(), threads=8)
+        assert errors(ys[i].cpu().numpy(), ref)[0] <= 1e-3, (i, M)
+        # same as the single-problem call (same kernels, split-K grouping may differ)
+        y1 = sel[i].gemm(xs[i])
+        assert torch.allclose(ys[i], y1, rtol=1e-4, atol=1e-4), (i, M)
