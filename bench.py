@@ -308,6 +308,9 @@ def main():
     ap.add_argument("--soak-ms", type=float, default=1500.0)
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-group", action="store_true", help="one launch per linear instead of per decoder layer")
+    ap.add_argument("--group-per-m", action="store_true",
+                    help="one grouped call per M (5 launches) instead of one call for the whole step "
+                         "(the API then issues one launch per n-tile class: M<=8 and M=16)")
     ap.add_argument("--prefill-M", type=int, default=2048)
     ap.add_argument("--e2e-order", default="", help="comma list: order of the M groups in the e2e step")
     args = ap.parse_args()
@@ -338,18 +341,29 @@ def main():
           .to(torch.bfloat16) for p in PROJS for M in MS}
     ys = {(p, M): torch.empty(M, models[0][p].out_rows, device=dev) for p in PROJS for M in MS}
     ws = {p: models[0][p].workspace(16, sfmp.PATH_GEMV) for p in PROJS}
+    # a workspace per (linear, M): problems of one launch must not share one
+    wsm = {(p, M): torch.zeros_like(ws[p]) for p in PROJS for M in MS}
     if world > 1:
         gath = {(p, M): torch.empty(world, M, models[0][p].out_rows, device=dev)
                 for p in PROJS for M in MS}
         yfull = {(p, M): torch.empty(M, SHAPES[p][0], device=dev) for p in PROJS for M in MS}
 
     grouped = not args.no_group
+    across = grouped and not args.group_per_m and world == 1
     # launches of OUR kernels per step: grouped = (x pre-pass + GEMV) per M;
     # per-linear = (x pre-pass + GEMV) per call; sharded adds the un-permute
-    launches_per_step = (len(MS) * 2 if grouped else len(MS) * len(PROJS) * 2) + \
+    n_class = len({M > 8 for M in MS})
+    launches_per_step = ((n_class * 2 if across else len(MS) * 2) if grouped else len(MS) * len(PROJS) * 2) + \
         (len(MS) * len(PROJS) if world > 1 else 0)
 
     def step(i, group=grouped):
+        if group and across:
+            # the whole step (7 linears x 5 token counts, 4 weight copies) in one
+            # grouped call: one pre-pass + one GEMV launch per n-tile class
+            keys = [(p, M, (i * len(MS) + mi) % COPIES) for mi, M in enumerate(MS) for p in PROJS]
+            sfmp.gemm_grouped([models[c][p] for p, M, c in keys], [xs[(p, M)] for p, M, c in keys],
+                              outs=[ys[(p, M)] for p, M, c in keys], workspaces=[wsm[(p, M)] for p, M, c in keys])
+            return
         for mi, M in enumerate(MS):
             c = (i * len(MS) + mi) % COPIES
             if group:
@@ -580,7 +594,7 @@ def main():
         for M in MS:
             b = algo_bytes(info_local, M, rows_local, SHAPES[p][1])
             step_bytes += b
-    n_launch = len(MS) if grouped else len(MS) * len(PROJS)  # GEMV launches per step
+    n_launch = (n_class if across else len(MS)) if grouped else len(MS) * len(PROJS)  # GEMV launches per step
     t_us = t_ms * 1e3
     # achieved = algorithmic bytes of one GEMV launch / its share of the step
     # (each launch's time includes its x pre-pass: a lower bound on the kernel)
@@ -601,8 +615,11 @@ def main():
         "dtype": "f16", "data": "synthetic",
         "config": {"workload": WORKLOAD, "avg_code_bits": AVG_BITS, "M": MS,
                    "projections": PROJS, "kernel": "K1 decode GEMV (gemv_kernel) + x pre-pass (xprep_kernel)",
-                   "launch_grouping": ("the 7 linears of one M share one pre-pass + one GEMV launch "
-                                       "(sfmp_gemm_grouped)") if grouped else "one launch per linear",
+                   "launch_grouping": (("the whole step is one grouped call (sfmp_gemm_grouped_v, a token count "
+                                        "per problem): one pre-pass + one GEMV launch for the 28 M<=8 problems, "
+                                        "one for the 7 M=16 problems") if across else
+                                       ("the 7 linears of one M share one pre-pass + one GEMV launch "
+                                        "(sfmp_gemm_grouped)")) if grouped else "one launch per linear",
                    "ungrouped_step_us": round(ungrouped_ms * 1e3, 2) if ungrouped_ms else None,
                    "l2": f"inputs larger than L2: {COPIES} rotating device copies of the layer "
                          f"({sum(i['payload_bytes'] for i in infos.values()) * COPIES / 1e6:.0f} MB)",
