@@ -587,6 +587,7 @@ def main():
     hbm, tc, src = peaks()
     # roofline over the GEMV launches of one step (per-rank bytes when sharded)
     step_bytes = 0
+    small_bytes = 0  # the M <= 8 class launch
     per_point = []
     for p in PROJS:
         rows_local = models[0][p].rows
@@ -594,18 +595,20 @@ def main():
         for M in MS:
             b = algo_bytes(info_local, M, rows_local, SHAPES[p][1])
             step_bytes += b
+            small_bytes += b if M <= 8 else 0
     n_launch = (n_class if across else len(MS)) if grouped else len(MS) * len(PROJS)  # GEMV launches per step
     t_us = t_ms * 1e3
     # achieved = algorithmic bytes of one GEMV launch / its share of the step
     # (each launch's time includes its x pre-pass: a lower bound on the kernel)
     achieved = step_bytes / (t_us * 1e-6) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemv_grouped_8b_M1.json")
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemv_grouped_8b_Mle8.json" if across else
+                        "r01_ncu_gemv_grouped_8b_M1.json")
     if os.path.exists(prof):
         try:
             mb = json.load(open(prof))["metrics"]["dram__bytes_read.sum"].split()[0]
             wb = json.load(open(prof))["metrics"]["dram__bytes_write.sum"].split()[0]
-            traffic = round((float(mb) + float(wb)) * 1e6)  # ncu --set full, grouped M=1 launch
+            traffic = round((float(mb) + float(wb)) * 1e6)  # ncu --set full, one gemv_kernel launch
         except Exception:
             traffic = None
     out = {
@@ -632,8 +635,10 @@ def main():
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
                      "algorithmic_bytes_per_step": step_bytes,
                      "algorithmic_bytes_per_launch": step_bytes // n_launch,
-                     "traffic_note": "dram read+write of one grouped M=1 gemv_kernel launch "
-                                     "(profiles/r01_ncu_gemv_grouped_8b_M1.json)",
+                     "traffic_note": ("dram read+write of the step's M<=8 gemv_kernel launch (28 problems; "
+                                      f"algorithmic {small_bytes} B), profiles/r01_ncu_gemv_grouped_8b_Mle8.json")
+                     if across else ("dram read+write of one grouped M=1 gemv_kernel launch "
+                                     "(profiles/r01_ncu_gemv_grouped_8b_M1.json)"),
                      "avg_launch_us": round(t_us / n_launch, 3), "launches_per_step": n_launch},
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": ("pinned host x -> H2D per M group on a copy stream, sfmp_gemm_grouped per M, "
