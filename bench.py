@@ -501,7 +501,14 @@ def main():
     # three groups' compute, a small group last (short exposed D2H).  Measured
     # (200 steps each, noisy): 1,4,8,16,2 -> 247-283 us; 1,16,8,4,2 -> 270-350;
     # 1,2,4,8,16 -> 290-348.
-    E2E_MS = [int(v) for v in args.e2e_order.split(",")] if args.e2e_order else [1, 4, 8, 16, 2]
+    # --e2e-order: groups separated by '/', token counts by ',' (one grouped call
+    # per group; its H2D / D2H overlap the other groups' compute).  Measured
+    # (200 steps, two runs each): 1/4/8/16/2 244-245 us; 1,2/16/4,8 247-250;
+    # 1,2/4,8/16 259-268; 1/16/2,4,8 262-264; 1,2,4,8/16 296 -- finer groups
+    # overlap the PCIe copies better than fewer, larger launches.
+    E2E_GROUPS = ([[int(v) for v in g.split(",")] for g in args.e2e_order.split("/")] if args.e2e_order
+                  else [[1], [4], [8], [16], [2]])
+    E2E_MS = [M for g in E2E_GROUPS for M in g]
     assert sorted(E2E_MS) == sorted(MS)
 
     def e2e_body(i):
@@ -510,34 +517,39 @@ def main():
         h2d_s.wait_stream(cur)
         d2h_s.wait_stream(cur)
         ready = []
-        for M in E2E_MS:
+        for grp in E2E_GROUPS:
             with torch.cuda.stream(h2d_s):
-                a, b = gx[M]
-                dxb[a:b].copy_(hxb[a:b], non_blocking=True)
+                for M in grp:
+                    a, b = gx[M]
+                    dxb[a:b].copy_(hxb[a:b], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d_s)
                 ready.append(ev)
-        for mi, M in enumerate(E2E_MS):
-            c = (i * len(MS) + mi) % COPIES
-            cur.wait_event(ready[mi])
+        for gi_, grp in enumerate(E2E_GROUPS):
+            cur.wait_event(ready[gi_])
+            cs = {M: (i * len(MS) + MS.index(M)) % COPIES for M in grp}
             if world == 1:
                 if grouped:
-                    sfmp.gemm_grouped([models[c][p] for p in PROJS], [dx[(p, M)] for p in PROJS],
-                                      outs=[dy[(p, M)] for p in PROJS], workspaces=[ws[p] for p in PROJS])
+                    keys = [(p, M) for M in grp for p in PROJS]
+                    sfmp.gemm_grouped([models[cs[M]][p] for p, M in keys], [dx[k] for k in keys],
+                                      outs=[dy[k] for k in keys], workspaces=[wsm[k] for k in keys])
                 else:
-                    for p in PROJS:
-                        models[c][p].gemm(dx[(p, M)], out=dy[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
+                    for M in grp:
+                        for p in PROJS:
+                            models[cs[M]][p].gemm(dx[(p, M)], out=dy[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
             else:
-                for p in PROJS:
-                    models[c][p].gemm(dx[(p, M)], out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
-                    dist.all_gather_into_tensor(gath[(p, M)], ys[(p, M)])
-                    models[c][p].unpermute_gathered(gath[(p, M)], M, out=dy[(p, M)])
+                for M in grp:
+                    for p in PROJS:
+                        models[cs[M]][p].gemm(dx[(p, M)], out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
+                        dist.all_gather_into_tensor(gath[(p, M)], ys[(p, M)])
+                        models[cs[M]][p].unpermute_gathered(gath[(p, M)], M, out=dy[(p, M)])
             done = torch.cuda.Event()
             done.record(cur)
             with torch.cuda.stream(d2h_s):
                 d2h_s.wait_event(done)
-                a, b = gy[M]
-                hyb[a:b].copy_(dyb[a:b], non_blocking=True)
+                for M in grp:
+                    a, b = gy[M]
+                    hyb[a:b].copy_(dyb[a:b], non_blocking=True)
         cur.wait_stream(d2h_s)
         cur.wait_stream(h2d_s)
 
@@ -643,7 +655,7 @@ def main():
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "api": ("pinned host x -> H2D per M group on a copy stream, sfmp_gemm_grouped per M, "
                        "D2H per group on a second copy stream (copies overlap compute); CUDA graph "
-                       "per step, host synchronises on y every step"), "group_order": E2E_MS},
+                       "per step, host synchronises on y every step"), "groups": E2E_GROUPS},
         "gpu_launches": args.steps * launches_per_step,
         "clocks": clk,
     }
