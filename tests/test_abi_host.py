@@ -73,3 +73,19 @@ def test_shard_plan_snake_partition():
     assert sorted(gmap.reshape(-1).tolist()) == list(range(1024))  # a bijection onto rows
     with pytest.raises(sfmp.ShapeError):
         sfmp.shard_plan(data, 4)  # 2 block rows cannot split 4 ways
+
+
+def test_grouped_argument_checks():
+    """sfmp_gemm_grouped(_v) validate before touching the device: an empty group is
+    a no-op, missing arrays are argument errors, negative token counts shape errors."""
+    import ctypes as C
+    L = sfmp.lib()
+    assert L.sfmp_gemm_grouped_v(None, None, 2, None, None, None, None, 0, None) == 0
+    assert L.sfmp_gemm_grouped(None, None, 2, C.c_int64(0), None, None, None, 0, None) == 0
+    assert L.sfmp_gemm_grouped_v(None, None, 2, None, None, None, None, 1, None) != 0
+    assert b"null" in L.sfmp_last_error()
+    one = (C.c_void_p * 1)(C.c_void_p(1))
+    ms = (C.c_int64 * 1)(-3)
+    st = L.sfmp_gemm_grouped_v(one, one, 2, ms, one, one, None, 1, None)
+    assert st != 0 and b"negative" in L.sfmp_last_error()
+    assert L.sfmp_gemm_grouped(one, one, 2, C.c_int64(-1), one, one, None, 1, None) != 0
