@@ -681,6 +681,15 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
         if (Ms[k] < 1 || Ms[k] > 16 || !ms[k]->gemv_ok || !workspaces[k]) return false;
         return !workspace_bytes || workspace_bytes[k] >= sfmpk::gemv_workspace_bytes(*ms[k], 16);
     };
+    // A later decode launch of this call may overlap the previous one when its
+    // workspaces are not used by any earlier launch of the call (the problems
+    // themselves are independent by contract).
+    static const bool overlap_on = [] {
+        const char* e = getenv("SFMP_GROUP_OVERLAP");
+        return !e || atoi(e) != 0;
+    }();
+    std::vector<const void*> used_ws;
+    bool prev_decode = false;
     int i = 0;
     while (i < count) {
         int j = i + 1;
@@ -708,13 +717,20 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
                 wss[k - i] = static_cast<uint8_t*>(workspaces[k]);
                 mi[k - i] = static_cast<int>(Ms[k]);
             }
+            bool disjoint = true;
+            for (int k = i; k < j; ++k)
+                for (const void* w : used_ws) disjoint = disjoint && w != workspaces[k];
+            const bool overlap = overlap_on && prev_decode && disjoint;
             cudaError_t e = sfmpk::launch_gemv_group(ms.data() + i, xs + i, ys + i, wss.data(), mi.data(), j - i, dtype,
-                                                     static_cast<cudaStream_t>(stream));
+                                                     static_cast<cudaStream_t>(stream), overlap);
             if (e != cudaSuccess) return cuda_fail(e, "grouped GEMV launch");
+            for (int k = i; k < j; ++k) used_ws.push_back(workspaces[k]);
+            prev_decode = true;
         } else {
             sfmp_status s = sfmp_gemm(models[i], xs[i], dtype, Ms[i], ys[i], workspaces[i],
                                       workspace_bytes ? workspace_bytes[i] : 0, stream);
             if (s) return s;
+            prev_decode = false;  // the next decode launch follows a non-grouped kernel
         }
         i = j;
     }

@@ -109,6 +109,7 @@ struct XParams {
     int nlin, M, n_b;
     uint32_t rec_bytes;
     int dbg;
+    int wait_prev;  // launched as a programmatic dependent of the previous GEMV
 };
 
 // Activation record of one block column (n_b columns), for M tokens:
@@ -294,6 +295,11 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
                 xg[u] = xg[bias_slot(u, 0)] = xg[bias_slot(u, 0) + 2] = xg[bias_slot(u, 1)] = xg[bias_slot(u, 1) + 2] = 0.f;
     }
     if (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
+    // When launched to overlap the previous GEMV of the same grouped call, do
+    // not complete before it: this grid's completion (which the next GEMV waits
+    // for) then implies the previous launch's, keeping stream order for any
+    // later work.  A no-op for a normal launch.
+    if (xp.wait_prev) pdl_wait();
 }
 
 // Fallback for x rows above kXprepRowLimit bytes.
@@ -491,6 +497,9 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int dbg = p.debug_mode;
+    // a programmatic dependent (only ever the next launch of the same grouped
+    // call, whose problems are independent of ours) may start now
+    pdl_launch_dependents();
     if (threadIdx.x == 0) DBG_STAMP(0);
     if (threadIdx.x == 0 && dbg == 5 && blockIdx.x < kDbgCtas - 1) {
         unsigned smid;
@@ -787,7 +796,7 @@ cudaError_t launch_nc(cudaLaunchConfig_t& cfg, const Params& p, int lo) {
 
 template <sfmp_dtype DT>
 cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems, int max_cols, int grid, size_t smem, int lo,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool overlap_prev) {
     const size_t elem = DT == SFMP_F32 ? 4 : 2;
     // K4: activation records (normal launch: it overwrites the workspace the
     // previous call may still read, and x may be that call's output, so it
@@ -818,7 +827,24 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
                                  cudaSharedmemCarveoutMaxShared);
             configured_rows[dev] = 1;
         }
-        xprep_rows_kernel<DT><<<dim3(xitems, p.M), 256, row_smem, st>>>(xp);
+        // overlap_prev: a later launch of one grouped call (independent problems,
+        // workspaces disjoint from the earlier launches'): the pre-pass may start
+        // while the previous GEMV still runs (it never waits on it), and this
+        // call's GEMV then fills the previous one's tail.
+        cudaLaunchAttribute a[1];
+        a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        a[0].val.programmaticStreamSerializationAllowed = overlap_prev ? 1 : 0;
+        XParams xq = xp;
+        xq.wait_prev = overlap_prev ? 1 : 0;
+        cudaLaunchConfig_t c{};
+        c.gridDim = dim3(xitems, p.M);
+        c.blockDim = dim3(256);
+        c.dynamicSmemBytes = row_smem;
+        c.stream = st;
+        c.attrs = a;
+        c.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&c, xprep_rows_kernel<DT>, xq);
+        if (e != cudaSuccess) return e;
     } else {
         const int per_cta = 8 / (p.n_b / 128);  // items per pre-pass CTA
         xprep_kernel<DT><<<(xwarps + per_cta - 1) / per_cta, 256, 0, st>>>(xp);
@@ -870,7 +896,7 @@ bool gemv_groupable(const DevModel& a, const DevModel& b) {
 }
 
 cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, float* const* ys, uint8_t* const* wss,
-                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st) {
+                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st, bool overlap_prev) {
     if (n < 1 || n > kMaxLin) return cudaErrorInvalidValue;
     const DevModel& m0 = *ms[0];
     int M = 0;
@@ -953,9 +979,9 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     p.Q = Q;
     const int grid = static_cast<int>((unit0 + Q - 1) / Q);
     switch (dt) {
-        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st);
-        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st);
-        default: return launch_t<SFMP_BF16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st);
+        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st, overlap_prev);
+        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st, overlap_prev);
+        default: return launch_t<SFMP_BF16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st, overlap_prev);
     }
 }
 
@@ -966,7 +992,7 @@ cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, 
     float* ys[1] = {y};
     uint8_t* wss[1] = {reinterpret_cast<uint8_t*>(ws)};
     const int Ms[1] = {M};
-    return launch_gemv_group(ms, xs, ys, wss, Ms, 1, dt, st);
+    return launch_gemv_group(ms, xs, ys, wss, Ms, 1, dt, st, false);
 }
 
 }  // namespace sfmpk

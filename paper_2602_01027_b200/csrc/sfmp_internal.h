@@ -85,7 +85,7 @@ size_t gemv_workspace_bytes(const DevModel& m, int M);
 // Several independent linears in one xprep + one GEMV launch (same n_b, floor bits, device).
 bool gemv_groupable(const DevModel& a, const DevModel& b);
 cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, float* const* ys, uint8_t* const* wss,
-                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st);
+                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st, bool overlap_prev);
 int gemv_ctas_per_sm(int NT);
 
 cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
