@@ -172,7 +172,9 @@ sfmp_status sfmp_gemm_grouped(const sfmp_dev_model* const* models, const void* c
 /* Same with a token count per problem (Ms[i] rows of xs[i] / ys[i]), e.g. the
  * experts of a mixture-of-experts layer.  Consecutive decode problems (M <= 16)
  * that are groupable, fall in the same class (M <= 8 or 9..16) and use distinct
- * workspaces share one launch (up to 40 per launch). */
+ * workspaces share one launch (up to 40 per launch).  The problems of one call
+ * must be independent (no ys[i] aliasing an xs[j]): a later launch of the call
+ * may start while an earlier one finishes. */
 sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
                                 const int64_t* Ms, float* const* ys, void* const* workspaces,
                                 const size_t* workspace_bytes, int count, void* stream);
