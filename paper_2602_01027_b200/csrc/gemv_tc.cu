@@ -99,7 +99,7 @@ struct XLin {
     const uint32_t* col_perm;
     uint8_t* xrec;
     int BC, cols, warp0;
-    int item0;  // first pre-pass CTA column (groups of 8 block columns) of this linear
+    int item0;  // first pre-pass CTA of this linear (one per token x 8 block columns)
     int lo;     // floor bit-width: records carry the magic biases of lo and lo+1 bit units
     int M;      // tokens of this linear
     uint32_t rec_bytes;
@@ -221,19 +221,20 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     pdl_launch_dependents();  // let the GEMV start streaming weights right away
     extern __shared__ __align__(16) uint8_t xsm[];
     const int dbg = xp.dbg;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && dbg == 5) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && dbg == 5) {
         // previous launch's GEMV end (complete: stream order), then this start
         g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 104] = g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102];
         DBG_KSTAMP(100);
     }
     const int n_b = xp.n_b, CH = n_b >> 7;
-    const int t = blockIdx.y;
-    int it = blockIdx.x, li = 0;
+    int it = blockIdx.x, li = 0;  // compact grid: (linear, token, 8 block columns)
     while (li + 1 < xp.nlin && it >= xp.lin[li + 1].item0) ++li;
     const XLin& XL = xp.lin[li];
     const int M = XL.M;
-    if (t >= M) return;  // grid.y = the launch's largest M
     it -= XL.item0;
+    const int nit = (XL.BC + 7) / 8;
+    const int t = it / nit;
+    it -= t * nit;
     const int bc0 = it * 8, nbc = min(8, XL.BC - bc0), cols = XL.cols;
     uint32_t* cp = reinterpret_cast<uint32_t*>(xsm);  // [nbc][n_b] column indices
     T* xr = reinterpret_cast<T*>(xsm + 8 * n_b * 4);  // x[t][0..cols)
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
             for (int u = M; u < 8 * G.nt_count(); ++u)
                 xg[u] = xg[bias_slot(u, 0)] = xg[bias_slot(u, 0) + 2] = xg[bias_slot(u, 1)] = xg[bias_slot(u, 1) + 2] = 0.f;
     }
-    if (blockIdx.x == gridDim.x - 1 && blockIdx.y == gridDim.y - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
     // When launched to overlap the previous GEMV of the same grouped call, do
     // not complete before it: this grid's completion (which the next GEMV waits
     // for) then implies the previous launch's, keeping stream order for any
@@ -837,7 +838,7 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
         XParams xq = xp;
         xq.wait_prev = overlap_prev ? 1 : 0;
         cudaLaunchConfig_t c{};
-        c.gridDim = dim3(xitems, p.M);
+        c.gridDim = dim3(xitems);
         c.blockDim = dim3(256);
         c.dynamicSmemBytes = row_smem;
         c.stream = st;
@@ -964,7 +965,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         X.M = Ms[i];
         X.rec_bytes = L.rec_bytes;
         xwarps += BC * NT;
-        xitems += (BC + 7) / 8;
+        xitems += (BC + 7) / 8 * Ms[i];  // pre-pass CTAs: (8 block columns) x tokens
         max_cols = std::max(max_cols, X.cols);
     }
     p.stage_w = static_cast<uint32_t>((4 * kTR + ceil_bits * kTR * (m0.n_b / 8) + 127) / 128 * 128);
