@@ -25,7 +25,8 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsfmp_b200.so")
+# SFMP_LIB: load an experiment build instead (tools/ only; the default is the product)
+LIB_PATH = os.environ.get("SFMP_LIB") or os.path.join(HERE, "libsfmp_b200.so")
 
 # status codes (include/sfmp_cuda.h)
 OK, E_SHAPE, E_CONFIG, E_MAGIC, E_VERSION, E_TRUNC, E_INVARIANT, E_IO, E_CUDA, E_NCCL, E_ARG, \

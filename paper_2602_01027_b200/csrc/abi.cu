@@ -209,7 +209,7 @@ void free_model(DevModel* d) {
 // split is chosen per launch (gemv_tc.cu).
 sfmp_status build_gemv_schedule(DevModel& d) {
     d.gemv_ok = d.TR == 128 && (d.n_b == 128 || d.n_b == 256) && d.cols < (1ull << 31) &&
-                d.rows < (1ull << 31) && d.payload_bytes < (1ull << 48);
+                d.rows < (1ull << 31) && d.payload_bytes < (1ull << 48) && sfmpk::gemv_feasible(d);
     return SFMP_OK;
 }
 
@@ -613,6 +613,8 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
     if (dtype != SFMP_F32 && dtype != SFMP_F16 && dtype != SFMP_BF16)
         return fail(SFMP_ERR_INVALID_ARGUMENT, "bad dtype");
     const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    if (workspace && (reinterpret_cast<uintptr_t>(workspace) & 127))
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "workspace must be 128-byte aligned");
     DeviceGuard guard(d.device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // the tensor-core pre-pass reads x rows with 16-byte vector loads
@@ -677,6 +679,9 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
     }
     // Runs of groupable decode problems go out as one launch; anything else
     // (prefill M, odd geometry) falls to the per-model entry point.
+    for (int k = 0; k < count; ++k)
+        if (workspaces[k] && (reinterpret_cast<uintptr_t>(workspaces[k]) & 127))
+            return fail(SFMP_ERR_INVALID_ARGUMENT, "workspaces must be 128-byte aligned");
     auto decode_ok = [&](int k) {
         if (Ms[k] < 1 || Ms[k] > 16 || !ms[k]->gemv_ok || !workspaces[k]) return false;
         return !workspace_bytes || workspace_bytes[k] >= sfmpk::gemv_workspace_bytes(*ms[k], 16);
@@ -684,10 +689,6 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
     // A later decode launch of this call may overlap the previous one when its
     // workspaces are not used by any earlier launch of the call (the problems
     // themselves are independent by contract).
-    static const bool overlap_on = [] {
-        const char* e = getenv("SFMP_GROUP_OVERLAP");
-        return !e || atoi(e) != 0;
-    }();
     std::vector<const void*> used_ws;
     bool prev_decode = false;
     int i = 0;
@@ -720,15 +721,16 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
             bool disjoint = true;
             for (int k = i; k < j; ++k)
                 for (const void* w : used_ws) disjoint = disjoint && w != workspaces[k];
-            const bool overlap = overlap_on && prev_decode && disjoint;
+            const bool overlap = prev_decode && disjoint;
             cudaError_t e = sfmpk::launch_gemv_group(ms.data() + i, xs + i, ys + i, wss.data(), mi.data(), j - i, dtype,
                                                      static_cast<cudaStream_t>(stream), overlap);
             if (e != cudaSuccess) return cuda_fail(e, "grouped GEMV launch");
             for (int k = i; k < j; ++k) used_ws.push_back(workspaces[k]);
             prev_decode = true;
         } else {
+            // workspace_bytes == NULL: the caller vouches for the sizes
             sfmp_status s = sfmp_gemm(models[i], xs[i], dtype, Ms[i], ys[i], workspaces[i],
-                                      workspace_bytes ? workspace_bytes[i] : 0, stream);
+                                      workspace_bytes ? workspace_bytes[i] : (workspaces[i] ? SIZE_MAX : 0), stream);
             if (s) return s;
             prev_decode = false;  // the next decode launch follows a non-grouped kernel
         }

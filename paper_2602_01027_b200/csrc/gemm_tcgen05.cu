@@ -15,32 +15,37 @@
 //    whose block is at ceil bits (compact, located by a 128-bit row mask).
 //    Because a tile's rows are consecutive output rows, the epilogue writes
 //    y with coalesced stores -- the row un-permutation costs nothing.
-//  * xprep_gemm_kernel gathers x[t][col_perm[.]], converts to f16 and lays
-//    every (token tile, 128-column chunk) out as the exact 128-byte-swizzled
-//    K-major shared-memory image of the MMA B operand, so the GEMM fetches
-//    it with one 1-D bulk copy (no tensor map).  The K order inside each
-//    32-column word follows the register order the unpacker produces.
-//  * Persistent warp-specialised kernel, one CTA per SM, tile = 256 output
-//    rows (two M=128 MMAs) x N<=128 tokens:
-//      warp 0      producer: cp.async.bulk of weight units and X tiles
-//      warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//      warps 2-5   epilogue: tcgen05.ld accumulators -> coalesced y stores
-//      warps 6-13  dequant: bit-planes -> codes -> f16(s*c+z) (one HFMA2 per
-//                  weight pair, fp16 s/z exactly as stored) written straight
-//                  into TMEM as the MMA A operand (tcgen05.st), so weights
-//                  never take a shared-memory round trip.
-//    TMEM (512 columns): 2 accumulators x 128 columns, 2 A buffers x 2 row
-//    halves x 64 columns (128 f16 of K per row).
+//  * The pre-pass (xprep_gemm_*) gathers x[t][col_perm[.]], scales each
+//    token by a power of two 2^-e_t (max|x_t| -> [2^14, 2^15): no finite
+//    input overflows f16), converts to f16 and lays every (token tile,
+//    128-column chunk) out as the exact 128-byte-swizzled K-major
+//    shared-memory image of the MMA B operand, so the GEMM fetches it with one
+//    1-D bulk copy (no tensor map).  The epilogue multiplies back by 2^e_t.
+//  * Persistent warp-specialised kernel, one CTA per SM, tile = 128 output
+//    rows (MMA M) x N <= 256 tokens (MMA N):
+//      warp 0       producers: lane 0 weight units, lane 1 X atoms (cp.async.bulk)
+//      warp 1       TMEM allocator + tcgen05.mma issuer (one elected lane)
+//      warps 2-17   epilogue: tcgen05.ld accumulators -> coalesced y stores
+//      warps 18-25  dequant: bit-planes -> codes -> f16(s*c+z) (one exact
+//                   HSUB2 + one HFMA2 per weight pair, fp16 s/z as stored)
+//                   written straight into TMEM as the MMA A operand
+//                   (tcgen05.st), so weights never take a shared-memory trip.
+//    TMEM (512 columns): accumulator 256 columns, 4 A buffers x 64 columns.
+//  * Schedule: work items (tile, K split), round-robin over the CTAs.  The
+//    number of K splits depends on the UNSHARDED matrix shape and M only
+//    (k_splits), so results are bit-identical on any device and for any
+//    shard count; split partials are summed in split order (gemm_reduce_kernel).
 //  * Precision: weights are rounded once to f16 (SURVEY §7 hard part 1:
-//    f16 dequant stays ~5x inside the 1e-3 bar, bf16 would not); the
-//    activations are converted to f16 (exact for bf16 values in f16 range);
-//    accumulation is f32 in TMEM.
+//    f16 dequant stays ~5x inside the 1e-3 bar, bf16 would not); the scaled
+//    activations are rounded to f16 (exact for bf16 input); accumulation is
+//    f32 in TMEM.  The f16 weight rounding (~2^-12 relative per weight)
+//    dominates the error, so f32 input gets no hi/lo split here (unlike K1).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 
 #include "ptx.cuh"
@@ -54,9 +59,7 @@ namespace {
 
 constexpr int kUnitHdr = 528;             // scales[128] | zeros[128] | highmask[4]
 constexpr int kPlaneBytes = 128 * 16;     // one plane of a unit
-// Tile = 128 output rows (MMA M) x N <= 256 tokens (MMA N): a single
-// M=128,N=256,K=16 tcgen05.mma costs ~138 cycles vs ~118 for N<=128
-// (tools/mma_bench.cu, measured), so wide N is what reaches the tensor peak.
+// Tile = 128 output rows (MMA M) x N <= 256 tokens (MMA N).
 constexpr int kDeqWarps = 8;              // dequant warps: 4 TMEM lane quarters x kKS K-splits
 constexpr int kKS = kDeqWarps / 4;        // K splits of a 128-column unit among dequant warps
 constexpr int kWords = 4 / kKS;           // 32-weight words per dequant thread per unit
@@ -73,19 +76,17 @@ struct GemmParams {
     const uint8_t* wl;       // row-tile layout payload
     const uint64_t* woff;    // [RT2*KC + 1] unit byte offsets
     const uint8_t* xs;       // [TT][KC][2][N][128 B] swizzled f16 X
+    const float* ysc;        // [TT*N] per-token output scale 2^e_t (pre-pass)
     float* y;
     int M, N, TT, KC, RT;    // tokens, tokens/tile, token tiles, 128-col chunks, row tiles
     uint64_t out_rows;
     int floor_bits, has_extra;
     int SX, SW;              // X / W ring stages
-    int64_t work, Q;         // (tile, kc) steps in all, per CTA (stream-K)
-    int64_t w0;              // steps [0, w0): whole tiles round-robin; [w0, work): stream-K ranges of Q
-    int rr;                  // 1: whole tiles only (w0 == work)
-    float* part;             // [grid][2][N][128] f32 stream-K partial tiles
+    int ks;                  // K splits per tile (a function of the matrix shape and M alone)
+    int items;               // tiles * ks
+    float* part;             // [items][N][128] f32 split-K partial tiles (ks > 1)
     uint32_t stage_w;        // W stage bytes (one unit)
-    uint32_t bar_bytes;      // barrier + offset area (multiple of 1024)
     uint32_t idesc;
-    int dbg;  // SFMP_GEMM_DEBUG bits: 1 skip dequant math, 2 skip MMAs, 4 skip y stores, 8 xprep only, 16 no xprep
 };
 
 // x[t][col_perm[...]] -> f16, in the K order of the unpacked A operand:
@@ -98,12 +99,30 @@ __host__ __device__ __forceinline__ int slot_col(int s) {
 }
 
 template <sfmp_dtype DT>
-__device__ __forceinline__ float ldx(const void* x, size_t i) {
-    if constexpr (DT == SFMP_F32) return __ldg(static_cast<const float*>(x) + i);
-    else if constexpr (DT == SFMP_F16)
-        return __half2float(__ldg(static_cast<const __half*>(x) + i));
-    else
-        return __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(x) + i));
+__device__ __forceinline__ float x_as_float(std::conditional_t<DT == SFMP_F32, float, uint16_t> v) {
+    if constexpr (DT == SFMP_F32) return v;
+    else if constexpr (DT == SFMP_F16) return __half2float(__ushort_as_half(v));
+    else return __bfloat162float(__ushort_as_bfloat16(v));
+}
+
+// Per-token power-of-two scale (as the decode pre-pass, gemv_tc.cu): e such
+// that max|x_t| * 2^-e lies in [2^14, 2^15), so no finite input overflows
+// f16; 0 for a zero or non-finite row.  f16 input is not scaled.
+__device__ __forceinline__ int token_exp(float amax) {
+    if (!(amax > 0.f) || !isfinite(amax)) return 0;
+    const int e = ilogbf(amax) - 14;
+    return e < -110 ? -110 : (e > 110 ? 110 : e);
+}
+__device__ __forceinline__ float block_max(float m, float* red) {
+    const int NW = static_cast<int>(blockDim.x >> 5);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __syncthreads();  // red[] free (previous use finished)
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = 0.f;
+    for (int w = 0; w < NW; ++w) m = fmaxf(m, red[w]);
+    return m;
 }
 
 // Persistent pre-pass (cols < 65536): each CTA keeps the slot table as u16 in
@@ -114,10 +133,11 @@ __device__ __forceinline__ float ldx(const void* x, size_t i) {
 template <sfmp_dtype DT>
 __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __restrict__ x,
                                                               const uint32_t* __restrict__ xslot,
-                                                              uint8_t* __restrict__ xs, int M, int N, int KC,
-                                                              int cols, int Mpad) {
+                                                              uint8_t* __restrict__ xs, float* __restrict__ ysc, int M,
+                                                              int N, int KC, int cols, int Mpad) {
     using T = std::conditional_t<DT == SFMP_F32, float, uint16_t>;
     extern __shared__ __align__(16) uint8_t xsm[];
+    __shared__ float red[16];
     pdl_launch_dependents();
     uint64_t* bar = reinterpret_cast<uint64_t*>(xsm);            // [2] row buffer full
     uint16_t* idx = reinterpret_cast<uint16_t*>(xsm + 16);        // [cols] slot table
@@ -152,6 +172,17 @@ __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __rest
         uint8_t* dst = xs + static_cast<size_t>(tt) * KC * 2 * N * 128 + r * 128;
         const T* xr = reinterpret_cast<const T*>(rowbuf + buf * static_cast<size_t>(row_bytes));
         if (t < M) mbar_wait(&bar[buf], static_cast<uint32_t>(k >> 1) & 1u);
+        float sc = 1.f;
+        if constexpr (DT != SFMP_F16) {
+            float m = 0.f;
+            if (t < M)
+                for (int i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(x_as_float<DT>(xr[i])));
+            const int e = token_exp(block_max(m, red));
+            sc = ldexpf(1.f, -e);
+            if (threadIdx.x == 0) ysc[t] = t < M ? ldexpf(1.f, e) : 0.f;
+        } else {
+            if (threadIdx.x == 0) ysc[t] = t < M ? 1.f : 0.f;
+        }
         for (int c = threadIdx.x; c < KC * 16; c += blockDim.x) {
             const int kc = c >> 4, a = (c >> 3) & 1, j = c & 7;
             uint4 out = make_uint4(0u, 0u, 0u, 0u);
@@ -162,13 +193,10 @@ __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __rest
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const T lo = xr[iv[e] & 0xFFFFu], hi = xr[iv[e] >> 16];
-                    if constexpr (DT == SFMP_F32) {
-                        o[e] = h2_as_u32(__floats2half2_rn(lo, hi));
-                    } else if constexpr (DT == SFMP_BF16) {
-                        o[e] = h2_as_u32(__floats2half2_rn(__bfloat162float(__ushort_as_bfloat16(lo)),
-                                                          __bfloat162float(__ushort_as_bfloat16(hi))));
-                    } else {
+                    if constexpr (DT == SFMP_F16) {
                         o[e] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+                    } else {
+                        o[e] = h2_as_u32(__floats2half2_rn(x_as_float<DT>(lo) * sc, x_as_float<DT>(hi) * sc));
                     }
                 }
                 out = make_uint4(o[0], o[1], o[2], o[3]);
@@ -188,46 +216,41 @@ __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __rest
     }
 }
 
-// One CTA per token (grid-stride): the x row is staged in shared memory as
-// f16 with coalesced 16-byte loads, then every 16-byte chunk of the swizzled
-// B image is gathered from shared memory through the slot table xslot
-// (xslot[kc*128 + s] = col_perm[kc*128 + slot_col(s)], built at upload).
+// One CTA per token (grid-stride), for wide rows or misaligned x: the x row
+// is staged in shared memory as f16 (scaled), then every 16-byte chunk of the
+// swizzled B image is gathered from shared memory through the slot table
+// xslot (xslot[kc*128 + s] = col_perm[kc*128 + slot_col(s)], built at upload).
 // Tokens M..TT*N-1 of the last tile are written as zeros.
 template <sfmp_dtype DT>
 __global__ void __launch_bounds__(1024) xprep_gemm_kernel(const void* __restrict__ x, const uint32_t* __restrict__ xslot,
-                                                         uint8_t* __restrict__ xs, int M, int N, int KC, int cols,
-                                                         int Mpad) {
+                                                         uint8_t* __restrict__ xs, float* __restrict__ ysc, int M, int N,
+                                                         int KC, int cols, int Mpad) {
+    using T = std::conditional_t<DT == SFMP_F32, float, uint16_t>;
     extern __shared__ __align__(16) __half xrow[];
+    __shared__ float red[32];
     pdl_launch_dependents();
     for (int t = blockIdx.x; t < Mpad; t += gridDim.x) {
         const int tt = t / N, r = t - tt * N;
         uint8_t* dst = xs + static_cast<size_t>(tt) * KC * 2 * N * 128 + r * 128;
         if (t < M) {
-            if constexpr (DT == SFMP_F32) {
-                const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(x) + static_cast<size_t>(t) * cols);
-                for (int i = threadIdx.x; i < cols / 4; i += blockDim.x) {
-                    const float4 v = __ldg(src + i);
-                    uint2 h;
-                    h.x = h2_as_u32(__floats2half2_rn(v.x, v.y));
-                    h.y = h2_as_u32(__floats2half2_rn(v.z, v.w));
-                    reinterpret_cast<uint2*>(xrow)[i] = h;
-                }
-            } else {
-                const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(x) + static_cast<size_t>(t) * cols);
-                for (int i = threadIdx.x; i < cols / 8; i += blockDim.x) {
-                    uint4 v = __ldg(src + i);
-                    if constexpr (DT == SFMP_BF16) {
-                        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
-                            w[e] = h2_as_u32(__float22half2_rn(__bfloat1622float2(b)));
-                        }
-                    }
-                    reinterpret_cast<uint4*>(xrow)[i] = v;
-                }
+            const T* src = static_cast<const T*>(x) + static_cast<size_t>(t) * cols;
+            float sc = 1.f;
+            if constexpr (DT != SFMP_F16) {
+                float m = 0.f;
+                for (int i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(x_as_float<DT>(src[i])));
+                const int e = token_exp(block_max(m, red));
+                sc = ldexpf(1.f, -e);
+                if (threadIdx.x == 0) ysc[t] = ldexpf(1.f, e);
+            } else if (threadIdx.x == 0) {
+                ysc[t] = 1.f;
+            }
+            for (int i = threadIdx.x; i < cols; i += blockDim.x) {
+                if constexpr (DT == SFMP_F16) xrow[i] = __ushort_as_half(src[i]);
+                else xrow[i] = __float2half_rn(x_as_float<DT>(src[i]) * sc);
             }
             __syncthreads();
+        } else if (threadIdx.x == 0) {
+            ysc[t] = 0.f;
         }
         for (int c = threadIdx.x; c < KC * 16; c += blockDim.x) {
             const int kc = c >> 4, a = (c >> 3) & 1, j = c & 7;
@@ -247,82 +270,31 @@ __global__ void __launch_bounds__(1024) xprep_gemm_kernel(const void* __restrict
     }
 }
 
-// Debug timeline (SFMP_GEMM_DEBUG & 32): CTAs 0/1, [kind][unit] globaltimer:
-// 0 dequant wfull seen, 1 dequant math done, 2 aempty seen, 3 afull arrived,
-// 4 MMA afull seen, 5 MMA xfull seen, 6 MMA issued+committed, 7 epilogue accfull seen (per tile).
-__device__ unsigned long long g_gemm_tl[2 * 8 * 256];
-// kernel phases of CTAs < 512 (SFMP_GEMM_DEBUG & 32): entry, setup done, first
-// W issue, griddepcontrol.wait returned, first X issue, exit
-constexpr int kPhCtas = 512;
-__device__ unsigned long long g_gemm_ph[kPhCtas * 16];  // + role ends: 6 W, 7 X, 8 MMA, 9 epilogue, 10 dequant
-__device__ __forceinline__ unsigned long long gtimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
+// Work items of this CTA: items b, b+G, b+2G, ... ; item i = (tile i / ks,
+// K split i % ks), split j covering chunks [j*KC/ks, (j+1)*KC/ks).  Every role
+// walks the same sequence.
 struct GSeg {
-    int tile, kc0, kc1;
-    bool first;  // first segment of this CTA's stream-K range
+    int item, tile, kc0, kc1;
 };
-// Segments of this CTA: whole tiles b, b+G, ... of the round-robin part
-// [0, w0), then its stream-K range [w0 + b*Q, w0 + (b+1)*Q) cut at tile
-// boundaries (hybrid: the last, partial wave of tiles is spread over all CTAs
-// instead of leaving most SMs idle while a few finish whole tiles).
-struct SegIter {
-    int64_t w, wend;
-    bool sk, first;
-    __device__ __forceinline__ bool next(const GemmParams& p, GSeg& g) {
-        if (!sk) {
-            if (w < p.w0) {
-                g.tile = static_cast<int>(w / p.KC);
-                g.kc0 = 0;
-                g.kc1 = p.KC;
-                g.first = false;
-                w += static_cast<int64_t>(gridDim.x) * p.KC;
-                return true;
-            }
-            sk = true;
-            w = p.w0 + static_cast<int64_t>(blockIdx.x) * p.Q;
-            wend = min(p.work, w + p.Q);
-        }
-        if (w >= wend) return false;
-        g.tile = static_cast<int>(w / p.KC);
-        g.kc0 = static_cast<int>(w - static_cast<int64_t>(g.tile) * p.KC);
-        g.kc1 = static_cast<int>(min(static_cast<int64_t>(p.KC), g.kc0 + (wend - w)));
-        g.first = first;
-        w += g.kc1 - g.kc0;
-        first = false;
-        return true;
-    }
-};
-__device__ __forceinline__ SegIter seg_begin(const GemmParams& p) {
-    SegIter it;
-    it.w = static_cast<int64_t>(blockIdx.x) * p.KC;
-    it.wend = 0;
-    it.sk = false;
-    it.first = true;
-    return it;
+__device__ __forceinline__ bool seg_at(const GemmParams& p, int k, GSeg& g) {
+    const int item = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+    if (item >= p.items) return false;
+    g.item = item;
+    g.tile = item / p.ks;
+    const int j = item - g.tile * p.ks;
+    g.kc0 = j * p.KC / p.ks;
+    g.kc1 = (j + 1) * p.KC / p.ks;
+    return true;
 }
 
-// Stream-K fix-up: a tile shared by CTAs c0..c1 gets the sum of their partial
-// tiles in CTA order (deterministic).  CTA c0's part is in slot 1 when its
-// range began in an earlier tile, slot 0 otherwise; the others' parts are
-// their first segments (slot 0).  grid = (N/32, CTA boundaries); boundary b
-// (end of CTA b's range) reduces the tile it falls in if it is that tile's
-// first boundary.
+// Split-K fix-up: tile's partials summed in split order (deterministic), times
+// the per-token scale.  grid = (N/32, tiles); warp wi handles tokens
+// j0 + wi + 4k (k < 8); lane l rows 4l..4l+3 (float4).
 __global__ void __launch_bounds__(128) gemm_reduce_kernel(const GemmParams p) {
-    const int64_t b = blockIdx.y;
-    const int64_t w = p.w0 + (b + 1) * p.Q;  // end of CTA b's stream-K range
-    if (w >= p.work) return;
-    const int64_t tile = w / p.KC;
-    const int64_t ts = tile * p.KC;  // >= w0: w0 is a tile boundary
-    if (w == ts || b != (ts - p.w0) / p.Q) return;
-    const int c0 = static_cast<int>((ts - p.w0) / p.Q), c1 = static_cast<int>((ts + p.KC - 1 - p.w0) / p.Q);
-    const int s0 = (p.w0 + static_cast<int64_t>(c0) * p.Q < ts) ? 1 : 0;
-    const int rt = static_cast<int>(tile / p.TT), tt = static_cast<int>(tile - static_cast<int64_t>(rt) * p.TT);
+    pdl_wait();
+    const int tile = blockIdx.y;
+    const int rt = tile / p.TT, tt = tile - rt * p.TT;
     const int N = p.N;
-    // warp wi handles tokens j0 + wi + 4k (k < 8); lane l rows 4l..4l+3 (float4)
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j0 = blockIdx.x * 32 + wi;
     const size_t pstride = static_cast<size_t>(N) * 128;
@@ -330,12 +302,9 @@ __global__ void __launch_bounds__(128) gemm_reduce_kernel(const GemmParams p) {
     float4 acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    // partials come from the previous kernel: read-only path (a strong ld.cg
-    // here was issued one at a time, 32 serial HBM round trips)
-    for (int c = c0; c <= c1; ++c) {  // CTA order: deterministic
-        const float4* src = reinterpret_cast<const float4*>(
-                                p.part + (static_cast<size_t>(c) * 2 + (c == c0 ? s0 : 0)) * pstride +
-                                static_cast<size_t>(j0) * 128) + lane;
+    for (int c = 0; c < p.ks; ++c) {  // split order: deterministic
+        const float4* src =
+            reinterpret_cast<const float4*>(p.part + (static_cast<size_t>(tile) * p.ks + c) * pstride + static_cast<size_t>(j0) * 128) + lane;
         float4 v[8];
         if (full) {  // unconditional loads: all 8 in flight together
 #pragma unroll
@@ -361,11 +330,13 @@ __global__ void __launch_bounds__(128) gemm_reduce_kernel(const GemmParams p) {
     for (int k = 0; k < 8; ++k) {
         const int j = j0 + 4 * k, t = tt * N + j;
         if (j >= N || t >= p.M) continue;
+        const float sc = p.ysc[t];
+        const float4 a4 = make_float4(acc[k].x * sc, acc[k].y * sc, acc[k].z * sc, acc[k].w * sc);
         float* yp = p.y + static_cast<size_t>(t) * p.out_rows + grow;
         if (vec && grow + 4 <= p.out_rows) {
-            *reinterpret_cast<float4*>(yp) = acc[k];
+            *reinterpret_cast<float4*>(yp) = a4;
         } else {
-            const float a[4] = {acc[k].x, acc[k].y, acc[k].z, acc[k].w};
+            const float a[4] = {a4.x, a4.y, a4.z, a4.w};
             for (int e = 0; e < 4; ++e)
                 if (grow + e < p.out_rows) yp[e] = a[e];
         }
@@ -405,8 +376,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool ph = (p.dbg & 32) && blockIdx.x < kPhCtas;
-    if (ph && threadIdx.x == 0) g_gemm_ph[blockIdx.x * 16 + 0] = gtimer_ns();
     if (threadIdx.x == 0) {
         for (int s = 0; s < SX; ++s) {
             mbar_init(&xfull[s], 1);
@@ -433,28 +402,24 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
-    if (ph && threadIdx.x == 0) g_gemm_ph[blockIdx.x * 16 + 1] = gtimer_ns();
+    // the split-K fix-up (if any) may launch now; it waits for this grid
+    pdl_launch_dependents();
 
-    // Work: the sequence of (tile, kc) steps, tile = rt * TT + tt, kc inner,
-    // cut into ranges [b*Q, (b+1)*Q), one per CTA.  With enough tiles Q is a
-    // whole number of tiles (plain persistent tiles); when the tiles cannot
-    // fill the SMs, ranges split tiles along K (stream-K): a segment that
-    // covers a whole tile stores y, the others store a partial tile that
-    // gemm_reduce_kernel sums in CTA order (deterministic) afterwards.
+    // Work: items (tile, K split), tile = rt * TT + tt, round-robin over the
+    // CTAs.  A whole-tile item (ks == 1) stores y; a split item stores its
+    // partial tile, summed in split order by gemm_reduce_kernel.
     const int KC = p.KC;
 
     if (warp == 0) {
         // ---------------- producers ----------------
         // Lane 0 streams the weight units, lane 1 the X atoms, each gated only
-        // by its own ring: the weights no longer wait for X slots (which free
-        // only as MMAs complete), so dequantisation can run ahead.  Lane 0
-        // reads each segment's unit offsets straight from global memory, the
-        // loads for a segment issued together (one latency per segment).
+        // by its own ring: the weights never wait for X slots (which free only
+        // as MMAs complete), so dequantisation can run ahead.
         const uint64_t pol_w = policy_evict_first();
         if (lane == 0) {
             int ws = 0, wph = 0;
-            SegIter it = seg_begin(p);
-            for (GSeg sg; it.next(p, sg);) {
+            GSeg sg;
+            for (int k = 0; seg_at(p, k, sg); ++k) {
                 const int rt = sg.tile / p.TT;
                 const uint64_t* off0 = p.woff + static_cast<size_t>(rt) * KC + sg.kc0;
                 uint64_t a_next = __ldg(off0);
@@ -465,26 +430,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                     mbar_wait_sleep(&wempty[ws], wph ^ 1, 500);
                     mbar_arrive_expect_tx(&wfull[ws], n0);
                     bulk_g2s(wbuf + static_cast<size_t>(ws) * p.stage_w, p.wl + a0, n0, &wfull[ws], pol_w);
-                    if (ph && sg.first && kc == sg.kc0) g_gemm_ph[blockIdx.x * 16 + 2] = gtimer_ns();
                     if (++ws == SW) { ws = 0; wph ^= 1; }
                 }
             }
-            if (ph) g_gemm_ph[blockIdx.x * 16 + 6] = gtimer_ns();
         } else if (lane == 1) {
             int xs = 0, xph = 0;
             pdl_wait();  // X is written by the pre-pass (programmatic dependent launch)
-            if (ph) g_gemm_ph[blockIdx.x * 16 + 3] = gtimer_ns();
-            SegIter it = seg_begin(p);
-            for (GSeg sg; it.next(p, sg);) {
+            GSeg sg;
+            for (int k = 0; seg_at(p, k, sg); ++k) {
                 const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
                 for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                     for (int h = 0; h < 2; ++h) {
                         mbar_wait_sleep(&xempty[xs], xph ^ 1, 200);
-                        if (p.dbg & 256) {  // probe: no X traffic
-                            mbar_arrive(&xfull[xs]);
-                            if (++xs == SX) { xs = 0; xph ^= 1; }
-                            continue;
-                        }
                         mbar_arrive_expect_tx(&xfull[xs], xstage);
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -492,60 +449,46 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                             "l"(p.xs + ((static_cast<size_t>(tt) * KC + kc) * 2 + h) * xstage), "r"(xstage),
                             "r"(smem_u32(&xfull[xs]))
                             : "memory");
-                        if (ph && sg.first && kc == sg.kc0 && h == 0) g_gemm_ph[blockIdx.x * 16 + 4] = gtimer_ns();
                         if (++xs == SX) { xs = 0; xph ^= 1; }
                     }
                 }
             }
-            if (ph) g_gemm_ph[blockIdx.x * 16 + 7] = gtimer_ns();
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         // The whole warp walks the loop (warp-uniform operands stay in uniform
         // registers, no per-MMA waterfall); one elected lane issues tcgen05.
-        {
-            int xs = 0, xph = 0, ab = 0, aph = 0, accph = 0;
-            unsigned long long* tl =
-                ((p.dbg & 32) && blockIdx.x < 2 && lane == 0) ? g_gemm_tl + blockIdx.x * 8 * 256 : nullptr;
-            int tcount = 0;
-            const uint32_t idesc = p.idesc;
-            const bool do_mma = !(p.dbg & 2);
-            SegIter it = seg_begin(p);
-            for (GSeg sg; it.next(p, sg);) {
-                mbar_wait(accempty, accph ^ 1);
+        int xs = 0, xph = 0, ab = 0, aph = 0, accph = 0;
+        const uint32_t idesc = p.idesc;
+        GSeg sg;
+        for (int k = 0; seg_at(p, k, sg); ++k) {
+            mbar_wait(accempty, accph ^ 1);
+            tc_fence_after();
+            for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
+                mbar_wait(&afull[ab], aph);
                 tc_fence_after();
-                for (int kc = sg.kc0; kc < sg.kc1; ++kc, ++tcount) {
-                    mbar_wait(&afull[ab], aph);
-                    if (tl) tl[4 * 256 + (tcount & 255)] = gtimer_ns();
+                const uint32_t a0 = tbase + kACol + ab * 64;
+                for (int h = 0; h < 2; ++h) {
+                    mbar_wait(&xfull[xs], xph);
                     tc_fence_after();
-                    const uint32_t a0 = tbase + kACol + ab * 64;
-                    for (int h = 0; h < 2; ++h) {
-                        mbar_wait(&xfull[xs], xph);
-                        if (tl && h == 0) tl[5 * 256 + (tcount & 255)] = gtimer_ns();
-                        tc_fence_after();
-                        const uint64_t bdesc = tc_desc_sw128(smem_u32(xbuf + static_cast<size_t>(xs) * xstage));
-                        if (elect_one()) {
-                            if (do_mma) {
+                    const uint64_t bdesc = tc_desc_sw128(smem_u32(xbuf + static_cast<size_t>(xs) * xstage));
+                    if (elect_one()) {
 #pragma unroll
-                                for (int kk = 0; kk < 4; ++kk)
-                                    tc_mma_ts(tbase + kAccCol, a0 + (h * 4 + kk) * 8, bdesc + 2 * kk, idesc,
-                                              ((kc - sg.kc0) | h | kk) != 0);
-                            }
-                            tc_commit(&xempty[xs]);
-                        }
-                        __syncwarp();
-                        if (++xs == SX) { xs = 0; xph ^= 1; }
+                        for (int kk = 0; kk < 4; ++kk)
+                            tc_mma_ts(tbase + kAccCol, a0 + (h * 4 + kk) * 8, bdesc + 2 * kk, idesc,
+                                      ((kc - sg.kc0) | h | kk) != 0);
+                        tc_commit(&xempty[xs]);
                     }
-                    if (elect_one()) tc_commit(&aempty[ab]);
                     __syncwarp();
-                    if (tl) tl[6 * 256 + (tcount & 255)] = gtimer_ns();
-                    if (++ab == kNA) { ab = 0; aph ^= 1; }
+                    if (++xs == SX) { xs = 0; xph ^= 1; }
                 }
-                if (elect_one()) tc_commit(accfull);
+                if (elect_one()) tc_commit(&aempty[ab]);
                 __syncwarp();
-                accph ^= 1;
+                if (++ab == kNA) { ab = 0; aph ^= 1; }
             }
-            if (ph && lane == 0) g_gemm_ph[blockIdx.x * 16 + 8] = gtimer_ns();
+            if (elect_one()) tc_commit(accfull);
+            __syncwarp();
+            accph ^= 1;
         }
     } else if (warp < 2 + kEpiWarps) {
         // ---------------- epilogue: TMEM -> registers -> coalesced y rows ----------------
@@ -555,22 +498,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         // tile's MMAs.
         constexpr int kCols = 256 / (kEpiWarps / 4);
         const int ew = warp - 2, q = warp & 3, cg = ew >> 2;
-        int accph = 0, ecount = 0;
-        SegIter it = seg_begin(p);
-        for (GSeg sg; it.next(p, sg);) {
-            const int slot = sg.first ? 0 : 1;  // partial slot: first / last segment of the range
+        int accph = 0;
+        GSeg sg;
+        for (int k = 0; seg_at(p, k, sg); ++k) {
             const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
             mbar_wait_sleep(accfull, accph, 200);  // a whole tile of MMAs away: sleep between polls
-            if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
-                g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + (ecount++ & 127)] = gtimer_ns();
             accph ^= 1;
             tc_fence_after();
             const int c_begin = cg * kCols;
             const int t0 = tt * N + c_begin;
             const uint64_t row = static_cast<uint64_t>(rt) * 128 + q * 32 + lane;
-            int lim = (p.dbg & 4) ? 0 : min(kCols, min(N - c_begin, p.M - t0));
-            // whole-tile segment -> y[t][row]; else partial [t][128 rows] of this CTA's slot
-            const bool full = sg.kc0 == 0 && sg.kc1 == KC;
+            int lim = min(kCols, min(N - c_begin, p.M - t0));
+            // whole-tile item -> y[t][row] * 2^e_t; else the item's partial [t][128 rows]
+            const bool full = p.ks == 1;
             float* yp;
             size_t ld;
             if (full) {
@@ -578,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 ld = p.out_rows;
                 if (row >= p.out_rows) lim = 0;
             } else {
-                yp = p.part + (static_cast<size_t>(blockIdx.x) * 2 + slot) * (static_cast<size_t>(N) * 128) +
+                yp = p.part + static_cast<size_t>(sg.item) * (static_cast<size_t>(N) * 128) +
                      static_cast<size_t>(c_begin) * 128 + q * 32 + lane;
                 ld = 128;
             }
@@ -597,29 +537,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(accempty);
-                    if ((p.dbg & 32) && blockIdx.x < 2 && ew == 0 && lane == 0)
-                        g_gemm_tl[blockIdx.x * 8 * 256 + 7 * 256 + 128 + ((ecount - 1) & 127)] = gtimer_ns();
                 }
+                float sv = 1.f;
+                if (full && 32 * c + lane < lim) sv = __ldg(p.ysc + t0 + 32 * c + lane);
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (32 * c + j < lim) yp[static_cast<size_t>(32 * c + j) * ld] = __uint_as_float(v[j]);
+                for (int j = 0; j < 32; ++j) {
+                    const float sj = full ? __shfl_sync(0xffffffffu, sv, j) : 1.f;
+                    if (32 * c + j < lim) yp[static_cast<size_t>(32 * c + j) * ld] = __uint_as_float(v[j]) * sj;
+                }
             }
         }
-        if (ph && ew == 0 && lane == 0) g_gemm_ph[blockIdx.x * 16 + 9] = gtimer_ns();
     } else {
         // ---------------- dequant: bit-planes -> f16 A operand in TMEM ----------------
         const int dw = warp - 2 - kEpiWarps, q = warp & 3, kh = dw >> 2;
         const int r = q * 32 + lane;  // row within the unit = TMEM lane
         const uint32_t woff = static_cast<uint32_t>(kh * kWords * 4);  // byte offset of this warp's words in a row
         int ws = 0, wph = 0, ab = 0, aph = 0;
-        unsigned long long* tl = ((p.dbg & 32) && blockIdx.x < 2 && dw == 0 && lane == 0)
-                                     ? g_gemm_tl + blockIdx.x * 8 * 256 : nullptr;
-        int tcount = 0;
-        SegIter it = seg_begin(p);
-        for (GSeg sg; it.next(p, sg);) {
+        GSeg sg;
+        for (int k = 0; seg_at(p, k, sg); ++k) {
             for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                 mbar_wait_sleep(&wfull[ws], wph, 200);
-                if (tl) tl[0 * 256 + (tcount & 255)] = gtimer_ns();
                 const uint32_t u = smem_u32(wbuf + static_cast<size_t>(ws) * p.stage_w);
                 const __half2 s2 = __half2half2(__ushort_as_half(lds_u16(u + 2 * r)));
                 const __half2 z2 = __half2half2(__ushort_as_half(lds_u16(u + 256 + 2 * r)));
@@ -655,11 +592,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&wempty[ws]);  // shared-memory reads of this stage are done
-                if (tl) tl[1 * 256 + (tcount & 255)] = gtimer_ns();
                 // 4 A buffers let dequant run ahead of the MMA, so waiting for the
                 // buffer before the math costs little and keeps registers low
                 mbar_wait_sleep(&aempty[ab], aph ^ 1, 300);
-                if (tl) tl[2 * 256 + (tcount & 255)] = gtimer_ns();
                 tc_fence_after();
                 const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + ab * 64 + kh * kWords * 16;
 #pragma unroll
@@ -668,42 +603,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
 #pragma unroll
                     for (int i = 0; i < NP; ++i) pw[i] = pl[i][w];
                     uint32_t H[16];
-                    if (p.dbg & 1) {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) H[j] = 0x3C003C00u;
-                    } else {
-                        dequant_word<NP>(pw, s2, z2, H);
-                    }
+                    dequant_word<NP>(pw, s2, z2, H);
                     tc_st_x16(ta + w * 16, H);
                 }
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[ab]);
-                if (tl) tl[3 * 256 + (tcount & 255)] = gtimer_ns();
-                ++tcount;
                 if (++ws == SW) { ws = 0; wph ^= 1; }
                 if (++ab == kNA) { ab = 0; aph ^= 1; }
             }
         }
-        if (ph && dw == 0 && lane == 0) g_gemm_ph[blockIdx.x * 16 + 10] = gtimer_ns();
     }
     tc_fence_before();
     __syncthreads();
-    if (ph && threadIdx.x == 0) g_gemm_ph[blockIdx.x * 16 + 5] = gtimer_ns();
     if (warp == 1) {
         tc_fence_after();
         tc_dealloc(tbase, kTmemCols);
     }
 }
 
-int tile_n(int64_t M) {
-    if (const char* e = getenv("SFMP_GEMM_N")) {
-        const int n = atoi(e);
-        if (n >= 16 && n <= kMaxN && n % 16 == 0) return n;
-    }
-    return M >= kMaxN ? kMaxN : static_cast<int>((M + 15) / 16 * 16);
-}
+int tile_n(int64_t M) { return M >= kMaxN ? kMaxN : static_cast<int>((M + 15) / 16 * 16); }
 
 uint32_t unit_max_bytes(const DevModel& m) {
     const int F = m.floor_bits;
@@ -711,17 +631,34 @@ uint32_t unit_max_bytes(const DevModel& m) {
     return static_cast<uint32_t>(kUnitHdr + F * kPlaneBytes + (extra ? kPlaneBytes : 0));
 }
 
+// K splits per tile: a function of the UNSHARDED matrix shape and M only
+// (never of the device or the shard), so a row's accumulation order -- and its
+// bits -- are the same on any B200, for any shard count.  Split when the
+// whole matrix has fewer tiles than half a virtual 148-SM grid: each split
+// keeps >= 8 K chunks.
+constexpr int kVirtualSMs = 148;
+int k_splits(const DevModel& m, int64_t M) {
+    const int64_t N = tile_n(M), TT = (M + N - 1) / N;
+    const int64_t KC = static_cast<int64_t>(m.cols / 128);
+    const int64_t tiles_g = static_cast<int64_t>((m.global_rows + 127) / 128) * TT;
+    if (tiles_g * 2 > kVirtualSMs) return 1;
+    int64_t ks = (kVirtualSMs + tiles_g - 1) / tiles_g;
+    ks = std::min<int64_t>(ks, KC / 8);
+    return static_cast<int>(std::max<int64_t>(1, ks));
+}
+
+template <class F>
+void once_per_device(std::once_flag* flags, F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(flags[dev & 63], f);
+}
+
 template <int NP>
 cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t st) {
     auto k = gemm_kernel<NP>;
-    static int configured[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-        if (e != cudaSuccess) return e;
-        configured[dev] = 1;
-    }
+    static std::once_flag fl[64];
+    once_per_device(fl, [&] { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit); });
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
@@ -734,28 +671,19 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t s
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, k, p);
     if (e != cudaSuccess) return e;
-    if (!p.rr && p.Q % p.KC != 0) {  // some tiles are split along K: stream-K fix-up
-        const int nb = static_cast<int>((p.work - p.w0 + p.Q - 1) / p.Q);  // CTAs with a stream-K range
-        gemm_reduce_kernel<<<dim3((p.N + 31) / 32, nb), 128, 0, st>>>(p);
-        e = cudaGetLastError();
+    if (p.ks > 1) {  // split-K fix-up, a programmatic dependent of the GEMM
+        cudaLaunchConfig_t rc{};
+        rc.gridDim = dim3((p.N + 31) / 32, p.items / p.ks);
+        rc.blockDim = dim3(128);
+        rc.stream = st;
+        rc.attrs = attr;
+        rc.numAttrs = 1;
+        e = cudaLaunchKernelEx(&rc, gemm_reduce_kernel, p);
     }
     return e;
 }
 
 }  // namespace
-
-extern "C" int sfmp_debug_gemm_phases(unsigned long long* host, size_t n) {
-    if (n > static_cast<size_t>(kPhCtas) * 16) n = static_cast<size_t>(kPhCtas) * 16;
-    cudaError_t e = cudaMemcpyFromSymbol(host, g_gemm_ph, n * sizeof(unsigned long long));
-    void* d = nullptr;
-    cudaGetSymbolAddress(&d, g_gemm_ph);
-    cudaMemset(d, 0, sizeof(unsigned long long) * kPhCtas * 16);
-    return static_cast<int>(e);
-}
-extern "C" int sfmp_debug_gemm_timeline(unsigned long long* host, size_t n) {
-    if (n > 2 * 8 * 256) n = 2 * 8 * 256;
-    return static_cast<int>(cudaMemcpyFromSymbol(host, g_gemm_tl, n * sizeof(unsigned long long)));
-}
 
 // ---------------------------------------------------------------------------
 // Upload-time row-tile layout (host).  For output column c of y (0..out_rows)
@@ -815,17 +743,44 @@ std::vector<uint32_t> gemm_slot_table(const std::vector<uint32_t>& col_perm) {
 }
 
 bool gemm_supported(const DevModel& m) {
-    return m.d_gl != nullptr && m.d_xslot != nullptr && m.cols * 2 <= static_cast<uint64_t>(kSmemLimit) && m.ceil_bits >= 1 && m.ceil_bits <= 8 && m.cols < (1ull << 31);
+    return m.d_gl != nullptr && m.d_xslot != nullptr && m.cols * 2 <= 200ull * 1024 && m.ceil_bits >= 1 && m.ceil_bits <= 8 && m.cols < (1ull << 31);
 }
 
-// Workspace: swizzled X images | stream-K partial tiles [grid <= num_sms][2][N][128] f32.
+template <sfmp_dtype DT>
+void launch_xprep_rows(const void* x, const DevModel& m, uint8_t* xs, float* ysc, const GemmParams& p, int cols, int Mpad,
+                       int grid, size_t smem, cudaStream_t st) {
+    static std::once_flag fl[64];
+    once_per_device(fl, [] { cudaFuncSetAttribute(xprep_gemm_rows_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+    xprep_gemm_rows_kernel<DT><<<grid, 512, smem, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad);
+}
+template <sfmp_dtype DT>
+void launch_xprep_tok(const void* x, const DevModel& m, uint8_t* xs, float* ysc, const GemmParams& p, int cols, int Mpad,
+                      cudaStream_t st) {
+    static std::once_flag fl[64];
+    once_per_device(fl, [] {
+        cudaFuncSetAttribute(xprep_gemm_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(xprep_gemm_kernel<DT>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    });
+    xprep_gemm_kernel<DT><<<Mpad, 128, static_cast<size_t>(cols) * 2, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad);
+}
+
+// Workspace: swizzled X images | per-token scales | split-K partial tiles [items][N][128] f32.
 size_t gemm_x_bytes(const DevModel& m, int64_t M) {
     const int N = tile_n(M);
     const int64_t TT = (M + N - 1) / N;
     return (static_cast<size_t>(TT) * N * m.cols * 2 + 255) / 256 * 256;
 }
+size_t gemm_scale_bytes(int64_t M) {
+    const int N = tile_n(M);
+    const int64_t TT = (M + N - 1) / N;
+    return (static_cast<size_t>(TT) * N * 4 + 255) / 256 * 256;
+}
 size_t gemm_workspace_bytes(const DevModel& m, int64_t M) {
-    return gemm_x_bytes(m, M) + static_cast<size_t>(m.num_sms) * 2 * tile_n(M) * 128 * 4;
+    const int ks = k_splits(m, M);
+    const int N = tile_n(M);
+    const int64_t TT = (M + N - 1) / N;
+    const size_t part = ks > 1 ? static_cast<size_t>(m.gl_row_tiles * TT * ks) * N * 128 * 4 : 0;
+    return gemm_x_bytes(m, M) + gemm_scale_bytes(M) + part;
 }
 
 cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y, void* ws,
@@ -838,23 +793,22 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     p.RT = static_cast<int>(m.gl_row_tiles);
     p.wl = m.d_gl;
     p.woff = m.d_gl_off;
-    p.xs = static_cast<const uint8_t*>(ws);
-    p.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + gemm_x_bytes(m, M));
+    uint8_t* xs = static_cast<uint8_t*>(ws);
+    float* ysc = reinterpret_cast<float*>(xs + gemm_x_bytes(m, M));
+    p.xs = xs;
+    p.ysc = ysc;
+    p.part = reinterpret_cast<float*>(xs + gemm_x_bytes(m, M) + gemm_scale_bytes(M));
     p.y = y;
     p.out_rows = m.out_rows;
     p.floor_bits = m.floor_bits;
     p.has_extra = m.ceil_bits > m.floor_bits;
     p.idesc = tc_idesc_f16(128, p.N);
-    if (const char* e = getenv("SFMP_GEMM_DEBUG")) p.dbg = atoi(e);
     p.stage_w = (unit_max_bytes(m) + 127) / 128 * 128;
     const uint32_t xstage = static_cast<uint32_t>(p.N) * 128;
-    const size_t bar_bytes = (256 + (static_cast<size_t>(p.KC) + 1) * 8 + 1023) / 1024 * 1024;
-    p.bar_bytes = static_cast<uint32_t>(bar_bytes);
-    constexpr size_t kStageBytes = 0;
-    // W ring: 4 units; X ring: as many 64-column atoms as the rest holds (<= 8)
-    const size_t avail = kSmemLimit - 1024 - bar_bytes - kStageBytes;
+    const size_t bar_bytes = 1024;
+    // W ring: up to 8 units; X ring: as many 64-column atoms as the rest holds (<= 8)
+    const size_t avail = kSmemLimit - 1024 - bar_bytes;
     p.SW = 8;
-    if (const char* e = getenv("SFMP_GEMM_SW")) p.SW = std::max(2, std::min(8, atoi(e)));
     p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
     while (p.SX < 4 && p.SW > 4) {
         --p.SW;
@@ -865,113 +819,47 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
         p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
     }
     if (p.SX < 2) return cudaErrorInvalidConfiguration;
-    const size_t smem = 1024 + p.SX * xstage + p.SW * p.stage_w + bar_bytes + kStageBytes;
-    // K4 (prefill flavour): gather + convert + swizzle X
+    const size_t smem = 1024 + p.SX * xstage + p.SW * p.stage_w + bar_bytes;
+    // K4 (prefill flavour): gather + scale + convert + swizzle X
     const int cols = static_cast<int>(m.cols);
     const int Mpad = p.TT * p.N;
-    // one token per CTA (all resident at once for the usual shapes): the pass
-    // costs about one token's load-gather-store latency instead of a loop
-    int xthreads = 128;
-    if (const char* e = getenv("SFMP_XPREP_THREADS")) xthreads = std::max(32, std::min(1024, atoi(e)));
-    const int xgrid = Mpad;
-    const size_t xsm = static_cast<size_t>(cols) * 2;
-    uint8_t* xs = static_cast<uint8_t*>(ws);
-    // persistent pre-pass when the u16 slot table + two rows fit (>= 2 CTAs per SM)
     const size_t elem = dt == SFMP_F32 ? 4 : 2;
+    // persistent pre-pass when the u16 slot table + two rows fit (>= 2 CTAs per SM)
     const size_t rsm = 16 + (static_cast<size_t>(cols) * 2 + 15) / 16 * 16 + 2 * static_cast<size_t>(cols) * elem;
-    const bool rows_ok = cols < 65536 && rsm <= 110 * 1024 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-                         !getenv("SFMP_XPREP_LEGACY");
-    if (!(p.dbg & 16) && rows_ok) {
+    const bool rows_ok = cols < 65536 && rsm <= 110 * 1024 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    cudaError_t e0 = cudaSuccess;
+    if (rows_ok) {
         const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / rsm)));
         const int rgrid = static_cast<int>(std::min<int64_t>(Mpad, static_cast<int64_t>(per_sm) * m.num_sms));
-        cudaError_t e0 = cudaSuccess;
         switch (dt) {
-            case SFMP_F32:
-                e0 = cudaFuncSetAttribute(xprep_gemm_rows_kernel<SFMP_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                xprep_gemm_rows_kernel<SFMP_F32><<<rgrid, 512, rsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
-                break;
-            case SFMP_F16:
-                e0 = cudaFuncSetAttribute(xprep_gemm_rows_kernel<SFMP_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                xprep_gemm_rows_kernel<SFMP_F16><<<rgrid, 512, rsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
-                break;
-            default:
-                e0 = cudaFuncSetAttribute(xprep_gemm_rows_kernel<SFMP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                xprep_gemm_rows_kernel<SFMP_BF16><<<rgrid, 512, rsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
-                break;
+            case SFMP_F32: launch_xprep_rows<SFMP_F32>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st); break;
+            case SFMP_F16: launch_xprep_rows<SFMP_F16>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st); break;
+            default: launch_xprep_rows<SFMP_BF16>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st); break;
         }
-        if (e0 != cudaSuccess) return e0;
-    } else if (!(p.dbg & 16)) {
-        cudaError_t e0 = cudaSuccess;
+    } else {
         switch (dt) {
-            case SFMP_F32:
-                e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F32>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-                xprep_gemm_kernel<SFMP_F32><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
-                break;
-            case SFMP_F16:
-                e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_F16>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-                xprep_gemm_kernel<SFMP_F16><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
-                break;
-            default:
-                e0 = cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
-                cudaFuncSetAttribute(xprep_gemm_kernel<SFMP_BF16>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-                xprep_gemm_kernel<SFMP_BF16><<<xgrid, xthreads, xsm, st>>>(x, m.d_xslot, xs, p.M, p.N, p.KC, cols, Mpad);
-                break;
+            case SFMP_F32: launch_xprep_tok<SFMP_F32>(x, m, xs, ysc, p, cols, Mpad, st); break;
+            case SFMP_F16: launch_xprep_tok<SFMP_F16>(x, m, xs, ysc, p, cols, Mpad, st); break;
+            default: launch_xprep_tok<SFMP_BF16>(x, m, xs, ysc, p, cols, Mpad, st); break;
         }
-        if (e0 != cudaSuccess) return e0;
     }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (p.dbg & 8) return cudaSuccess;
+    e0 = cudaGetLastError();
+    if (e0 != cudaSuccess) return e0;
     // (Clusters of 4 sharing X by TMA multicast measured no faster and capped the
     // grid at the co-resident cluster count, 132 of 148 SMs: not used.)
-    // Whole tiles per CTA when they fill the SMs (measured: splitting big
-    // tile counts along K costs more than the wave it saves); stream-K when
-    // there are fewer tiles than SMs (small M, k/v): >= 8 steps per CTA.
     const int64_t ntiles = static_cast<int64_t>(p.RT) * p.TT;
-    p.work = ntiles * p.KC;
-    const int sms = m.num_sms;
-    // measured (tools/sweep.py, prof_gemm.py): stream-K pays off when the tiles
-    // leave at least half the SMs idle (k/v at M <= 2048: 64 tiles, 35 vs 38 us;
-    // q at M=512: 29 vs 33 us) or leave SMs idle while each CTA still gets a
-    // long K range (>= 32 steps); otherwise whole tiles round-robin (k/v at
-    // M=4096, 128 tiles: 49 vs 59 us)
-    const bool sk = ntiles * 2 <= sms || (ntiles < sms && (p.work + sms - 1) / sms >= 32);
-    p.rr = sk ? 0 : 1;
-    if (const char* e = getenv("SFMP_GEMM_SK")) p.rr = atoi(e) ? 0 : 1;
-    p.Q = p.KC;
-    p.w0 = p.work;
-    int S = static_cast<int>(std::min<int64_t>(ntiles, sms));
-    if (!p.rr) {
-        p.w0 = 0;
-        p.Q = std::max<int64_t>(std::min<int64_t>(p.KC, 8), (p.work + sms - 1) / sms);
-        S = static_cast<int>((p.work + p.Q - 1) / p.Q);
-    } else if (ntiles > sms) {
-        // Hybrid: full rounds of whole tiles, the remainder (a partial wave)
-        // as stream-K ranges of >= 8 steps over all CTAs -- when the remainder
-        // is small (measured: gate/up 896 tiles = 6 x 148 + 8: 195 -> 190 us;
-        // with a large remainder the partial tiles' reduction costs more than
-        // the idle SMs: q 256 = 148 + 108 tiles, 63 -> 68 us).
-        const int64_t rounds = ntiles / sms, rem = ntiles - rounds * sms;
-        bool hybrid = rem > 0 && rem * 4 <= static_cast<int64_t>(sms);
-        if (const char* e = getenv("SFMP_GEMM_HYBRID")) hybrid = hybrid && atoi(e) != 0;
-        if (hybrid) {
-            p.rr = 0;
-            p.w0 = rounds * sms * p.KC;
-            p.Q = std::max<int64_t>(8, (rem * p.KC + sms - 1) / sms);
-            S = sms;
-        }
-    }
+    p.ks = k_splits(m, M);
+    p.items = static_cast<int>(ntiles * p.ks);
+    const int grid = static_cast<int>(std::min<int64_t>(p.items, m.num_sms));
     switch (m.ceil_bits) {
-        case 1: return launch_np<1>(p, smem, S, st);
-        case 2: return launch_np<2>(p, smem, S, st);
-        case 3: return launch_np<3>(p, smem, S, st);
-        case 4: return launch_np<4>(p, smem, S, st);
-        case 5: return launch_np<5>(p, smem, S, st);
-        case 6: return launch_np<6>(p, smem, S, st);
-        case 7: return launch_np<7>(p, smem, S, st);
-        default: return launch_np<8>(p, smem, S, st);
+        case 1: return launch_np<1>(p, smem, grid, st);
+        case 2: return launch_np<2>(p, smem, grid, st);
+        case 3: return launch_np<3>(p, smem, grid, st);
+        case 4: return launch_np<4>(p, smem, grid, st);
+        case 5: return launch_np<5>(p, smem, grid, st);
+        case 6: return launch_np<6>(p, smem, grid, st);
+        case 7: return launch_np<7>(p, smem, grid, st);
+        default: return launch_np<8>(p, smem, grid, st);
     }
 }
 

@@ -10,30 +10,45 @@
 //    HBM (sfmp_internal.h), so a unit is one contiguous span fetched by ONE
 //    1-D bulk async copy (cp.async.bulk on the TMA engine) into a small
 //    mbarrier ring.
-//  * Each 128-row tile is split over C CTAs (split-K); CTA s streams block
-//    columns [s*BC/C, (s+1)*BC/C), writes its f32 partial tile to the
-//    workspace and bumps the tile's counter; the last CTA to finish sums the
-//    C partials in split order and stores them un-permuted (deterministic,
-//    no float atomics) and re-zeroes the counter for the next call.
+//  * Canonical accumulation order ("independent of thread count,
+//    deterministic merge"): every 128-row tile is cut into fixed K segments of
+//    kSegCols = 1024 columns.  A segment's units are folded sequentially from
+//    zero; the segment sums of a tile are added in segment order.  The cut
+//    depends on the matrix alone, so a linear's output bits do not depend on
+//    the grid, the SM count, the other linears of a grouped launch, the
+//    number of shards or the token count M (MMA columns are independent).
+//  * Work items = (linear, tile, segment), handed out by a global queue
+//    (one atomic per item, claimed one item ahead by the producer), so SMs
+//    that run ahead take more items and all finish together.  A segment of a
+//    multi-segment tile stores its f32 partial and moves on (no barrier, no
+//    fence in the GEMV); gemv_fixup_kernel, a programmatic dependent launch,
+//    sums each tile's partials in segment order and stores the un-permuted
+//    rows (no float atomics).
 //  * The activation gather x[t][col_perm[.]] runs once per call in a small
-//    pre-pass (xprep_kernel) that writes, per block column, an "activation
-//    record": f16 MMA B fragments + per-token column sums.  The GEMV is a
-//    programmatic dependent of it: its producer streams weights while xprep
-//    runs and waits (griddepcontrol.wait) only before copying the records.
-//  * Compute: the bit-planes of a row's 32-weight word are transposed into
-//    nibble codes with 4 delta-swaps, and each nibble pair becomes one f16x2
-//    by a single LOP3 against a magic exponent (1024+c or 64+c).  The magic
-//    offsets are a per-token constant folded in f32 after the MMA (bias term
-//    from the record), so the tensor pipe (mma.m16n8k16, tokens = N)
-//    contracts exact integer codes against f16 activations.  The per-row
-//    affine (s, z) of each block is applied in f32 after the block column:
-//    y += s*(C - bias) + z*sum(x) == sum((s*c+z)*x) up to f32 rounding.  The
-//    K permutation inside each 128-column chunk is absorbed by the record.
+//    pre-pass (xprep_*) that writes, per block column, an "activation
+//    record": f16 MMA B fragments + per-token column sums + the per-token
+//    output scale.  Each token row is first scaled by a power of two 2^-e_t
+//    (max|x_t| -> [2^-10, 2^-9)), so every finite input stays in range; f32
+//    inputs are split x = hi + lo into two f16 terms (22 significant bits)
+//    contracted by two MMAs; y is multiplied back by 2^e_t (exact).
+//    The GEMV is a programmatic dependent of the pre-pass: its producer
+//    streams weights while the pre-pass runs and waits (griddepcontrol.wait)
+//    only before copying the records.
+//  * Compute: each unit's bit planes were re-arranged at upload (repack.cuh)
+//    so every f16x2 MMA A register is one LOP3 AND of a word: the codes land
+//    in mantissa bits [p, p+B) under a zero exponent, i.e. the EXACT f16
+//    subnormal c * 2^(p-24).  The activation paired with that register is
+//    pre-scaled by 2^(24-p) in the record (one record section per bit-width
+//    layout of the matrix), so the tensor pipe (mma.m16n8k16, tokens = N)
+//    contracts exact integer codes against the scaled activations with no
+//    magic offset to cancel.  The per-row affine (s, z) of each block is
+//    applied in f32 after the block column: y += s*C + z*sum(x)
+//    == sum((s*c+z)*x) up to f32 rounding.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
-#include <cstdlib>
+#include <mutex>
 
 #include "ptx.cuh"
 #include "repack.cuh"
@@ -44,149 +59,137 @@ namespace sfmpk {
 
 namespace {
 
-constexpr int kTR = 128;  // rows per unit
-#ifndef SFMP_GEMV_MT
-#define SFMP_GEMV_MT 2
+constexpr int kTR = 128;          // rows per unit
+constexpr int kMT = 2;            // m16 tiles (16 rows each) per compute warp
+constexpr int kNCW = 8 / kMT;     // compute warps per 128-row tile
+constexpr int kThreads = 32 * (1 + kNCW);  // producer | compute warps
+#ifndef SFMP_SEG_COLS
+#define SFMP_SEG_COLS 1024
 #endif
-constexpr int kMT = SFMP_GEMV_MT;  // m16 tiles (16 rows each) per compute warp
-constexpr int kNCW = 8 / kMT;      // compute warps per 128-row tile
-#ifndef SFMP_GEMV_CTAS1
-#define SFMP_GEMV_CTAS1 (SFMP_GEMV_MT == 2 ? 4 : 3)
+constexpr int kSegCols = SFMP_SEG_COLS;  // canonical K segment (columns)
+constexpr int kHdrBytes = 1024;   // barriers | zero fragments | stage info | flag
+constexpr int kSmemSM = 225 * 1024;
+#ifndef SFMP_CTAS1
+#define SFMP_CTAS1 4
 #endif
-#ifndef SFMP_GEMV_CTAS2
-#define SFMP_GEMV_CTAS2 (SFMP_GEMV_MT == 2 ? 3 : 2)
+#ifndef SFMP_CTAS2
+#define SFMP_CTAS2 3
 #endif
-constexpr int kCtasNT1 = SFMP_GEMV_CTAS1, kCtasNT2 = SFMP_GEMV_CTAS2;  // resident CTAs per SM
-constexpr int kThreads = 32 * (1 + kNCW);
-constexpr int kHdrBytes = 1280;  // barriers | zeros | stage bit-widths | out_map
-// resident CTAs per SM: 4 for M<=8 (NT=1), 3 for M<=16 (NT=2, more registers)
+constexpr int kCtasNT1 = SFMP_CTAS1, kCtasNT2 = SFMP_CTAS2;  // resident CTAs per SM (M <= 8 / 9..16)
 __host__ __device__ constexpr int ctas_per_sm(int NT) { return NT == 1 ? kCtasNT1 : kCtasNT2; }
-__host__ __device__ constexpr int smem_per_cta(int NT) { return (225 * 1024) / ctas_per_sm(NT); }
 
-// One linear of a (possibly grouped) launch: independent matrices -- e.g. the
-// seven linears of a decoder layer -- share one launch so the fixed per-call
-// latencies (launch, first HBM bytes, split-K tail) are paid once.
-constexpr int kMaxLin = 40;
-constexpr int kMaxSplit = 32;  // CTAs that may share one row tile
-struct Lin {
-    const uint8_t* payload;
-    const uint64_t* unit_desc;  // [RT*BC] row-tile-major
-    const uint32_t* out_map;
-    const uint8_t* xrec;        // [BC] activation records of rec_bytes (xprep_kernel)
-    float* y;
-    float* part;                // [RT][C][16][128] f32 split-K partials
-    unsigned* counters;         // [RT] completion counters (zero between calls)
-    uint64_t out_rows;
-    int BC;
-    int M;                      // tokens of this linear (problems of one launch may differ)
-    uint32_t rec_bytes;         // its activation record bytes (RecGeom{M})
-    int64_t unit0;              // first unit of this linear in the group's unit sequence
-};
-struct Params {
-    Lin lin[kMaxLin];
-    int nlin;
-    int64_t units;  // units of all linears
-    int64_t Q;      // units per CTA
-    int M;          // max tokens over the linears (all <= 8 or all in 9..16)
-    int n_b;
-    int stages;
-    uint32_t stage_w;    // bytes per weight stage (smem)
-    uint32_t rec_bytes;  // max activation record bytes (shared-memory stage stride)
-    int debug_mode;      // 0 normal; 5 timeline stamps
-};
-struct XLin {
-    const void* x;
-    const uint32_t* col_perm;
-    uint8_t* xrec;
-    int BC, cols, warp0;
-    int item0;  // first pre-pass CTA of this linear (one per token x 8 block columns)
-    int lo;     // floor bit-width: records carry the magic biases of lo and lo+1 bit units
-    int M;      // tokens of this linear
-    uint32_t rec_bytes;
-};
-struct XParams {
-    XLin lin[kMaxLin];
-    int nlin, M, n_b;
-    uint32_t rec_bytes;
-    int dbg;
-    int wait_prev;  // launched as a programmatic dependent of the previous GEMV
-};
-
-// Activation record of one block column (n_b columns), for M tokens:
-//   for chunk c (128 columns), n-tile nt (8 tokens), token n < Mnt, k-step s:
-//     4 lanes x 8 B of f16 B fragments  (tokens >= M omitted)
-//   then Xg[16] (f32 column sums), then for the floor-bit and the ceil-bit
-//   layout the NEGATED per-token magic offset (repack.cuh) as MMA accumulator
-//   fragments [nt][lane quad q][4] = {-b(2q), -b(2q+1), -b(2q), -b(2q+1)} of
-//   n-tile nt: one 16-byte load initialises an accumulator, so C - bias comes
-//   out of the MMA itself.
-// Within a (c, nt, n) run the 8 k-steps are contiguous (stride 32 B), so a
-// lane's fragment addresses are compile-time offsets from one base.  Runs are
-// kRun = 288 B apart (256 B + 32 B pad): a warp's k-step load then spreads the
-// 8 tokens over all 32 banks (2 wavefronts for 256 B) instead of hitting one
-// bank pair 8 times (at 256 B stride the B loads were 59 % bank conflicts and
-// the shared-memory pipe the M=16 bottleneck).
-constexpr int kRun = 288;
-// float index (from xg_off) of token t's accumulator-init slots, layout hi=0/1
-__host__ __device__ __forceinline__ int bias_slot(int t, int hi) {
-    return 16 + hi * 32 + ((t >> 3) * 4 + ((t & 7) >> 1)) * 4 + (t & 1);
+#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
+}  // namespace
+// Experiment builds only: per-CTA [start ns, end ns, smid, items] of the last
+// launch; then kernel-level [min start, max end] of xprep, gemv, fixup.
+__device__ unsigned long long g_gemv_tl[4096 * 4 + 16];
+namespace {
+__device__ __forceinline__ void tl_kernel(int k, bool start) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (start) atomicMin(&g_gemv_tl[4096 * 4 + 2 * k], t);
+    else atomicMax(&g_gemv_tl[4096 * 4 + 2 * k + 1], t);
 }
-struct RecGeom {
-    int M;
-    __host__ __device__ int mnt(int nt) const { return nt == 0 ? (M < 8 ? M : 8) : M - 8; }
-    __host__ __device__ int nt_count() const { return M > 8 ? 2 : 1; }
-    __host__ __device__ int chunk_bytes() const { return kRun * M; }  // all n-tiles
-    __host__ __device__ int lane_off(int c, int nt, int n, int q) const {
-        return c * chunk_bytes() + nt * 8 * kRun + n * kRun + q * 8;
-    }
-    __host__ __device__ int frag_off(int c, int nt, int s, int n, int q) const {
-        return lane_off(c, nt, n, q) + s * 32;
-    }
-    __host__ __device__ int xg_off(int CH) const { return CH * chunk_bytes(); }
-    __host__ __device__ int bytes(int CH) const { return (xg_off(CH) + 320 + 127) / 128 * 128; }
-};
-
-// Debug timeline (SFMP_GEMV_DEBUG=5): [cta][slot] globaltimer stamps for the
-// first kDbgCtas CTAs: slot 0 start, 1 end, 2+3i producer issue of unit i,
-// 3+3i full observed by compute warp 0, 4+3i unit done; row kDbgCtas-1 slots
-// 100.. hold kernel-level stamps.
-constexpr int kDbgCtas = 512, kDbgSlots = 128;
-__device__ unsigned long long g_dbg_timeline[kDbgCtas * kDbgSlots];
-__device__ __forceinline__ unsigned long long gtimer() {
+#define TL_K(k, start) tl_kernel(k, start)
+__device__ __forceinline__ unsigned long long tl_now() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define DBG_STAMP(slot)                                                                       \
-    do {                                                                                      \
-        if (dbg == 5 && blockIdx.x < kDbgCtas - 1 && (slot) < kDbgSlots)                      \
-            g_dbg_timeline[blockIdx.x * kDbgSlots + (slot)] = gtimer();                       \
-    } while (0)
-#define DBG_KSTAMP(slot)                                                                      \
-    do {                                                                                      \
-        if (dbg == 5) g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + (slot)] = gtimer();         \
-    } while (0)
-// Per-unit stamps cost ~12 issue slots per unit even when off: compiled in
-// only with -DSFMP_GEMV_TIMELINE=1 (tools/prof_group.py's timeline).
-#ifndef SFMP_GEMV_TIMELINE
-#define SFMP_GEMV_TIMELINE 0
-#endif
-#if SFMP_GEMV_TIMELINE
-#define DBG_USTAMP(slot) DBG_STAMP(slot)
 #else
-#define DBG_USTAMP(slot) \
-    do {                 \
-    } while (0)
+#define TL_K(k, start) do {} while (0)
 #endif
 
-template <sfmp_dtype DT>
-__device__ __forceinline__ float load_x(const void* x, size_t i) {
-    if constexpr (DT == SFMP_F32) return __ldg(static_cast<const float*>(x) + i);
-    else if constexpr (DT == SFMP_F16)
-        return __half2float(__ldg(static_cast<const __half*>(x) + i));
-    else
-        return __bfloat162float(__ldg(static_cast<const __nv_bfloat16*>(x) + i));
+#ifndef SFMP_L2_PREFETCH
+#define SFMP_L2_PREFETCH 0  // measured slower (weights of the next item into L2 during the pre-pass)
+#endif
+
+// stage info flags (producer -> compute warps, one 16-byte record per stage)
+constexpr uint32_t kFirst = 1, kLast = 2, kEnd = 4;
+
+// One linear of a (possibly grouped) launch.
+constexpr int kMaxLin = 40;
+struct Lin {
+    const uint8_t* payload;
+    const uint64_t* unit_desc;  // [RT*BC] row-tile-major
+    const uint32_t* out_map;
+    const uint8_t* xrec;        // [BC] activation records of rec_bytes (nl sections of sec_bytes)
+    float* y;
+    float* part;                // [RT][P][16][128] f32 segment partials
+    uint64_t out_rows;
+    int BC, M, P, L;            // block columns, tokens, segments per tile, units per segment
+    int RT;
+    uint32_t rec_bytes;         // its activation record bytes
+    uint32_t sec_bytes;         // one bit-width layout section of the record
+    uint32_t lo_off;            // offset of the lo fragments inside a 128-column chunk (f32 input)
+    int item0;                  // first work item of this linear
+    int fix0;                   // first fix-up (tile, token) pair of this linear
+    int lo;                     // floor bits: units at lo use section 0, lo+1 section 1
+};
+struct Params {
+    Lin lin[kMaxLin];
+    int nlin;
+    int n_items;
+    int n_fix;           // fix-up (tile, token) pairs
+    int item_start[kMaxLin + 1];  // first work item of each linear (+ total)
+    int fix_start[kMaxLin + 1];   // first fix-up pair of each linear (+ total; none if P == 1)
+    unsigned* queue;     // [0] next item, [1] CTAs done (zero between calls)
+    int n_b;
+    int stages;
+    uint32_t stage_w;    // bytes per weight stage (smem)
+    uint32_t sec_bytes;  // max record section bytes (shared-memory stage stride)
+};
+// Index of the linear owning entry `v` of a prefix array (binary search).
+__device__ __forceinline__ int owner_of(const int* start, int n, int v) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (start[mid] <= v) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
 }
+
+struct XLin {
+    const void* x;
+    const uint32_t* col_perm;
+    uint8_t* xrec;
+    float* escale;  // per-token exponents from rowscale_kernel (wide-row pre-pass)
+    int BC, cols, warp0;
+    int item0;      // first pre-pass CTA of this linear (one per token x 8 block columns)
+    int lo, nl;     // floor bit-width, number of layout sections (1 or 2)
+    int M;          // tokens of this linear
+    uint32_t rec_bytes, sec_bytes;
+};
+struct XParams {
+    XLin lin[kMaxLin];
+    int nlin, M, n_b;
+    int wait_prev;  // launched as a programmatic dependent of the previous GEMV
+};
+
+// Activation record of one block column (n_b columns), for M tokens: one
+// SECTION per bit-width layout (floor, ceil) of the matrix -- the producer
+// copies only the section of the unit's own bit-width.  A section:
+//   for chunk c (128 columns): hi runs of tokens 0..M-1, then (f32 input)
+//   lo runs of tokens 0..M-1.  A run = the token's 8 k-step B fragments,
+//   4 lanes x 8 B each (256 B), runs kRun = 288 B apart (the 32-byte pad
+//   spreads a warp's 8 tokens over all banks); each value is the scaled
+//   activation times 2^(24-p) of the register slot it pairs with.
+//   Tail (floats): Xg[16] column sums of the scaled x | ysa[16], ysb[16]
+//   with ysa*ysb = 2^e_t (two factors: 2^e_t may not be a normal float).
+constexpr int kRun = 288;
+constexpr int kTailFloats = 48;
+constexpr int kYsIdx = 16;
+struct RecGeom {
+    int M;
+    bool X2;
+    __host__ __device__ int nt_count() const { return M > 8 ? 2 : 1; }
+    __host__ __device__ int chunk_bytes() const { return kRun * M * (X2 ? 2 : 1); }
+    __host__ __device__ int lo_off() const { return kRun * M; }
+    __host__ __device__ int run_off(int c, int t, int q) const { return c * chunk_bytes() + t * kRun + q * 8; }
+    __host__ __device__ int xg_off(int CH) const { return CH * chunk_bytes(); }
+    __host__ __device__ int sec_bytes(int CH) const { return (xg_off(CH) + 4 * kTailFloats + 127) / 128 * 128; }
+};
 
 template <sfmp_dtype DT>
 struct XT;
@@ -207,25 +210,96 @@ struct XT<SFMP_BF16> {
 };
 constexpr int kXprepRowLimit = 192 * 1024;  // staged x row bytes (larger rows: xprep_kernel)
 
+// Per-token power-of-two scale: e such that max|x| * 2^-e lies in
+// [2^-10, 2^-9), so the largest record value (slot factor 2^24) lies in
+// [2^14, 2^15): every finite input stays finite in f16.  0 for an all-zero or
+// non-finite row (inf/nan then propagate as in the f32 reference).
+__device__ __forceinline__ int token_exponent(float amax) {
+    if (!(amax > 0.f) || !isfinite(amax)) return 0;
+    return ilogbf(amax) + 10;
+}
+// 2^e for |e| <= 254 as a product of two normal floats
+__device__ __forceinline__ float2 pow2_pair(int e) {
+    const int a = e / 2;
+    return make_float2(__int_as_float((a + 127) << 23), __int_as_float((e - a + 127) << 23));
+}
+
+// f16 hi (+ lo for f32 input) parts of v0*f, v1*f (f a power of two).
+template <bool X2>
+__device__ __forceinline__ void split2(float v0, float v1, float f, uint32_t& hi, uint32_t& lo) {
+    const float a = v0 * f, b = v1 * f;
+    const __half2 h = __floats2half2_rn(a, b);
+    hi = h2_as_u32(h);
+    if constexpr (X2) lo = h2_as_u32(__floats2half2_rn(a - __low2float(h), b - __high2float(h)));
+    else lo = 0u;
+}
+// slot factor 2^(24-p) of register j in the layout of B-bit units
+__device__ __forceinline__ float slot_factor(int B, int j) {
+    return __int_as_float((24 - sub_pos(B, j) + 127) << 23);
+}
+
+// Row-wide max |x| reduction of a staged row (256 threads).
+template <class T, class F>
+__device__ __forceinline__ float row_absmax(const T* xr, int cols, F cvt, float* red) {
+    float m = 0.f;
+    for (int i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(cvt(xr[i])));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+    return m;
+}
+
+// Record piece of one block column for token t from 4 gathered, scaled
+// values per chunk: lane (s8, q) owns registers 2*s8, 2*s8+1 of k-step s8;
+// each layout section gets them times its slot factors.
+template <bool X2>
+__device__ __forceinline__ void write_fragments(uint8_t* rec, const RecGeom& G, int c, int t, int q, int s8,
+                                                const float (&v)[4], int lo, int nl, uint32_t sec_bytes) {
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+        if (l >= nl) break;
+        const int B = lo + l;
+        uint2 h, w;
+        split2<X2>(v[0], v[1], slot_factor(B, 2 * s8), h.x, w.x);      // pairs with A register 2*s8
+        split2<X2>(v[2], v[3], slot_factor(B, 2 * s8 + 1), h.y, w.y);  // ... and 2*s8+1
+        uint8_t* dst = rec + l * sec_bytes + G.run_off(c, t, q) + s8 * 32;
+        *reinterpret_cast<uint2*>(dst) = h;
+        if constexpr (X2) *reinterpret_cast<uint2*>(dst + G.lo_off()) = w;
+    }
+}
+__device__ __forceinline__ void write_tail(uint8_t* rec, const RecGeom& G, int CH, int t, int M, float xs, int e,
+                                           int nl, uint32_t sec_bytes) {
+    const float2 ys = pow2_pair(e);
+    for (int l = 0; l < nl; ++l) {
+        float* xg = reinterpret_cast<float*>(rec + l * sec_bytes + G.xg_off(CH));
+        xg[t] = xs;
+        xg[kYsIdx + t] = ys.x;
+        xg[kYsIdx + 16 + t] = ys.y;
+        if (t == M - 1)  // token columns the GEMV computes but never stores
+            for (int u = M; u < 8 * G.nt_count(); ++u) xg[u] = xg[kYsIdx + u] = xg[kYsIdx + 16 + u] = 0.f;
+    }
+}
+
 // K4 (decode flavour, staged): one CTA per (token t, 8 block columns of one
 // linear).  It stages token t's x row and the 8 block columns' col_perm in
-// shared memory with coalesced 16 B loads, then each warp writes the record
-// piece of one block column for token t: lane (s, q) gathers the 4 k-slots
-// 32q + 8(s&1) + 4j + 16e + (s>>1) of each 128-column chunk from shared
-// memory and stores 8 B at frag_off(c, nt, s, n, q) -- the token's 256 B of a
-// chunk are one contiguous warp store.  The column sum X_g (lutgemm.cpp:
-// 113-115) uses the input values, the magic bias the f16-rounded ones.
+// shared memory with coalesced 16 B loads, finds the row's power-of-two
+// scale, then each warp writes the record piece of one block column for
+// token t: lane (s, q) gathers the 4 k-slots 32q + 8(s&1) + 4j + 16e + (s>>1)
+// of each 128-column chunk from shared memory and stores 8 B of B fragments
+// per layout (hi, and lo for f32 input) -- the token's 256 B of a chunk are
+// one contiguous warp store.  The column sum X_g (lutgemm.cpp:113-115) uses
+// the scaled input values.
 template <sfmp_dtype DT>
 __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     using T = typename XT<DT>::T;
+    constexpr bool X2 = DT == SFMP_F32;
     pdl_launch_dependents();  // let the GEMV start streaming weights right away
+    if (threadIdx.x == 0) TL_K(0, true);
     extern __shared__ __align__(16) uint8_t xsm[];
-    const int dbg = xp.dbg;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && dbg == 5) {
-        // previous launch's GEMV end (complete: stream order), then this start
-        g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 104] = g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102];
-        DBG_KSTAMP(100);
-    }
+    __shared__ float red[8];
     const int n_b = xp.n_b, CH = n_b >> 7;
     int it = blockIdx.x, li = 0;  // compact grid: (linear, token, 8 block columns)
     while (li + 1 < xp.nlin && it >= xp.lin[li + 1].item0) ++li;
@@ -252,50 +326,30 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
         }
     }
     __syncthreads();
+    const int e = token_exponent(row_absmax(xr, cols, [](T v) { return XT<DT>::f(v); }, red));
+    const float2 sc = pow2_pair(-e);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp >= nbc) return;
     const int bc = bc0 + warp, s8 = lane >> 2, q = lane & 3;
-    const RecGeom G{M};
+    const RecGeom G{M, X2};
     uint8_t* rec = XL.xrec + static_cast<size_t>(bc) * XL.rec_bytes;
     const uint32_t* cpw = cp + warp * n_b;
-    const int lo = XL.lo;
-    auto mag = [](int B, int j) { return B <= 4 ? rp_magic(B, j) : 0.f; };
-    const float mlx = mag(lo, 2 * s8), mly = mag(lo, 2 * s8 + 1);
-    const float mhx = mag(lo + 1, 2 * s8), mhy = mag(lo + 1, 2 * s8 + 1);
     const int kb = 32 * q + 8 * (s8 & 1) + (s8 >> 1);
-    float xs = 0.f, bias_lo = 0.f, bias_hi = 0.f;
+    float xs = 0.f;
     for (int c = 0; c < CH; ++c) {
         float v[4];
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) v[j * 2 + e] = XT<DT>::f(xr[cpw[c * 128 + kb + 4 * j + 16 * e]]);
-        uint2 st;
-        st.x = h2_as_u32(__floats2half2_rn(v[0], v[1]));  // pairs with A register 2*s8
-        st.y = h2_as_u32(__floats2half2_rn(v[2], v[3]));  // ... and 2*s8+1
-        *reinterpret_cast<uint2*>(rec + G.frag_off(c, t >> 3, s8, t & 7, q)) = st;
-        const float sx = __low2float(u32_as_h2(st.x)) + __high2float(u32_as_h2(st.x));
-        const float sy = __low2float(u32_as_h2(st.y)) + __high2float(u32_as_h2(st.y));
-        bias_lo += mlx * sx + mly * sy;
-        bias_hi += mhx * sx + mhy * sy;
+            for (int e2 = 0; e2 < 2; ++e2)
+                v[j * 2 + e2] = XT<DT>::f(xr[cpw[c * 128 + kb + 4 * j + 16 * e2]]) * sc.x * sc.y;
+        write_fragments<X2>(rec, G, c, t, q, s8, v, XL.lo, XL.nl, XL.sec_bytes);
         xs += (v[0] + v[1]) + (v[2] + v[3]);
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        xs += __shfl_xor_sync(0xffffffffu, xs, o);
-        bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, o);
-        bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, o);
-    }
-    if (lane == 0) {
-        float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
-        xg[t] = xs;
-        xg[bias_slot(t, 0)] = xg[bias_slot(t, 0) + 2] = -bias_lo;
-        xg[bias_slot(t, 1)] = xg[bias_slot(t, 1) + 2] = -bias_hi;
-        if (t == M - 1)  // token columns the GEMV computes but never stores
-            for (int u = M; u < 8 * G.nt_count(); ++u)
-                xg[u] = xg[bias_slot(u, 0)] = xg[bias_slot(u, 0) + 2] = xg[bias_slot(u, 1)] = xg[bias_slot(u, 1) + 2] = 0.f;
-    }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
+    for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+    if (lane == 0) write_tail(rec, G, CH, t, M, xs, e, XL.nl, XL.sec_bytes);
+    if (lane == 0) TL_K(0, false);
     // When launched to overlap the previous GEMV of the same grouped call, do
     // not complete before it: this grid's completion (which the next GEMV waits
     // for) then implies the previous launch's, keeping stream order for any
@@ -303,27 +357,31 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     if (xp.wait_prev) pdl_wait();
 }
 
-// Fallback for x rows above kXprepRowLimit bytes.
-// K4 (decode flavour): gather x[t][col_perm[.]] once per call into per-block-
-// column records laid out exactly as the MMA B fragments the GEMV consumes,
-// plus per-token column sums X_g (lutgemm.cpp:113-115) and the magic-offset
-// bias.  One item per (block column, n-tile); its CH 128-column chunks go to
-// CH warps of one CTA (so the col_perm -> x dependent loads of the chunks are
-// in flight together), whose sums are combined in chunk order through shared
-// memory.  Lane (n,q) owns token nt*8+n and k-slots 32q + 4h + a (+16).
+// Per-token exponents for the wide-row pre-pass: one CTA per (token, linear).
+template <sfmp_dtype DT>
+__global__ void __launch_bounds__(256) rowscale_kernel(const XParams xp) {
+    __shared__ float red[8];
+    const XLin& XL = xp.lin[blockIdx.y];
+    const int t = blockIdx.x;
+    if (t >= XL.M) return;
+    using T = typename XT<DT>::T;
+    const T* xrow = static_cast<const T*>(XL.x) + static_cast<size_t>(t) * XL.cols;
+    const float m = row_absmax(xrow, XL.cols, [](T v) { return XT<DT>::f(v); }, red);
+    if (threadIdx.x == 0) XL.escale[t] = static_cast<float>(token_exponent(m));
+}
+
+// Fallback for x rows above kXprepRowLimit bytes: one item per (block column,
+// n-tile); its CH 128-column chunks go to CH warps of one CTA, whose column
+// sums are combined in chunk order through shared memory.  Lane (n,q) owns
+// token nt*8+n and k-slots 32q + 4h + a (+16).
 template <sfmp_dtype DT>
 __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
-    pdl_launch_dependents();  // let the GEMV start streaming weights right away
-    __shared__ float red[8][3][8];
-    const int dbg = xp.dbg;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && dbg == 5) {
-        // previous launch's GEMV end (complete: stream order), then this start
-        g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 104] = g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102];
-        DBG_KSTAMP(100);
-    }
+    constexpr bool X2 = DT == SFMP_F32;
+    pdl_launch_dependents();
+    __shared__ float red[8][8];
     const int n_b = xp.n_b;
-    const int NT = RecGeom{xp.M}.nt_count();  // per launch (its linears share the n-tile count)
-    const int CH = n_b >> 7;  // 1..8 (host: 8 % CH == 0)
+    const int NT = RecGeom{xp.M, X2}.nt_count();
+    const int CH = n_b >> 7;  // 1..2
     const int warp = threadIdx.x >> 5, c = warp % CH;
     int w = blockIdx.x * (8 / CH) + warp / CH;  // item
     int li = 0;
@@ -331,23 +389,20 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     const XLin& XL = xp.lin[li];
     w -= XL.warp0;
     const int M = XL.M;
-    const uint32_t rec_bytes = XL.rec_bytes;
-    const RecGeom G{M};
+    const RecGeom G{M, X2};
     const int BC = XL.BC, cols = XL.cols;
-    const void* x = XL.x;
-    const uint32_t* col_perm = XL.col_perm;
-    uint8_t* xrec = XL.xrec;
-    const int lo = XL.lo;
     const bool item_ok = w < BC * NT;
     const int bc = w / NT, nt = w - bc * NT;
     const int lane = threadIdx.x & 31, q = lane & 3, n = lane >> 2;
     const int t = nt * 8 + n;
-    const bool live = item_ok && n < G.mnt(nt);
-    uint8_t* rec = xrec + static_cast<size_t>(bc) * rec_bytes;
-    float xs = 0.f, bias_lo = 0.f, bias_hi = 0.f;
+    const bool live = item_ok && t < M;
+    uint8_t* rec = XL.xrec + static_cast<size_t>(bc) * XL.rec_bytes;
+    const int e = live ? static_cast<int>(XL.escale[t]) : 0;
+    const float2 sc = pow2_pair(-e);
+    float xs = 0.f;
     if (item_ok) {
-        const uint4 idx4 =
-            ldg_keep_v4(reinterpret_cast<const uint4*>(col_perm + bc * n_b + c * 128) + lane, policy_evict_last());
+        const uint4 idx4 = ldg_keep_v4(reinterpret_cast<const uint4*>(XL.col_perm + bc * n_b + c * 128) + lane,
+                                       policy_evict_last());
         uint32_t gi[32];
 #pragma unroll
         for (int s8 = 0; s8 < 8; ++s8) {
@@ -356,157 +411,124 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int wk = 4 * (2 * (s8 & 1) + j) + a + 16 * e;
-                    gi[s8 * 4 + j * 2 + e] = __shfl_sync(0xffffffffu, comp, 8 * q + (wk >> 2));
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const int wk = 4 * (2 * (s8 & 1) + j) + a + 16 * e2;
+                    gi[s8 * 4 + j * 2 + e2] = __shfl_sync(0xffffffffu, comp, 8 * q + (wk >> 2));
                 }
         }
         if (live) {
-            const size_t rowoff = static_cast<size_t>(t) * cols;
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = load_x<DT>(x, rowoff + gi[e]);
+            using T = typename XT<DT>::T;
+            const T* xrow = static_cast<const T*>(XL.x) + static_cast<size_t>(t) * cols;
 #pragma unroll
             for (int s8 = 0; s8 < 8; ++s8) {
-                uint2 st;
-                st.x = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 0], v[s8 * 4 + 1]));
-                st.y = h2_as_u32(__floats2half2_rn(v[s8 * 4 + 2], v[s8 * 4 + 3]));
-                *reinterpret_cast<uint2*>(rec + G.frag_off(c, nt, s8, n, q)) = st;
-                // st.x pairs with A register 2*s8, st.y with 2*s8+1; each carries the
-                // magic of its register in the repacked layout of a lo / lo+1 bit
-                // unit (0 for the exact >4-bit path).  The bias uses the f16-rounded
-                // values the MMA sees.
-                const float sx = __low2float(u32_as_h2(st.x)) + __high2float(u32_as_h2(st.x));
-                const float sy = __low2float(u32_as_h2(st.y)) + __high2float(u32_as_h2(st.y));
-                auto mag = [](int B, int j) { return B <= 4 ? rp_magic(B, j) : 0.f; };
-                bias_lo += mag(lo, 2 * s8) * sx + mag(lo, 2 * s8 + 1) * sy;
-                bias_hi += mag(lo + 1, 2 * s8) * sx + mag(lo + 1, 2 * s8 + 1) * sy;
-            }
+                float v[4];
 #pragma unroll
-            for (int e = 0; e < 32; ++e) xs += v[e];
+                for (int k = 0; k < 4; ++k) v[k] = XT<DT>::f(xrow[gi[s8 * 4 + k]]) * sc.x * sc.y;
+                write_fragments<X2>(rec, G, c, t, q, s8, v, XL.lo, XL.nl, XL.sec_bytes);
+                xs += (v[0] + v[1]) + (v[2] + v[3]);
+            }
         }
         xs += __shfl_xor_sync(0xffffffffu, xs, 1);
         xs += __shfl_xor_sync(0xffffffffu, xs, 2);
-        bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 1);
-        bias_lo += __shfl_xor_sync(0xffffffffu, bias_lo, 2);
-        bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 1);
-        bias_hi += __shfl_xor_sync(0xffffffffu, bias_hi, 2);
     }
     if (CH > 1) {
-        if (q == 0) {
-            red[warp][0][n] = xs;
-            red[warp][1][n] = bias_lo;
-            red[warp][2][n] = bias_hi;
-        }
+        if (q == 0) red[warp][n] = xs;
         __syncthreads();
         if (c != 0) return;
         if (q == 0) {
-            xs = bias_lo = bias_hi = 0.f;
-            for (int k = 0; k < CH; ++k) {
-                xs += red[warp + k][0][n];
-                bias_lo += red[warp + k][1][n];
-                bias_hi += red[warp + k][2][n];
-            }
+            xs = 0.f;
+            for (int k = 0; k < CH; ++k) xs += red[warp + k][n];
         }
     }
     if (item_ok && q == 0) {
-        float* xg = reinterpret_cast<float*>(rec + G.xg_off(CH));
-        const int tt = nt * 8 + n;
-        xg[tt] = live ? xs : 0.f;
-        xg[bias_slot(tt, 0)] = xg[bias_slot(tt, 0) + 2] = live ? -bias_lo : 0.f;
-        xg[bias_slot(tt, 1)] = xg[bias_slot(tt, 1) + 2] = live ? -bias_hi : 0.f;
+        const float2 ys = pow2_pair(e);
+        for (int l = 0; l < XL.nl; ++l) {
+            float* xg = reinterpret_cast<float*>(rec + l * XL.sec_bytes + G.xg_off(CH));
+            xg[t] = live ? xs : 0.f;
+            xg[kYsIdx + t] = live ? ys.x : 0.f;
+            xg[kYsIdx + 16 + t] = live ? ys.y : 0.f;
+        }
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) DBG_KSTAMP(101);
 }
 
-// One 128-column chunk of a unit for this warp's 32 rows (2 m16 tiles), four
-// independent accumulator chains (m-tile x even/odd k-step).  prow / xb are
-// 32-bit shared addresses; all other offsets are compile-time immediates.
-template <int B, int NT, int CH>
-__device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[NT], int chunk_bytes, int c,
+// One 128-column chunk of a unit for this warp's 32 rows (2 m16 tiles).
+// prow / xb are 32-bit shared addresses; all other offsets are immediates or
+// per-linear constants.  X2: the lo B fragments (lo_off further) are
+// contracted into the same accumulators.
+template <int B, int NT, bool X2>
+__device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[NT], uint32_t lo_off, int nb8,
                                            float (&cacc)[kMT][NT][4]) {
-    constexpr int NB8 = CH * 16;   // bytes of one row of one plane
-    constexpr int PS = kTR * NB8;  // bytes of one plane of the unit
+    const int PS = kTR * nb8;  // bytes of one plane of the unit
     // rows r0 + 8*r: (r0, r0+8) is m-tile 0, (r0+16, r0+24) m-tile 1
     uint32_t p[2 * kMT][B];
 #pragma unroll
     for (int i = 0; i < B; ++i)
 #pragma unroll
-        for (int r = 0; r < 2 * kMT; ++r) p[r][i] = lds_u32(prow + i * PS + r * 8 * NB8 + c * 16);
+        for (int r = 0; r < 2 * kMT; ++r) p[r][i] = lds_u32(prow + i * PS + r * 8 * nb8);
     uint32_t A[2 * kMT][16];
 #pragma unroll
     for (int r = 0; r < 2 * kMT; ++r) {
-        if constexpr (B <= 4) unpack_rp<B>(p[r], A[r]);  // repacked layout (repack.cuh)
-        else unpack_word<B>(p[r], A[r]);                // bit planes, exact codes
+        if constexpr (B <= 4) unpack_rp_sub<B>(p[r], A[r]);  // repacked layout (repack.cuh)
+        else unpack_word_sub<B>(p[r], A[r]);                // bit planes (unpack.cuh)
     }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const uint2 b = lds_v2(xb[nt] + c * chunk_bytes + s * 32);
+            const uint2 b = lds_v2(xb[nt] + s * 32);
+            uint2 bl;
+            if constexpr (X2) bl = lds_v2(xb[nt] + lo_off + s * 32);
 #pragma unroll
-            for (int m = 0; m < kMT; ++m)
+            for (int m = 0; m < kMT; ++m) {
                 mma_16816(cacc[m][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
                           A[2 * m + 1][2 * s + 1], b.x, b.y);
+                if constexpr (X2)
+                    mma_16816(cacc[m][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
+                              A[2 * m + 1][2 * s + 1], bl.x, bl.y);
+            }
         }
     }
 }
 
-// LO = the model's floor bit-width: every unit has LO or LO+1 bits
-// (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
-// two unpack paths and its hot loop stays resident in the instruction cache.
-// Work split: all units of all linears form one sequence (linear, row tile,
-// block column); CTA b streams units [b*Q, (b+1)*Q) -- equal work per CTA,
-// one wave.  A CTA's range is cut into segments at row-tile boundaries; a
-// row tile covered by several CTAs is reduced split-K style (part k of the
-// tile = the k-th CTA that touches it, summed in k order).
-struct Seg {
-    int li, rt, bc0, bc1;  // units [bc0, bc1) of row tile rt of linear li
-    int k, C;              // this CTA is the k-th of the C CTAs touching the tile
-};
-__device__ __forceinline__ Seg seg_at(const Params& p, int64_t u, int64_t end) {
-    int li = 0;
-    while (li + 1 < p.nlin && u >= p.lin[li + 1].unit0) ++li;
-    const Lin& L = p.lin[li];
-    const int64_t rel = u - L.unit0;
-    Seg sg;
-    sg.li = li;
-    sg.rt = static_cast<int>(rel / L.BC);
-    sg.bc0 = static_cast<int>(rel - static_cast<int64_t>(sg.rt) * L.BC);
-    const int64_t t0 = L.unit0 + static_cast<int64_t>(sg.rt) * L.BC, t1 = t0 + L.BC;  // tile's unit range
-    sg.bc1 = static_cast<int>((end < t1 ? end : t1) - t0);
-    const int64_t c0 = t0 / p.Q, c1 = (t1 - 1) / p.Q;
-    sg.C = static_cast<int>(c1 - c0 + 1);
-    sg.k = static_cast<int>(static_cast<int64_t>(blockIdx.x) - c0);
-    return sg;
+// Producer waits for a free stage: suspend in the barrier (woken by the
+// phase completion) instead of spinning -- a spinning producer took ~20 % of
+// the SM's issue slots from the compute warps (ncu source counts, round 1).
+#ifndef SFMP_PROD_IDLE
+#define SFMP_PROD_IDLE 1
+#endif
+__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
+    if (!SFMP_PROD_IDLE) {
+        mbar_wait_a(bar, parity);
+        return;
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAITI_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITI_%=;\n\t}" ::"r"(bar),
+        "r"(parity), "r"(1000000u)
+        : "memory");
 }
 
 // LO = the model's floor bit-width: every unit has LO or LO+1 bits
 // (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
 // two unpack paths and its hot loop stays resident in the instruction cache.
-template <int NT, int CH, int LO>
+template <int NT, int CH, int LO, bool X2>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const Params p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + S;
-    uint8_t* zeros = smem + 256;                               // 256 B: B fragments of absent tokens
-    uint32_t* sbits = reinterpret_cast<uint32_t*>(smem + 512);  // bit-width of the unit in stage s
-    uint32_t* flag = reinterpret_cast<uint32_t*>(smem + 640);    // "this CTA finishes the tile"
+    uint8_t* zeros = smem + 256;                          // 256 B: B fragments of absent tokens
+    uint4* sinfo = reinterpret_cast<uint4*>(smem + 512);  // [S] stage info
+    const uint8_t** pend_src = reinterpret_cast<const uint8_t**>(smem + 768);  // [S] producer only
     uint8_t* wbase = smem + kHdrBytes;
     uint8_t* xbase = wbase + static_cast<size_t>(S) * p.stage_w;
+    constexpr int nb8 = CH * 16;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int dbg = p.debug_mode;
-    // a programmatic dependent (only ever the next launch of the same grouped
-    // call, whose problems are independent of ours) may start now
+    // a programmatic dependent (the fix-up of this launch, or the next launch
+    // of the same grouped call, whose problems are independent of ours) may
+    // start now: it waits for this grid's completion before it reads our data
     pdl_launch_dependents();
-    if (threadIdx.x == 0) DBG_STAMP(0);
-    if (threadIdx.x == 0 && dbg == 5 && blockIdx.x < kDbgCtas - 1) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_dbg_timeline[blockIdx.x * kDbgSlots + 123] = smid;
-    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -517,188 +539,201 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     }
     if (threadIdx.x < 64) reinterpret_cast<uint32_t*>(zeros)[threadIdx.x] = 0u;
     __syncthreads();
-
-    constexpr int nb8 = CH * 16;
+#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
+    unsigned n_claimed = 0;
+    if (threadIdx.x == 0) TL_K(1, true);
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_gemv_tl[blockIdx.x * 4 + 0] = tl_now();
+        g_gemv_tl[blockIdx.x * 4 + 2] = smid;
+    }
+#endif
 
     if (warp == 0) {
-        // ---------------- producer: one bulk copy per unit (+ its activation record) ----
+        // ---------------- producer: claims items, one bulk copy per unit (+ its record section) ----
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             const uint64_t keep = policy_evict_last();
             const uint32_t pbytes = kTR * nb8;
-            int gi = 0;  // unit counter of this CTA (debug stamps)
-            auto issue_w = [&](int s, const Lin& L, uint64_t d) {
-                const int bits = static_cast<int>((d >> 48) & 0xF);
-                sbits[s] = static_cast<uint32_t>(bits);  // published by the arrive below
-                DBG_USTAMP(2 + 3 * gi);
-                const uint32_t wbytes = 4 * kTR + bits * pbytes;
-                mbar_arrive_expect_tx(&full[s], wbytes + L.rec_bytes);
-                bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
-                         &full[s], pol);
-            };
-            auto issue_x = [&](int s, const Lin& L, int bc_) {
+            int s = 0, ph = 0;
+            bool released = false;  // griddepcontrol.wait done: records may be copied
+            int npend = 0;          // stages 0..npend-1 wait for their records (source in pend_src)
+            auto issue_x = [&](int st, const uint8_t* src, uint32_t n) {
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_u32(xbase + static_cast<size_t>(s) * p.rec_bytes)),
-                    "l"(L.xrec + static_cast<size_t>(bc_) * L.rec_bytes), "r"(L.rec_bytes), "r"(smem_u32(&full[s]))
+                        smem_u32(xbase + static_cast<size_t>(st) * p.sec_bytes)),
+                    "l"(src), "r"(n), "r"(smem_u32(&full[st]))
                     : "memory");
             };
-            int s = 0, ph = 0;
-            bool first = true;
-            const int64_t uend = min(p.units, (static_cast<int64_t>(blockIdx.x) + 1) * p.Q);
-            for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.Q; u < uend;) {
-                const Seg I = seg_at(p, u, uend);
-                u += I.bc1 - I.bc0;
-                const Lin& L = p.lin[I.li];
-                const uint64_t* gdesc = L.unit_desc + static_cast<size_t>(I.rt) * L.BC + I.bc0;
-                const int nunits = I.bc1 - I.bc0;
-                int i0 = 0;
-                if (first) {
-                    // weights of the first ring-full do not depend on x: issue them,
-                    // then wait for the activation records (programmatic dependent launch)
-                    const int pre = nunits < S ? nunits : S;
-                    uint64_t dpre[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        if (i < pre) dpre[i] = ldg_keep_u64(gdesc + i, keep);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        if (i < pre) {
-                            issue_w(i, L, dpre[i]);
-                            ++gi;
-                        }
-                    pdl_wait();
-                    for (int i = 0; i < pre; ++i) issue_x(i, L, I.bc0 + i);
-                    s = pre % S;
-                    ph = pre == S ? 1 : 0;
-                    i0 = pre;
-                    first = false;
+            // The weights of the first ring-full do not depend on x: they are
+            // issued before griddepcontrol.wait, their records after it.
+            auto release = [&]() {
+                if (released) return;
+                pdl_wait();
+                released = true;
+                for (int i = 0; i < npend; ++i) issue_x(i, pend_src[i], sinfo[i].w);
+                npend = 0;
+            };
+            unsigned item = atomicAdd(p.queue, 1u);
+            while (item < static_cast<unsigned>(p.n_items)) {
+                const unsigned next = atomicAdd(p.queue, 1u);  // claim ahead: latency overlaps this item
+                const int li = owner_of(p.item_start, p.nlin, static_cast<int>(item));
+                const Lin& L = p.lin[li];
+                const int rel = static_cast<int>(item) - L.item0;
+                const int rt = rel / L.P, seg = rel - rt * L.P;
+                const int bc0 = seg * L.L, bc1 = min(L.BC, bc0 + L.L);
+                if (SFMP_L2_PREFETCH && !released && next < static_cast<unsigned>(p.n_items)) {
+                    // While the pre-pass runs, pull the next item's weights into
+                    // L2 (the ring holds only the first few units of this one).
+                    const Lin& N = p.lin[owner_of(p.item_start, p.nlin, static_cast<int>(next))];
+                    const int rn = static_cast<int>(next) - N.item0, rtn = rn / N.P, sn = rn - rtn * N.P;
+                    const uint64_t* nd = N.unit_desc + static_cast<size_t>(rtn) * N.BC;
+                    for (int bc = sn * N.L; bc < min(N.BC, (sn + 1) * N.L); ++bc) {
+                        const uint64_t d = ldg_keep_u64(nd + bc, keep);
+                        bulk_prefetch_l2(N.payload + (d & 0xFFFFFFFFFFFFull), 4 * kTR + static_cast<uint32_t>((d >> 48) & 0xF) * pbytes);
+                    }
                 }
-                uint64_t dnext = i0 < nunits ? ldg_keep_u64(gdesc + i0, keep) : 0;
-                for (int i = i0; i < nunits; ++i) {
+                const uint64_t* gdesc = L.unit_desc + static_cast<size_t>(rt) * L.BC;
+                uint64_t dnext = ldg_keep_u64(gdesc + bc0, keep);
+                for (int bc = bc0; bc < bc1; ++bc) {
                     const uint64_t d = dnext;
-                    if (i + 1 < nunits) dnext = ldg_keep_u64(gdesc + i + 1, keep);
-                    mbar_wait(&empty[s], ph ^ 1);
-                    issue_w(s, L, d);
-                    issue_x(s, L, I.bc0 + i);
-                    ++gi;
+                    if (bc + 1 < bc1) dnext = ldg_keep_u64(gdesc + bc + 1, keep);
+                    if (!released && npend == S) release();  // ring full: records now
+                    mbar_wait_idle(smem_u32(&empty[s]), ph ^ 1);
+                    const int bits = static_cast<int>((d >> 48) & 0xF);
+                    const uint32_t fl = (bc == bc0 ? kFirst : 0u) | (bc == bc1 - 1 ? kLast : 0u);
+                    sinfo[s] = make_uint4(static_cast<uint32_t>(li) | (static_cast<uint32_t>(bits) << 8) | (fl << 16),
+                                          static_cast<uint32_t>(rt), static_cast<uint32_t>(seg), L.sec_bytes);
+                    const uint32_t wbytes = 4 * kTR + bits * pbytes;
+                    mbar_arrive_expect_tx(&full[s], wbytes + L.sec_bytes);  // publishes sinfo[s]
+                    bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
+                             &full[s], pol);
+                    // the record section of this unit's bit-width layout
+                    const uint8_t* rsrc = L.xrec + static_cast<size_t>(bc) * L.rec_bytes + (bits == L.lo ? 0u : L.sec_bytes);
+                    if (released) issue_x(s, rsrc, L.sec_bytes);
+                    else pend_src[npend++] = rsrc;  // == stage s (no wrap before the release)
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
+                item = next;
+#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
+                ++n_claimed;
+#endif
             }
+            release();
+            // end of work: one empty stage with the END flag
+            mbar_wait_idle(smem_u32(&empty[s]), ph ^ 1);
+            sinfo[s] = make_uint4(kEnd << 16, 0u, 0u, 0u);
+            mbar_arrive(&full[s]);
         }
+        __syncwarp();
     } else {
         // ---------------- compute warps ------------------------------------------
         const int cw = warp - 1;
         const int g = lane >> 2, q = lane & 3;
         const int r0 = cw * 16 * kMT + g;  // rows r0 + 8*r of the tile
-        const uint32_t stage_w = p.stage_w, rec_bytes = p.rec_bytes;
-        // per-lane shared addresses for stage 0; a stage adds s * stage_w / rec_bytes
+        const uint32_t stage_w = p.stage_w, sec_stride = p.sec_bytes;
+        // per-lane shared addresses for stage 0; a stage adds s * stage_w / sec_stride
         const uint32_t prow0 = smem_u32(wbase) + 4 * kTR + r0 * nb8 + q * 4;
         const uint32_t sz0 = smem_u32(wbase) + 2 * r0;
-        // record addresses depend on the linear's M: set per segment
-        int chunk_bytes = 0, cur_li = -1;
-        uint32_t xb0[NT], xstep[NT], xg0 = 0, bc_a = 0;
-        const uint32_t sbits_a = smem_u32(sbits);
+        const uint32_t sinfo_a = smem_u32(sinfo);
         const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
-        int s = 0, ph = 0, gi = 0;
+        // record addresses depend on the linear's M: set when the linear changes
+        int chunk_bytes = 0, cur_li = -1;
+        uint32_t lo_off = 0, live_mask = 0;
+        uint32_t xb0[NT], xg0 = 0;
+        float yacc[kMT][NT][4];
+        float ysa[NT][2], ysb[NT][2];
+        int s = 0, ph = 0;
         uint32_t wo = 0, xo = 0;  // byte offsets of stage s in the weight / record rings
-        const int64_t uend = min(p.units, (static_cast<int64_t>(blockIdx.x) + 1) * p.Q);
-        for (int64_t u = static_cast<int64_t>(blockIdx.x) * p.Q; u < uend;) {
-            const Seg I = seg_at(p, u, uend);
-            u += I.bc1 - I.bc0;
-            const Lin& L = p.lin[I.li];
-            const int C = I.C, rt = I.rt, nunits = I.bc1 - I.bc0;
-            if (I.li != cur_li) {
-                cur_li = I.li;
-                const RecGeom GL{L.M};
+        for (;;) {
+            mbar_wait_a(full_a + 8 * s, ph);
+            const uint4 info = lds_v4(sinfo_a + 16 * s);
+            const uint32_t fl = info.x >> 16;
+            if (fl & kEnd) break;
+            const int li = static_cast<int>(info.x & 0xFF), bits = static_cast<int>((info.x >> 8) & 0xFF);
+            if (li != cur_li) {
+                cur_li = li;
+                const Lin& L = p.lin[li];
+                const RecGeom GL{L.M, X2};
                 chunk_bytes = GL.chunk_bytes();
+                lo_off = L.lo_off;
+                live_mask = 0;
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
-                    const bool live = g < GL.mnt(nt);
-                    xb0[nt] = live ? smem_u32(xbase) + GL.lane_off(0, nt, g, q) : smem_u32(zeros) + q * 8;
-                    xstep[nt] = live ? rec_bytes : 0u;
+                    const bool live = nt * 8 + g < L.M;
+                    live_mask |= live ? 1u << nt : 0u;
+                    xb0[nt] = live ? smem_u32(xbase) + GL.run_off(0, nt * 8 + g, q) : smem_u32(zeros) + q * 8;
                 }
                 xg0 = smem_u32(xbase) + GL.xg_off(CH) + 8 * q;
-                bc_a = smem_u32(xbase) + GL.xg_off(CH) + 64 + 16 * q;  // accumulator inits
             }
-            float yacc[kMT][NT][4];
-#pragma unroll
-            for (int m = 0; m < kMT; ++m)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
-            for (int i = 0; i < nunits; ++i, ++gi) {
-                mbar_wait_a(full_a + 8 * s, ph);
-                if (cw == 0 && lane == 0) DBG_USTAMP(3 + 3 * gi);
-                const int bits = static_cast<int>(lds_u32(sbits_a + 4 * s));
-                uint32_t xb[NT];
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + (xstep[nt] ? xo : 0u);
-                const uint32_t prow = prow0 + wo;
-                // accumulators start at -bias (this unit's layout): C - bias from the MMA
-                const uint32_t xg = xg0 + xo;
-                const uint32_t binit = bc_a + xo + (bits == LO ? 0u : 128u);
-                float cacc[kMT][NT][4];
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const uint4 b4 = lds_v4(binit + 64 * nt);
-#pragma unroll
-                    for (int h = 0; h < kMT; ++h) {
-                        cacc[h][nt][0] = __uint_as_float(b4.x);
-                        cacc[h][nt][1] = __uint_as_float(b4.y);
-                        cacc[h][nt][2] = __uint_as_float(b4.z);
-                        cacc[h][nt][3] = __uint_as_float(b4.w);
-                    }
-                }
-#pragma unroll
-                for (int c = 0; c < CH; ++c) {
-                    if (bits == LO) {
-                        unit_chunk<LO, NT, CH>(prow, xb, chunk_bytes, c, cacc);
-                    } else if constexpr (LO < 8) {
-                        unit_chunk<LO + 1, NT, CH>(prow, xb, chunk_bytes, c, cacc);
-                    }
-                }
-                // per-row affine of this block: y += s*(C - bias) + z*Xg
-                const uint32_t sz = sz0 + wo;
-#pragma unroll
-                for (int m = 0; m < kMT; ++m) {
-                    const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
-                    const float za = lds_h2f(sz + 2 * kTR + 32 * m), zb = lds_h2f(sz + 2 * kTR + 32 * m + 16);
-#pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
-                        const float2 xg01 = lds_f2(xg + 32 * nt);
-                        const float* c0 = cacc[m][nt];  // = C - bias
-                        yacc[m][nt][0] = fmaf(sa, c0[0], fmaf(za, xg01.x, yacc[m][nt][0]));
-                        yacc[m][nt][1] = fmaf(sa, c0[1], fmaf(za, xg01.y, yacc[m][nt][1]));
-                        yacc[m][nt][2] = fmaf(sb, c0[2], fmaf(zb, xg01.x, yacc[m][nt][2]));
-                        yacc[m][nt][3] = fmaf(sb, c0[3], fmaf(zb, xg01.y, yacc[m][nt][3]));
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive_a(empty_a + 8 * s);
-                if (cw == 0 && lane == 0) DBG_USTAMP(4 + 3 * gi);
-                wo += stage_w;
-                xo += rec_bytes;
-                if (++s == S) { s = 0; ph ^= 1; wo = 0; xo = 0; }
-            }
-            if (C == 1) {
-                // whole row tile in this item: un-permuted store straight to y
+            if (fl & kFirst) {
 #pragma unroll
                 for (int m = 0; m < kMT; ++m)
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int t = nt * 8 + 2 * q + (e & 1);
-                            if (t < L.M)
-                                L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + r0 + 16 * m + 8 * (e >> 1))] =
-                                    yacc[m][nt][e];
-                        }
-                continue;
+                        for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {  // output scale of tokens nt*8+2q, +1
+                    const float2 a = lds_f2(xg0 + xo + 4 * kYsIdx + 32 * nt);
+                    const float2 b = lds_f2(xg0 + xo + 4 * (kYsIdx + 16) + 32 * nt);
+                    ysa[nt][0] = a.x;
+                    ysa[nt][1] = a.y;
+                    ysb[nt][0] = b.x;
+                    ysb[nt][1] = b.y;
+                }
             }
-            // split-K partial tile [t][128 rows] of this item (coalesced rows)
-            float* part = L.part + (static_cast<size_t>(rt) * kMaxSplit + I.k) * (16 * kTR);
+            uint32_t xb[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + ((live_mask >> nt) & 1u ? xo : 0u);
+            const uint32_t prow = prow0 + wo;
+            float cacc[kMT][NT][4];
+#pragma unroll
+            for (int m = 0; m < kMT; ++m)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) cacc[m][nt][e] = 0.f;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                uint32_t xbc[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) xbc[nt] = xb[nt] + ((live_mask >> nt) & 1u ? c * chunk_bytes : 0);
+                if (bits == LO) {
+                    unit_chunk<LO, NT, X2>(prow + c * 16, xbc, lo_off, nb8, cacc);
+                } else if constexpr (LO < 8) {
+                    unit_chunk<LO + 1, NT, X2>(prow + c * 16, xbc, lo_off, nb8, cacc);
+                }
+            }
+            // per-row affine of this block: y += s*C + z*Xg
+            const uint32_t sz = sz0 + wo, xg = xg0 + xo;
+#pragma unroll
+            for (int m = 0; m < kMT; ++m) {
+                const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
+                const float za = lds_h2f(sz + 2 * kTR + 32 * m), zb = lds_h2f(sz + 2 * kTR + 32 * m + 16);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const float2 xg01 = lds_f2(xg + 32 * nt);
+                    const float* c0 = cacc[m][nt];
+                    yacc[m][nt][0] = fmaf(sa, c0[0], fmaf(za, xg01.x, yacc[m][nt][0]));
+                    yacc[m][nt][1] = fmaf(sa, c0[1], fmaf(za, xg01.y, yacc[m][nt][1]));
+                    yacc[m][nt][2] = fmaf(sb, c0[2], fmaf(zb, xg01.x, yacc[m][nt][2]));
+                    yacc[m][nt][3] = fmaf(sb, c0[3], fmaf(zb, xg01.y, yacc[m][nt][3]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(empty_a + 8 * s);
+            wo += stage_w;
+            xo += sec_stride;
+            if (++s == S) { s = 0; ph ^= 1; wo = 0; xo = 0; }
+            if (!(fl & kLast)) continue;
+
+            // ---- end of a segment: scale back by 2^e_t (exact), store y or the partial ----
+            const Lin& L = p.lin[li];
+            const int rt = static_cast<int>(info.y), seg = static_cast<int>(info.z);
+            const bool whole = L.P == 1;
+            float* dst = whole ? L.y : L.part + (static_cast<size_t>(rt) * L.P + seg) * (16 * kTR);
 #pragma unroll
             for (int m = 0; m < kMT; ++m)
 #pragma unroll
@@ -706,132 +741,158 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int t = nt * 8 + 2 * q + (e & 1);
-                        if (t < L.M) part[t * kTR + r0 + 16 * m + 8 * (e >> 1)] = yacc[m][nt][e];
+                        if (t >= L.M) continue;
+                        const float v = (yacc[m][nt][e] * ysa[nt][e & 1]) * ysb[nt][e & 1];
+                        const int row = r0 + 16 * m + 8 * (e >> 1);
+                        if (whole) dst[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = v;  // un-permuted
+                        else dst[t * kTR + row] = v;  // [t][128 rows], coalesced
                     }
-            // Deterministic split-K: the last of the C items of this row tile
-            // sums the partials in split order and stores them un-permuted.
-            // Compute warps only (the producer streams on): named barrier 1.
-            named_bar_sync(1, kNCW * 32);  // every partial store precedes the release below
-            if (threadIdx.x == 32) DBG_STAMP(124);
-            if (threadIdx.x == 32) {
-                const unsigned old = atomic_add_acq_rel_gpu(L.counters + rt, 1u);
-                *flag = (old == static_cast<unsigned>(C - 1)) ? 1u : 0u;
-            }
-            named_bar_sync(1, kNCW * 32);
-            if (threadIdx.x == 32) DBG_STAMP(125);
-            if (*flag) {
-                // Acquire by thread 32 (it also invalidates this SM's L1) + the
-                // barrier order these plain loads after every partial store
-                // (the semaphore pattern).  Weak loads: a strong ld.cg is
-                // issued one at a time.
-                // One row per thread, all tokens; RB splits per round so that
-                // RB*8*NT loads are in flight together (latency, not bandwidth).
-                static_assert(kNCW * 32 >= kTR, "fixup maps one compute thread per row");
-                constexpr int RB = NT == 1 ? 4 : 2;
-                const int row = threadIdx.x - 32;
-                if (row < kTR) {
-                const float* pp = L.part + static_cast<size_t>(rt) * kMaxSplit * (16 * kTR) + row;
-                const uint32_t orow = __ldg(L.out_map + rt * kTR + row);
-                float acc[8 * NT];
-#pragma unroll
-                for (int t = 0; t < 8 * NT; ++t) acc[t] = 0.f;
-                for (int r0 = 0; r0 < C; r0 += RB) {
-                    float v[RB][8 * NT];
-#pragma unroll
-                    for (int r = 0; r < RB; ++r)
-#pragma unroll
-                        for (int t = 0; t < 8 * NT; ++t)
-                            v[r][t] = (r0 + r < C && t < L.M)
-                                          ? pp[static_cast<size_t>(r0 + r) * (16 * kTR) + t * kTR]
-                                          : 0.f;
-#pragma unroll
-                    for (int r = 0; r < RB; ++r)
-#pragma unroll
-                        for (int t = 0; t < 8 * NT; ++t)
-                            if (r0 + r < C) acc[t] += v[r][t];  // split order, as the partials were cut
-                }
-#pragma unroll
-                for (int t = 0; t < 8 * NT; ++t)
-                    if (t < L.M) L.y[t * L.out_rows + orow] = acc[t];
-                }
-                if (threadIdx.x == 32) L.counters[rt] = 0u;  // ready for the next call (stream-ordered)
-                if (threadIdx.x == 32) DBG_STAMP(126);
-            }
         }
     }
-    if (threadIdx.x == 0) DBG_STAMP(1);
-    if (threadIdx.x == 32) DBG_STAMP(127);
-    if (dbg == 5 && threadIdx.x == 32) {  // kernel-level: max end over all CTAs (compute warps)
-        atomicMax(&g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 102], gtimer());
-        if (blockIdx.x == gridDim.x - 1) g_dbg_timeline[(kDbgCtas - 1) * kDbgSlots + 103] = gridDim.x;
+    // the last CTA out resets the work queue for the next call (stream-ordered)
+    __syncthreads();
+#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {
+        g_gemv_tl[blockIdx.x * 4 + 1] = tl_now();
+        g_gemv_tl[blockIdx.x * 4 + 3] = n_claimed;
+    }
+    if (threadIdx.x == 0) TL_K(1, false);
+#endif
+    if (threadIdx.x == 0) {
+        const unsigned done = atomicAdd(p.queue + 1, 1u);
+        if (done == gridDim.x - 1) {
+            p.queue[0] = 0u;
+            p.queue[1] = 0u;
+        }
     }
 }
 
-template <int NT, int CH, int LO>
-cudaError_t launch_k(cudaLaunchConfig_t& cfg, const Params& p) {
-    auto k = gemv_kernel<NT, CH, LO>;
-    static int configured[64] = {0};
+// Split-tile fix-up (programmatic dependent of the GEMV).  Work = (tile,
+// token) pairs of every multi-segment linear (fix_start prefix), 128 threads
+// (the tile's rows) per pair; persistent CTAs of 8 groups walk the pairs two
+// at a time so that 2 x P loads per thread are in flight.  The P segment
+// partials are added in segment order -- the canonical order -- and stored
+// un-permuted.
+__global__ void __launch_bounds__(8 * kTR) gemv_fixup_kernel(const Params p) {
+    pdl_launch_dependents();  // a later launch of the same grouped call may start its pre-pass
+    const int row = threadIdx.x & (kTR - 1);
+    const int stride = static_cast<int>(gridDim.x) * 8;
+    int w = static_cast<int>(blockIdx.x) * 8 + static_cast<int>(threadIdx.x >> 7);
+    pdl_wait();  // the GEMV grid has completed and its partials are visible
+    if (threadIdx.x == 0) TL_K(2, true);
+    for (; w < p.n_fix; w += 2 * stride) {
+        const float* pp[2];
+        float* yp[2];
+        int P[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int wh = w + h * stride;
+            P[h] = 0;
+            if (wh >= p.n_fix) continue;
+            const Lin& L = p.lin[owner_of(p.fix_start, p.nlin, wh)];
+            const int rel = wh - L.fix0, rt = rel / L.M, t = rel - rt * L.M;
+            P[h] = L.P;
+            pp[h] = L.part + static_cast<size_t>(rt) * L.P * (16 * kTR) + t * kTR + row;
+            yp[h] = L.y + static_cast<size_t>(t) * L.out_rows + __ldg(L.out_map + rt * kTR + row);
+        }
+        float acc[2] = {0.f, 0.f};
+        const int Pm = max(P[0], P[1]);
+        for (int k0 = 0; k0 < Pm; k0 += 16) {
+            float v[2][16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (k0 + k < P[h]) v[h][k] = __ldg(pp[h] + (k0 + k) * (16 * kTR));  // previous grid's data
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (k0 + k < P[h]) acc[h] += v[h][k];  // segment order
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if (P[h]) *yp[h] = acc[h];
+    }
+    if (threadIdx.x == 0) TL_K(2, false);
+}
+
+#ifndef SFMP_GEMV_TIMELINE
+#define SFMP_GEMV_TIMELINE 0
+#endif
+#if SFMP_GEMV_TIMELINE
+}  // namespace
+extern "C" int sfmp_debug_gemv_timeline(unsigned long long* host, size_t n) {
+    if (n > 4096 * 4 + 16) n = 4096 * 4 + 16;
+    cudaError_t e = cudaMemcpyFromSymbol(host, g_gemv_tl, n * sizeof(unsigned long long));
+    unsigned long long init[16];
+    for (int i = 0; i < 16; ++i) init[i] = (i & 1) ? 0ull : ~0ull;
+    cudaMemcpyToSymbol(g_gemv_tl, init, sizeof(init), 4096 * 4 * sizeof(unsigned long long));
+    return static_cast<int>(e);
+}
+namespace {
+#endif
+
+// One-time (per device, thread-safe) function attribute setup.
+template <class F>
+void once_per_device(std::once_flag* flags, F&& f) {
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_per_cta(NT));
-        if (e != cudaSuccess) return e;
-        configured[dev] = 1;
-    }
+    if (dev < 0 || dev >= 64) dev = 0;
+    std::call_once(flags[dev], f);
+}
+
+template <int NT, int CH, int LO, bool X2>
+cudaError_t launch_k(cudaLaunchConfig_t& cfg, const Params& p) {
+    auto k = gemv_kernel<NT, CH, LO, X2>;
+    static std::once_flag fl[64];
+    static cudaError_t err[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    once_per_device(fl, [&] { err[dev & 63] = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
+    if (err[dev & 63] != cudaSuccess) return err[dev & 63];
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
-template <int NT, int CH>
+template <int NT, int CH, bool X2>
 cudaError_t launch_nc(cudaLaunchConfig_t& cfg, const Params& p, int lo) {
     switch (lo) {
-        case 1: return launch_k<NT, CH, 1>(cfg, p);
-        case 2: return launch_k<NT, CH, 2>(cfg, p);
-        case 3: return launch_k<NT, CH, 3>(cfg, p);
-        case 4: return launch_k<NT, CH, 4>(cfg, p);
-        case 5: return launch_k<NT, CH, 5>(cfg, p);
-        case 6: return launch_k<NT, CH, 6>(cfg, p);
-        case 7: return launch_k<NT, CH, 7>(cfg, p);
-        default: return launch_k<NT, CH, 8>(cfg, p);
+        case 1: return launch_k<NT, CH, 1, X2>(cfg, p);
+        case 2: return launch_k<NT, CH, 2, X2>(cfg, p);
+        case 3: return launch_k<NT, CH, 3, X2>(cfg, p);
+        case 4: return launch_k<NT, CH, 4, X2>(cfg, p);
+        case 5: return launch_k<NT, CH, 5, X2>(cfg, p);
+        case 6: return launch_k<NT, CH, 6, X2>(cfg, p);
+        case 7: return launch_k<NT, CH, 7, X2>(cfg, p);
+        default: return launch_k<NT, CH, 8, X2>(cfg, p);
     }
 }
 
 template <sfmp_dtype DT>
-cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems, int max_cols, int grid, size_t smem, int lo,
-                     cudaStream_t st, bool overlap_prev) {
+cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems, int max_cols, int grid, size_t smem,
+                     int lo, cudaStream_t st, bool overlap_prev) {
+    constexpr bool X2 = DT == SFMP_F32;
     const size_t elem = DT == SFMP_F32 ? 4 : 2;
     // K4: activation records (normal launch: it overwrites the workspace the
     // previous call may still read, and x may be that call's output, so it
-    // follows it in stream order).  Measured: chaining it programmatically
-    // lets the next GEMV's CTAs occupy slots early and slows both calls.
-    const int NT = p.M > 8 ? 2 : 1;
-    {
-        // Same shared-memory carveout as the GEMV: an SM running a pre-pass CTA
-        // then needs no reconfiguration (which waits for the SM to drain)
-        // before the GEMV's CTAs can join it.
-        static int configured[64] = {0};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 64 && !configured[dev]) {
-            cudaFuncSetAttribute(xprep_kernel<DT>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
-            configured[dev] = 1;
-        }
-    }
+    // follows it in stream order).
+    int maxM = 1;
+    for (int i = 0; i < xp.nlin; ++i) maxM = std::max(maxM, xp.lin[i].M);
+    const int NT = maxM > 8 ? 2 : 1;
     const size_t row_smem = static_cast<size_t>(8) * p.n_b * 4 + static_cast<size_t>(max_cols) * elem;
     if (row_smem <= static_cast<size_t>(kXprepRowLimit)) {
-        static int configured_rows[64] = {0};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev < 64 && !configured_rows[dev]) {
+        static std::once_flag fl[64];
+        once_per_device(fl, [] {
             cudaFuncSetAttribute(xprep_rows_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXprepRowLimit);
+            // same carveout as the GEMV: an SM running a pre-pass CTA needs no
+            // reconfiguration before the GEMV's CTAs can join it
             cudaFuncSetAttribute(xprep_rows_kernel<DT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
-            configured_rows[dev] = 1;
-        }
+        });
         // overlap_prev: a later launch of one grouped call (independent problems,
         // workspaces disjoint from the earlier launches'): the pre-pass may start
-        // while the previous GEMV still runs (it never waits on it), and this
-        // call's GEMV then fills the previous one's tail.
+        // while the previous GEMV still runs, and this call's GEMV then fills the
+        // previous one's tail.
         cudaLaunchAttribute a[1];
         a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         a[0].val.programmaticStreamSerializationAllowed = overlap_prev ? 1 : 0;
@@ -847,6 +908,7 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
         cudaError_t e = cudaLaunchKernelEx(&c, xprep_rows_kernel<DT>, xq);
         if (e != cudaSuccess) return e;
     } else {
+        if (DT != SFMP_F16) rowscale_kernel<DT><<<dim3(16, xp.nlin), 256, 0, st>>>(xp);
         const int per_cta = 8 / (p.n_b / 128);  // items per pre-pass CTA
         xprep_kernel<DT><<<(xwarps + per_cta - 1) / per_cta, 256, 0, st>>>(xp);
     }
@@ -854,7 +916,7 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
-    // K1: C CTAs per 128-row tile of every linear, programmatic dependent of xprep
+    // K1: persistent CTAs over the work queue, programmatic dependent of the pre-pass
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
@@ -866,31 +928,66 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
     const int CH = p.n_b / 128;
-    if (NT == 1) return CH == 1 ? launch_nc<1, 1>(cfg, p, lo) : launch_nc<1, 2>(cfg, p, lo);
-    return CH == 1 ? launch_nc<2, 1>(cfg, p, lo) : launch_nc<2, 2>(cfg, p, lo);
+    cudaError_t e;
+    if (NT == 1) e = CH == 1 ? launch_nc<1, 1, X2>(cfg, p, lo) : launch_nc<1, 2, X2>(cfg, p, lo);
+    else e = CH == 1 ? launch_nc<2, 1, X2>(cfg, p, lo) : launch_nc<2, 2, X2>(cfg, p, lo);
+    if (e != cudaSuccess || p.n_fix == 0) return e;
+    // split tiles: sum the segment partials (programmatic dependent of the GEMV)
+    cudaLaunchConfig_t fc{};
+    fc.gridDim = dim3(std::min((p.n_fix + 7) / 8, 2 * 148));  // <= 2 CTAs of 1024 threads per SM
+    fc.blockDim = dim3(8 * kTR);
+    fc.stream = st;
+    fc.attrs = pdl;
+    fc.numAttrs = 1;
+    return cudaLaunchKernelEx(&fc, gemv_fixup_kernel, p);
+}
+
+int units_per_segment(const DevModel& m) { return std::max(1, kSegCols / static_cast<int>(m.n_b)); }
+int segments_per_tile(const DevModel& m) {
+    const int L = units_per_segment(m);
+    return (static_cast<int>(m.BC) + L - 1) / L;
+}
+
+// Shared-memory plan of one launch: stages and resident CTAs per SM (fewer
+// CTAs when two stages of the widest unit + record section would not fit).
+struct SmemPlan {
+    int stages, ctas;
+    size_t smem;
+};
+SmemPlan smem_plan(uint32_t stage_w, uint32_t sec_bytes, int NT) {
+    for (int ctas = ctas_per_sm(NT); ctas >= 1; --ctas) {
+        const int budget = (ctas == 1 ? 227 * 1024 : kSmemSM / ctas) - kHdrBytes;
+        const int stages = std::min<int>(4, budget / static_cast<int>(stage_w + sec_bytes));
+        if (stages >= 2) return {stages, ctas, kHdrBytes + static_cast<size_t>(stages) * (stage_w + sec_bytes)};
+    }
+    return {0, 0, 0};
+}
+int layouts_of(const DevModel& m) { return m.ceil_bits > m.floor_bits ? 2 : 1; }
+uint32_t stage_bytes(const DevModel& m, int ceil_bits) {
+    return static_cast<uint32_t>((4 * kTR + ceil_bits * kTR * (m.n_b / 8) + 127) / 128 * 128);
 }
 
 }  // namespace
 
-// Not part of the ABI: copies the debug timeline (SFMP_GEMV_DEBUG=5) to the host.
-extern "C" int sfmp_debug_gemv_timeline(unsigned long long* host, size_t n) {
-    if (n > static_cast<size_t>(kDbgCtas) * kDbgSlots) n = static_cast<size_t>(kDbgCtas) * kDbgSlots;
-    return static_cast<int>(cudaMemcpyFromSymbol(host, g_dbg_timeline, n * sizeof(unsigned long long)));
-}
-
-// Workspace: activation records | split-K partials | completion counters.
+// Workspace: activation records | segment partials | queue | row exponents.
 size_t gemv_rec_bytes(const DevModel& m) {
-    return (static_cast<size_t>(m.BC) * RecGeom{16}.bytes(static_cast<int>(m.n_b / 128)) + 255) / 256 * 256;
+    const size_t rec = static_cast<size_t>(layouts_of(m)) * RecGeom{16, true}.sec_bytes(static_cast<int>(m.n_b / 128));
+    return (static_cast<size_t>(m.BC) * rec + 255) / 256 * 256;
 }
 size_t gemv_part_bytes(const DevModel& m) {
-    return static_cast<size_t>(m.RT) * kMaxSplit * 16 * kTR * 4;
+    return segments_per_tile(m) > 1 ? static_cast<size_t>(m.RT) * segments_per_tile(m) * 16 * kTR * 4 : 0;
 }
 size_t gemv_workspace_bytes(const DevModel& m, int M) {
     (void)M;
-    return gemv_rec_bytes(m) + gemv_part_bytes(m) + static_cast<size_t>(m.RT) * 4;
+    return gemv_rec_bytes(m) + gemv_part_bytes(m) + 128;  // + queue[2] | pad | exponents[16]
 }
 
 int gemv_ctas_per_sm(int NT) { return ctas_per_sm(NT); }
+
+bool gemv_feasible(const DevModel& m) {
+    return smem_plan(stage_bytes(m, m.ceil_bits), static_cast<uint32_t>(RecGeom{16, true}.sec_bytes(static_cast<int>(m.n_b / 128))), 2)
+               .stages >= 2;
+}
 
 bool gemv_groupable(const DevModel& a, const DevModel& b) {
     return a.gemv_ok && b.gemv_ok && a.n_b == b.n_b && a.floor_bits == b.floor_bits && a.device == b.device;
@@ -908,81 +1005,79 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     const int NT = M > 8 ? 2 : 1;
     for (int i = 0; i < n; ++i)
         if ((Ms[i] > 8 ? 2 : 1) != NT) return cudaErrorInvalidValue;  // one n-tile count per launch
+    const bool X2 = dt == SFMP_F32;
     const int CH = static_cast<int>(m0.n_b / 128);
     Params p{};
     XParams xp{};
     p.nlin = xp.nlin = n;
-    p.M = xp.M = M;
+    xp.M = M;
     p.n_b = xp.n_b = static_cast<int>(m0.n_b);
-    p.rec_bytes = xp.rec_bytes = static_cast<uint32_t>(RecGeom{M}.bytes(CH));  // stage stride: the largest
-    {
-        const char* dbg = getenv("SFMP_GEMV_DEBUG");
-        p.debug_mode = xp.dbg = dbg ? atoi(dbg) : 0;
-    }
-    // split-K: every CTA gets ~U units so that all linears' CTAs fit one wave
-    // of resident slots with equal work (balanced across the group)
-    int ceil_bits = 0;
-    int64_t units = 0;
-    for (int i = 0; i < n; ++i) {
-        units += static_cast<int64_t>(ms[i]->RT) * ms[i]->BC;
-        ceil_bits = std::max(ceil_bits, ms[i]->ceil_bits);
-    }
-    const int slots = m0.num_sms * ctas_per_sm(NT);
-    // One wave: G CTAs, each Q consecutive units of the group's unit sequence
-    // (Q large enough that no row tile is shared by more than kMaxSplit CTAs).
-    int max_bc = 1;
-    for (int i = 0; i < n; ++i) max_bc = std::max(max_bc, static_cast<int>(ms[i]->BC));
-    int64_t Q = std::max<int64_t>({2, (units + slots - 1) / slots, (max_bc + kMaxSplit - 2) / (kMaxSplit - 1)});
-    if (const char* e = getenv("SFMP_GEMV_Q")) Q = std::max<int64_t>(Q, atoi(e));
-    int64_t unit0 = 0;
-    int xwarps = 0, xitems = 0, max_cols = 0;
+    p.sec_bytes = static_cast<uint32_t>(RecGeom{M, X2}.sec_bytes(CH));  // stage stride: the largest
+    int ceil_bits = 0, items = 0, fix = 0, xwarps = 0, xitems = 0, max_cols = 0;
     for (int i = 0; i < n; ++i) {
         const DevModel& m = *ms[i];
+        ceil_bits = std::max(ceil_bits, m.ceil_bits);
         Lin& L = p.lin[i];
         const int BC = static_cast<int>(m.BC);
+        const RecGeom G{Ms[i], X2};
+        const int nl = layouts_of(m);
         L.payload = m.d_payload;
         L.unit_desc = m.d_unit_desc;
         L.out_map = m.d_out_map;
         L.xrec = wss[i];
         L.y = ys[i];
         L.part = reinterpret_cast<float*>(wss[i] + gemv_rec_bytes(m));
-        L.counters = reinterpret_cast<unsigned*>(wss[i] + gemv_rec_bytes(m) + gemv_part_bytes(m));
         L.out_rows = m.out_rows;
         L.BC = BC;
+        L.RT = static_cast<int>(m.RT);
         L.M = Ms[i];
-        L.rec_bytes = static_cast<uint32_t>(RecGeom{Ms[i]}.bytes(CH));
-        L.unit0 = unit0;
-        unit0 += static_cast<int64_t>(m.RT) * BC;
+        L.L = units_per_segment(m);
+        L.P = segments_per_tile(m);
+        L.sec_bytes = static_cast<uint32_t>(G.sec_bytes(CH));
+        L.rec_bytes = nl * L.sec_bytes;
+        L.lo_off = static_cast<uint32_t>(G.lo_off());
+        L.lo = m.floor_bits;
+        L.item0 = items;
+        p.item_start[i] = items;
+        p.fix_start[i] = fix;
+        items += static_cast<int>(m.RT) * L.P;
+        L.fix0 = fix;
+        if (L.P > 1) fix += static_cast<int>(m.RT) * Ms[i];  // (tile, token) fix-up pairs
+        uint8_t* tail = wss[i] + gemv_rec_bytes(m) + gemv_part_bytes(m);  // queue[4] | pad | exponents[16] | counters
         XLin& X = xp.lin[i];
         X.x = xs[i];
         X.col_perm = m.d_col_perm;
         X.xrec = wss[i];
+        X.escale = reinterpret_cast<float*>(tail + 64);
         X.BC = BC;
         X.cols = static_cast<int>(m.cols);
         X.warp0 = xwarps;
         X.item0 = xitems;
         X.lo = m.floor_bits;
+        X.nl = nl;
         X.M = Ms[i];
         X.rec_bytes = L.rec_bytes;
+        X.sec_bytes = L.sec_bytes;
         xwarps += BC * NT;
         xitems += (BC + 7) / 8 * Ms[i];  // pre-pass CTAs: (8 block columns) x tokens
         max_cols = std::max(max_cols, X.cols);
     }
-    p.stage_w = static_cast<uint32_t>((4 * kTR + ceil_bits * kTR * (m0.n_b / 8) + 127) / 128 * 128);
-    int max_stages = 4;
-    if (const char* ss = getenv("SFMP_GEMV_STAGES")) max_stages = std::max(2, atoi(ss));
-    const int fixed = kHdrBytes;
-    const int stages = std::min<int>(max_stages, (smem_per_cta(NT) - fixed) / static_cast<int>(p.stage_w + p.rec_bytes));
-    if (stages < 2) return cudaErrorInvalidConfiguration;
-    p.stages = stages;
-    const size_t smem = fixed + static_cast<size_t>(stages) * (p.stage_w + p.rec_bytes);
-    p.units = unit0;
-    p.Q = Q;
-    const int grid = static_cast<int>((unit0 + Q - 1) / Q);
+    // the launch's work queue lives in the first problem's workspace (problems
+    // of one launch have distinct workspaces)
+    p.queue = reinterpret_cast<unsigned*>(wss[0] + gemv_rec_bytes(m0) + gemv_part_bytes(m0));
+    p.n_items = items;
+    p.n_fix = fix;
+    p.item_start[n] = items;
+    p.fix_start[n] = fix;
+    p.stage_w = stage_bytes(m0, ceil_bits);
+    const SmemPlan sp = smem_plan(p.stage_w, p.sec_bytes, NT);
+    if (sp.stages < 2) return cudaErrorInvalidConfiguration;  // excluded at upload (gemv_feasible)
+    p.stages = sp.stages;
+    const int grid = std::min(items, m0.num_sms * sp.ctas);
     switch (dt) {
-        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st, overlap_prev);
-        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st, overlap_prev);
-        default: return launch_t<SFMP_BF16>(p, xp, xwarps, xitems, max_cols, grid, smem, m0.floor_bits, st, overlap_prev);
+        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
+        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
+        default: return launch_t<SFMP_BF16>(p, xp, xwarps, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
     }
 }
 

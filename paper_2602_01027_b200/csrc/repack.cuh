@@ -70,6 +70,37 @@ inline void rp_pack(const uint32_t* codes, int B, uint32_t* out) {
     }
 }
 
+// Exponent offset of register j's codes when read as f16 SUBNORMALS: with the
+// exponent field zero, mantissa bits [p, p+B) holding c give exactly
+// c * 2^(p-24), so the activation paired with register j is pre-scaled by
+// 2^(24-p) (the decode pre-pass) and the MMA contracts the exact codes with
+// no magic offset to cancel.  Wider (5..8-bit) units put c at p = 0.
+__host__ __device__ constexpr int sub_pos(int B, int j) { return B <= 4 ? rp_pos(B, j) : 0; }
+
+// Device: 16 f16x2 registers from the B repacked words, codes as subnormals
+// (one LOP3 AND per register; no magic exponent).
+template <int B>
+__device__ __forceinline__ void unpack_rp_sub(const uint32_t* w, uint32_t (&H)[16]) {
+    uint32_t sh[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) sh[i] = w[i] >> (B == 4 ? 8 : B == 3 ? 9 : 10);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if constexpr (B == 3) {
+            if (j == 15) {
+                const uint32_t t1 = (w[1] >> 14) & 0x00020002u;
+                const uint32_t t2 = lop3_and_or(w[2] >> 13, 0x00040004u, t1);
+                H[15] = lop3_and_or(w[0] >> 15, 0x00010001u, t2);
+                continue;
+            }
+        }
+        const int wi = rp_word(B, j), s = rp_shift(B, j), p = rp_pos(B, j);
+        const uint32_t src = s ? sh[wi] : w[wi];
+        const uint32_t m = ((1u << B) - 1u) << p;
+        H[j] = src & (m | (m << 16));
+    }
+}
+
 // Device: 16 f16x2 (2^(10-p_j) + c) registers from the B repacked words.
 template <int B>
 __device__ __forceinline__ void unpack_rp(const uint32_t* w, uint32_t (&H)[16]) {

@@ -87,6 +87,8 @@ bool gemv_groupable(const DevModel& a, const DevModel& b);
 cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, float* const* ys, uint8_t* const* wss,
                               const int* Ms, int n, sfmp_dtype dt, cudaStream_t st, bool overlap_prev);
 int gemv_ctas_per_sm(int NT);
+// Two pipeline stages of the widest unit + activation record fit in shared memory.
+bool gemv_feasible(const DevModel& m);
 
 cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
                            cudaStream_t st);

@@ -95,4 +95,24 @@ __device__ __forceinline__ void unpack_word(const uint32_t* p, uint32_t (&H)[16]
     }
 }
 
+// 5..8-bit units for the decode GEMV: exact codes as f16 subnormals
+// c * 2^-24 (code in mantissa bits 0-7, exponent 0); H[4a+h] = weights
+// (4h+a, 4h+a+16) of the word.
+template <int B>
+__device__ __forceinline__ void unpack_word_sub(const uint32_t* p, uint32_t (&H)[16]) {
+    static_assert(B > 4 && B <= 8, "wide codes only");
+    uint32_t q[4], qh[4];
+    planes_to_nibbles<4>(p, q);
+    planes_to_nibbles<B - 4>(p + 4, qh);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            // nibble h of q (low 4 bits) and of qh (high bits), both halves
+            const uint32_t lo = (q[a] >> (4 * h)) & 0x000F000Fu;
+            const uint32_t hi = h == 0 ? (qh[a] << 4) : h == 1 ? qh[a] : (qh[a] >> (4 * h - 4));
+            H[4 * a + h] = lop3_and_or(hi, 0x00F000F0u, lo);
+        }
+}
+
 }  // namespace sfmpk

@@ -45,3 +45,36 @@ def errors(y, ref):
     d = np.abs(y - ref)
     scale = max(np.abs(ref).max(), 1e-30)
     return float(d.max() / scale), float(np.linalg.norm(y - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def _build_one(spec):
+    from oracle.oracle import Port
+    rows, cols, bits, kw = spec
+    model_bytes(Port(), rows, cols, bits, **kw)
+    return spec
+
+
+def prebuild(specs, workers=None):
+    """Build (and cache) several models in parallel processes: the big
+    Llama-3.1-70B / 8192x28672 fixtures take ~25 s each in the C packer."""
+    todo = []
+    for rows, cols, bits, kw in specs:
+        key = f"{rows}x{cols}_b{bits}_m{kw.get('mode', 3)}_{kw.get('m_b', 512)}x{kw.get('n_b', 128)}_s{kw.get('seed', 0)}"
+        if not os.path.exists(os.path.join(_CACHE, key + ".sfmp")):
+            todo.append((rows, cols, bits, kw))
+    if not todo:
+        return
+    import multiprocessing as mp
+    n = workers or min(len(todo), max(1, (os.cpu_count() or 2) - 1))
+    with mp.get_context("spawn").Pool(n) as pool:
+        list(pool.imap_unordered(_build_one, todo))
+
+
+def f32_activations(M, cols, seed=0, scale=1.0, outlier=True):
+    """Full-mantissa f32 activations (NOT bf16-representable) with one outlier
+    column 64x larger: exercises the hi/lo split and the per-token scaling."""
+    rng = np.random.default_rng(7000 + seed)
+    x = (rng.standard_normal((M, cols)) * scale).astype(np.float32)
+    if outlier:
+        x[:, (seed * 7919) % cols] *= 64.0
+    return x

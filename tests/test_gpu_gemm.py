@@ -120,15 +120,13 @@ def test_gemm_misaligned_x_routes_to_gemv(gpu, port):
         dm.gemm(x, path=gpu.PATH_GEMM)
 
 
-@pytest.mark.parametrize("dtype,legacy", [("bfloat16", False), ("bfloat16", True), ("float32", False)])
-def test_gemm_prepass_variants(gpu, port, dtype, legacy, monkeypatch):
+@pytest.mark.parametrize("dtype,cols", [("bfloat16", 14336), ("float32", 14336), ("float16", 14336)])
+def test_gemm_prepass_variants(gpu, port, dtype, cols):
     """Both prefill pre-passes: the persistent row-streaming one (bf16 rows of
-    a 14336-column linear) and the one-token-per-CTA one (forced, and taken
-    by f32 rows whose two staging buffers exceed its shared-memory budget)."""
+    a 14336-column linear) and the one-token-per-CTA one (f32 rows whose two
+    staging buffers exceed its shared-memory budget; rows of >= 65536 columns)."""
     import torch
-    if legacy:
-        monkeypatch.setenv("SFMP_XPREP_LEGACY", "1")
-    rows, cols, M = 512, 14336, 300
+    rows, M = 512, 300
     data = model_bytes(port, rows, cols, 3.0)
     dm = gpu.DeviceModel(data)
     xt = torch.from_numpy(activations(port, M, cols, seed=21)).cuda().to(getattr(torch, dtype))
