@@ -67,8 +67,23 @@ constexpr int kThreads = 32 * (1 + kNCW);  // producer | compute warps
 #define SFMP_SEG_COLS 1024
 #endif
 constexpr int kSegCols = SFMP_SEG_COLS;  // canonical K segment (columns)
-constexpr int kHdrBytes = 1024;   // barriers | zero fragments | stage info | flag
+constexpr int kHdrBytes = 1024;   // barriers | stage info | pending record copies
 constexpr int kSmemSM = 225 * 1024;
+#ifndef SFMP_MAX_STAGES
+#define SFMP_MAX_STAGES 4
+#endif
+#ifndef SFMP_SU
+#define SFMP_SU 2  // units per pipeline stage for n_b = 128
+#endif
+#ifndef SFMP_UNROLL_U
+#define SFMP_UNROLL_U 1
+#endif
+#ifndef SFMP_NOCOMPUTE
+#define SFMP_NOCOMPUTE 0
+#endif
+#ifndef SFMP_SPIN
+#define SFMP_SPIN 0
+#endif
 #ifndef SFMP_CTAS1
 #define SFMP_CTAS1 4
 #endif
@@ -78,49 +93,19 @@ constexpr int kSmemSM = 225 * 1024;
 constexpr int kCtasNT1 = SFMP_CTAS1, kCtasNT2 = SFMP_CTAS2;  // resident CTAs per SM (M <= 8 / 9..16)
 __host__ __device__ constexpr int ctas_per_sm(int NT) { return NT == 1 ? kCtasNT1 : kCtasNT2; }
 
-#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
-}  // namespace
-// Experiment builds only: per-CTA [start ns, end ns, smid, items] of the last
-// launch; then kernel-level [min start, max end] of xprep, gemv, fixup.
-__device__ unsigned long long g_gemv_tl[4096 * 4 + 16];
-namespace {
-__device__ __forceinline__ void tl_kernel(int k, bool start) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (start) atomicMin(&g_gemv_tl[4096 * 4 + 2 * k], t);
-    else atomicMax(&g_gemv_tl[4096 * 4 + 2 * k + 1], t);
-}
-#define TL_K(k, start) tl_kernel(k, start)
-__device__ __forceinline__ unsigned long long tl_now() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#else
-#define TL_K(k, start) do {} while (0)
-#endif
-
-#ifndef SFMP_L2_PREFETCH
-#define SFMP_L2_PREFETCH 0  // measured slower (weights of the next item into L2 during the pre-pass)
-#endif
-
-// stage info flags (producer -> compute warps, one 16-byte record per stage)
-constexpr uint32_t kFirst = 1, kLast = 2, kEnd = 4;
-
 // One linear of a (possibly grouped) launch.
 constexpr int kMaxLin = 40;
 struct Lin {
     const uint8_t* payload;
     const uint64_t* unit_desc;  // [RT*BC] row-tile-major
     const uint32_t* out_map;
-    const uint8_t* xrec;        // [BC] activation records of rec_bytes (nl sections of sec_bytes)
+    const uint8_t* xrec;        // activation records: [nl sections][BC] of sec_bytes
     float* y;
     float* part;                // [RT][P][16][128] f32 segment partials
     uint64_t out_rows;
     int BC, M, P, L;            // block columns, tokens, segments per tile, units per segment
     int RT;
-    uint32_t rec_bytes;         // its activation record bytes
-    uint32_t sec_bytes;         // one bit-width layout section of the record
+    uint32_t sec_bytes;         // one record section (one block column, one bit-width layout)
     uint32_t lo_off;            // offset of the lo fragments inside a 128-column chunk (f32 input)
     int item0;                  // first work item of this linear
     int fix0;                   // first fix-up (tile, token) pair of this linear
@@ -136,8 +121,8 @@ struct Params {
     unsigned* queue;     // [0] next item, [1] CTAs done (zero between calls)
     int n_b;
     int stages;
-    uint32_t stage_w;    // bytes per weight stage (smem)
-    uint32_t sec_bytes;  // max record section bytes (shared-memory stage stride)
+    uint32_t stage_w;    // bytes per weight stage (smem): SU units of the widest bit-width
+    uint32_t sec_bytes;  // max record section bytes (shared-memory record slot stride)
 };
 // Index of the linear owning entry `v` of a prefix array (binary search).
 __device__ __forceinline__ int owner_of(const int* start, int n, int v) {
@@ -159,7 +144,7 @@ struct XLin {
     int item0;      // first pre-pass CTA of this linear (one per token x 8 block columns)
     int lo, nl;     // floor bit-width, number of layout sections (1 or 2)
     int M;          // tokens of this linear
-    uint32_t rec_bytes, sec_bytes;
+    uint32_t sec_bytes;
 };
 struct XParams {
     XLin lin[kMaxLin];
@@ -167,17 +152,20 @@ struct XParams {
     int wait_prev;  // launched as a programmatic dependent of the previous GEMV
 };
 
-// Activation record of one block column (n_b columns), for M tokens: one
-// SECTION per bit-width layout (floor, ceil) of the matrix -- the producer
-// copies only the section of the unit's own bit-width.  A section:
+// Activation record section of one block column (n_b columns) for M tokens
+// in one bit-width layout (floor or ceil) of the matrix; the producer copies
+// the section of the unit's own bit-width.  Sections are stored [layout][BC],
+// so the records of consecutive block columns in one layout are contiguous.
+// A section:
 //   for chunk c (128 columns): hi runs of tokens 0..M-1, then (f32 input)
-//   lo runs of tokens 0..M-1.  A run = the token's 8 k-step B fragments,
-//   4 lanes x 8 B each (256 B), runs kRun = 288 B apart (the 32-byte pad
-//   spreads a warp's 8 tokens over all banks); each value is the scaled
-//   activation times 2^(24-p) of the register slot it pairs with.
+//   lo runs.  A run = the token's 8 k-step B fragments (256 B) arranged so a
+//   lane reads the fragments of k-steps 2j, 2j+1 with ONE 16-byte load at
+//   j*64 + q*16; runs sit kRun = 320 B apart (20 x 16 B: the two tokens of
+//   a quarter-warp then fall into disjoint bank quads).  Each value is the
+//   scaled activation times 2^(24-p) of the register slot it pairs with.
 //   Tail (floats): Xg[16] column sums of the scaled x | ysa[16], ysb[16]
 //   with ysa*ysb = 2^e_t (two factors: 2^e_t may not be a normal float).
-constexpr int kRun = 288;
+constexpr int kRun = 320;
 constexpr int kTailFloats = 48;
 constexpr int kYsIdx = 16;
 struct RecGeom {
@@ -186,7 +174,8 @@ struct RecGeom {
     __host__ __device__ int nt_count() const { return M > 8 ? 2 : 1; }
     __host__ __device__ int chunk_bytes() const { return kRun * M * (X2 ? 2 : 1); }
     __host__ __device__ int lo_off() const { return kRun * M; }
-    __host__ __device__ int run_off(int c, int t, int q) const { return c * chunk_bytes() + t * kRun + q * 8; }
+    __host__ __device__ int run_off(int c, int t, int q) const { return c * chunk_bytes() + t * kRun + q * 16; }
+    __host__ __device__ static int step_off(int s8) { return (s8 >> 1) * 64 + (s8 & 1) * 8; }
     __host__ __device__ int xg_off(int CH) const { return CH * chunk_bytes(); }
     __host__ __device__ int sec_bytes(int CH) const { return (xg_off(CH) + 4 * kTailFloats + 127) / 128 * 128; }
 };
@@ -254,10 +243,11 @@ __device__ __forceinline__ float row_absmax(const T* xr, int cols, F cvt, float*
 
 // Record piece of one block column for token t from 4 gathered, scaled
 // values per chunk: lane (s8, q) owns registers 2*s8, 2*s8+1 of k-step s8;
-// each layout section gets them times its slot factors.
+// each layout section gets them times its slot factors.  rec0 = the block
+// column's layout-0 section; layout l is l * lstride further.
 template <bool X2>
-__device__ __forceinline__ void write_fragments(uint8_t* rec, const RecGeom& G, int c, int t, int q, int s8,
-                                                const float (&v)[4], int lo, int nl, uint32_t sec_bytes) {
+__device__ __forceinline__ void write_fragments(uint8_t* rec0, size_t lstride, const RecGeom& G, int c, int t, int q,
+                                                int s8, const float (&v)[4], int lo, int nl) {
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
         if (l >= nl) break;
@@ -265,16 +255,16 @@ __device__ __forceinline__ void write_fragments(uint8_t* rec, const RecGeom& G, 
         uint2 h, w;
         split2<X2>(v[0], v[1], slot_factor(B, 2 * s8), h.x, w.x);      // pairs with A register 2*s8
         split2<X2>(v[2], v[3], slot_factor(B, 2 * s8 + 1), h.y, w.y);  // ... and 2*s8+1
-        uint8_t* dst = rec + l * sec_bytes + G.run_off(c, t, q) + s8 * 32;
+        uint8_t* dst = rec0 + l * lstride + G.run_off(c, t, q) + RecGeom::step_off(s8);
         *reinterpret_cast<uint2*>(dst) = h;
         if constexpr (X2) *reinterpret_cast<uint2*>(dst + G.lo_off()) = w;
     }
 }
-__device__ __forceinline__ void write_tail(uint8_t* rec, const RecGeom& G, int CH, int t, int M, float xs, int e,
-                                           int nl, uint32_t sec_bytes) {
+__device__ __forceinline__ void write_tail(uint8_t* rec0, size_t lstride, const RecGeom& G, int CH, int t, int M,
+                                          float xs, int e, int nl) {
     const float2 ys = pow2_pair(e);
     for (int l = 0; l < nl; ++l) {
-        float* xg = reinterpret_cast<float*>(rec + l * sec_bytes + G.xg_off(CH));
+        float* xg = reinterpret_cast<float*>(rec0 + l * lstride + G.xg_off(CH));
         xg[t] = xs;
         xg[kYsIdx + t] = ys.x;
         xg[kYsIdx + 16 + t] = ys.y;
@@ -289,15 +279,13 @@ __device__ __forceinline__ void write_tail(uint8_t* rec, const RecGeom& G, int C
 // scale, then each warp writes the record piece of one block column for
 // token t: lane (s, q) gathers the 4 k-slots 32q + 8(s&1) + 4j + 16e + (s>>1)
 // of each 128-column chunk from shared memory and stores 8 B of B fragments
-// per layout (hi, and lo for f32 input) -- the token's 256 B of a chunk are
-// one contiguous warp store.  The column sum X_g (lutgemm.cpp:113-115) uses
-// the scaled input values.
+// per layout (hi, and lo for f32 input).  The column sum X_g
+// (lutgemm.cpp:113-115) uses the scaled input values.
 template <sfmp_dtype DT>
 __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     using T = typename XT<DT>::T;
     constexpr bool X2 = DT == SFMP_F32;
     pdl_launch_dependents();  // let the GEMV start streaming weights right away
-    if (threadIdx.x == 0) TL_K(0, true);
     extern __shared__ __align__(16) uint8_t xsm[];
     __shared__ float red[8];
     const int n_b = xp.n_b, CH = n_b >> 7;
@@ -332,7 +320,8 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     if (warp >= nbc) return;
     const int bc = bc0 + warp, s8 = lane >> 2, q = lane & 3;
     const RecGeom G{M, X2};
-    uint8_t* rec = XL.xrec + static_cast<size_t>(bc) * XL.rec_bytes;
+    const size_t lstride = static_cast<size_t>(XL.BC) * XL.sec_bytes;
+    uint8_t* rec0 = XL.xrec + static_cast<size_t>(bc) * XL.sec_bytes;
     const uint32_t* cpw = cp + warp * n_b;
     const int kb = 32 * q + 8 * (s8 & 1) + (s8 >> 1);
     float xs = 0.f;
@@ -343,13 +332,12 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
 #pragma unroll
             for (int e2 = 0; e2 < 2; ++e2)
                 v[j * 2 + e2] = XT<DT>::f(xr[cpw[c * 128 + kb + 4 * j + 16 * e2]]) * sc.x * sc.y;
-        write_fragments<X2>(rec, G, c, t, q, s8, v, XL.lo, XL.nl, XL.sec_bytes);
+        write_fragments<X2>(rec0, lstride, G, c, t, q, s8, v, XL.lo, XL.nl);
         xs += (v[0] + v[1]) + (v[2] + v[3]);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
-    if (lane == 0) write_tail(rec, G, CH, t, M, xs, e, XL.nl, XL.sec_bytes);
-    if (lane == 0) TL_K(0, false);
+    if (lane == 0) write_tail(rec0, lstride, G, CH, t, M, xs, e, XL.nl);
     // When launched to overlap the previous GEMV of the same grouped call, do
     // not complete before it: this grid's completion (which the next GEMV waits
     // for) then implies the previous launch's, keeping stream order for any
@@ -396,7 +384,8 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     const int lane = threadIdx.x & 31, q = lane & 3, n = lane >> 2;
     const int t = nt * 8 + n;
     const bool live = item_ok && t < M;
-    uint8_t* rec = XL.xrec + static_cast<size_t>(bc) * XL.rec_bytes;
+    const size_t lstride = static_cast<size_t>(BC) * XL.sec_bytes;
+    uint8_t* rec0 = XL.xrec + static_cast<size_t>(bc) * XL.sec_bytes;
     const int e = live ? static_cast<int>(XL.escale[t]) : 0;
     const float2 sc = pow2_pair(-e);
     float xs = 0.f;
@@ -424,7 +413,7 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
                 float v[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) v[k] = XT<DT>::f(xrow[gi[s8 * 4 + k]]) * sc.x * sc.y;
-                write_fragments<X2>(rec, G, c, t, q, s8, v, XL.lo, XL.nl, XL.sec_bytes);
+                write_fragments<X2>(rec0, lstride, G, c, t, q, s8, v, XL.lo, XL.nl);
                 xs += (v[0] + v[1]) + (v[2] + v[3]);
             }
         }
@@ -443,7 +432,7 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     if (item_ok && q == 0) {
         const float2 ys = pow2_pair(e);
         for (int l = 0; l < XL.nl; ++l) {
-            float* xg = reinterpret_cast<float*>(rec + l * XL.sec_bytes + G.xg_off(CH));
+            float* xg = reinterpret_cast<float*>(rec0 + l * lstride + G.xg_off(CH));
             xg[t] = live ? xs : 0.f;
             xg[kYsIdx + t] = live ? ys.x : 0.f;
             xg[kYsIdx + 16 + t] = live ? ys.y : 0.f;
@@ -451,20 +440,31 @@ __global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     }
 }
 
+// Decode layout of a unit (upload time, sfmp_internal.h "lane-major"): a
+// 512-byte s/z block [warp cw][g][r] of (s, z) fp16 pairs for row
+// cw*32 + 8r + g, then the planes as [chunk c][cw][plane i][lane][r] words,
+// lane = 4g + q holding word q of the 16-byte row segment of chunk c.  A
+// compute lane therefore fetches its 4 rows' words of one plane with ONE
+// 16-byte shared load, and its 4 rows' (s, z) with one more.
+__host__ __device__ constexpr uint32_t unit_bytes(int B, int nb8) { return 512u + static_cast<uint32_t>(B) * 128u * nb8; }
+
 // One 128-column chunk of a unit for this warp's 32 rows (2 m16 tiles).
-// prow / xb are 32-bit shared addresses; all other offsets are immediates or
-// per-linear constants.  X2: the lo B fragments (lo_off further) are
-// contracted into the same accumulators.
+// pw = this lane's word of plane 0 (planes 512 B apart); xb = this lane's
+// B-fragment piece 0 of each n-tile (pieces 64 B apart).  X2: the lo B
+// fragments (lo_off further) are contracted into the same accumulators.
 template <int B, int NT, bool X2>
-__device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[NT], uint32_t lo_off, int nb8,
+__device__ __forceinline__ void unit_chunk(const uint8_t* pw, const uint8_t* const (&xb)[NT], uint32_t lo_off,
                                            float (&cacc)[kMT][NT][4]) {
-    const int PS = kTR * nb8;  // bytes of one plane of the unit
     // rows r0 + 8*r: (r0, r0+8) is m-tile 0, (r0+16, r0+24) m-tile 1
     uint32_t p[2 * kMT][B];
 #pragma unroll
-    for (int i = 0; i < B; ++i)
-#pragma unroll
-        for (int r = 0; r < 2 * kMT; ++r) p[r][i] = lds_u32(prow + i * PS + r * 8 * nb8);
+    for (int i = 0; i < B; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4*>(pw + i * 512);
+        p[0][i] = v.x;
+        p[1][i] = v.y;
+        p[2][i] = v.z;
+        p[3][i] = v.w;
+    }
     uint32_t A[2 * kMT][16];
 #pragma unroll
     for (int r = 0; r < 2 * kMT; ++r) {
@@ -472,35 +472,72 @@ __device__ __forceinline__ void unit_chunk(uint32_t prow, const uint32_t (&xb)[N
         else unpack_word_sub<B>(p[r], A[r]);                // bit planes (unpack.cuh)
     }
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int j = 0; j < 4; ++j) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-            const uint2 b = lds_v2(xb[nt] + s * 32);
-            uint2 bl;
-            if constexpr (X2) bl = lds_v2(xb[nt] + lo_off + s * 32);
+            const uint4 b = *reinterpret_cast<const uint4*>(xb[nt] + j * 64);
+            uint4 bl;
+            if constexpr (X2) bl = *reinterpret_cast<const uint4*>(xb[nt] + lo_off + j * 64);
 #pragma unroll
-            for (int m = 0; m < kMT; ++m) {
-                mma_16816(cacc[m][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
-                          A[2 * m + 1][2 * s + 1], b.x, b.y);
-                if constexpr (X2)
+            for (int h = 0; h < 2; ++h) {
+                const int s = 2 * j + h;
+                const uint32_t b0 = h ? b.z : b.x, b1 = h ? b.w : b.y;
+#pragma unroll
+                for (int m = 0; m < kMT; ++m) {
                     mma_16816(cacc[m][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
-                              A[2 * m + 1][2 * s + 1], bl.x, bl.y);
+                              A[2 * m + 1][2 * s + 1], b0, b1);
+                    if constexpr (X2)
+                        mma_16816(cacc[m][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
+                                  A[2 * m + 1][2 * s + 1], h ? bl.z : bl.x, h ? bl.w : bl.y);
+                }
             }
         }
     }
 }
 
-// Producer waits for a free stage: suspend in the barrier (woken by the
-// phase completion) instead of spinning -- a spinning producer took ~20 % of
-// the SM's issue slots from the compute warps (ncu source counts, round 1).
-#ifndef SFMP_PROD_IDLE
-#define SFMP_PROD_IDLE 1
-#endif
-__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
-    if (!SFMP_PROD_IDLE) {
-        mbar_wait_a(bar, parity);
-        return;
+// One unit (block column) of B bits: the MMA over its chunks, then the
+// block's per-row affine y += s*C + z*Xg (the mirror identity of
+// quantizer.cpp:57-72 without the LUT).
+template <int B, int CH, int NT, bool X2>
+__device__ __forceinline__ void unit_step(const uint8_t* ub, const uint8_t* xr, const uint32_t (&xoff)[NT],
+                                          uint32_t chunk_bytes, uint32_t lo_off, uint32_t xg_off, int cw, int lane,
+                                          float (&yacc)[kMT][NT][4]) {
+    float cacc[kMT][NT][4];
+#pragma unroll
+    for (int m = 0; m < kMT; ++m)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) cacc[m][nt][e] = 0.f;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const uint8_t* xbc[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) xbc[nt] = xr + xoff[nt] + c * chunk_bytes;
+        unit_chunk<B, NT, X2>(ub + 512 + c * (B * 2048) + cw * (B * 512) + lane * 16, xbc, lo_off, cacc);
     }
+    const uint4 sz = *reinterpret_cast<const uint4*>(ub + cw * 128 + (lane >> 2) * 16);
+    const uint32_t szw[4] = {sz.x, sz.y, sz.z, sz.w};
+#pragma unroll
+    for (int m = 0; m < kMT; ++m) {
+        const __half2 pa = u32_as_h2(szw[2 * m]), pb = u32_as_h2(szw[2 * m + 1]);
+        const float sa = __low2float(pa), za = __high2float(pa);
+        const float sb = __low2float(pb), zb = __high2float(pb);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const float2 xg01 = *reinterpret_cast<const float2*>(xr + xg_off + 8 * (lane & 3) + 32 * nt);
+            const float* c0 = cacc[m][nt];
+            yacc[m][nt][0] = fmaf(sa, c0[0], fmaf(za, xg01.x, yacc[m][nt][0]));
+            yacc[m][nt][1] = fmaf(sa, c0[1], fmaf(za, xg01.y, yacc[m][nt][1]));
+            yacc[m][nt][2] = fmaf(sb, c0[2], fmaf(zb, xg01.x, yacc[m][nt][2]));
+            yacc[m][nt][3] = fmaf(sb, c0[3], fmaf(zb, xg01.y, yacc[m][nt][3]));
+        }
+    }
+}
+
+// Barrier waits that suspend the thread (woken by the phase completion)
+// instead of spinning: spinning waiters took issue slots from working warps.
+__device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tWAITI_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAITI_%=;\n\t}" ::"r"(bar),
@@ -508,21 +545,31 @@ __device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// A stage holds SU consecutive units of one work item (SU = 2 for n_b = 128,
+// 1 for n_b = 256: 256 columns either way) and their record sections.
+// Stage info (16 B): x = linear | bits0 << 8 | bits1 << 12 | units << 16 | flags << 20, y = row tile, z = segment.
+constexpr uint32_t kFirst = 1, kLast = 2, kEnd = 4;
+struct PendCopy {
+    const uint8_t* src;
+    uint32_t dst, bytes;
+};
+
 // LO = the model's floor bit-width: every unit has LO or LO+1 bits
 // (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
 // two unpack paths and its hot loop stays resident in the instruction cache.
 template <int NT, int CH, int LO, bool X2>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const Params p) {
+    constexpr int SU = CH == 1 ? SFMP_SU : 1;
+    constexpr int nb8 = CH * 16;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* empty = full + S;
-    uint8_t* zeros = smem + 256;                          // 256 B: B fragments of absent tokens
-    uint4* sinfo = reinterpret_cast<uint4*>(smem + 512);  // [S] stage info
-    const uint8_t** pend_src = reinterpret_cast<const uint8_t**>(smem + 768);  // [S] producer only
+    uint64_t* empty = full + 8;
+    uint4* sinfo = reinterpret_cast<uint4*>(smem + 128);                  // [S]
+    PendCopy* pend = reinterpret_cast<PendCopy*>(smem + 256);             // [2S] producer only
     uint8_t* wbase = smem + kHdrBytes;
+    const uint32_t xstride = SU * p.sec_bytes;
     uint8_t* xbase = wbase + static_cast<size_t>(S) * p.stage_w;
-    constexpr int nb8 = CH * 16;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // a programmatic dependent (the fix-up of this launch, or the next launch
@@ -537,33 +584,21 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         fence_mbar_init();
         fence_proxy_async();
     }
-    if (threadIdx.x < 64) reinterpret_cast<uint32_t*>(zeros)[threadIdx.x] = 0u;
     __syncthreads();
-#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
-    unsigned n_claimed = 0;
-    if (threadIdx.x == 0) TL_K(1, true);
-    if (threadIdx.x == 0 && blockIdx.x < 4096) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_gemv_tl[blockIdx.x * 4 + 0] = tl_now();
-        g_gemv_tl[blockIdx.x * 4 + 2] = smid;
-    }
-#endif
 
     if (warp == 0) {
-        // ---------------- producer: claims items, one bulk copy per unit (+ its record section) ----
+        // ---------------- producer: claims items, one bulk copy per stage (+ its record sections) ----
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             const uint64_t keep = policy_evict_last();
-            const uint32_t pbytes = kTR * nb8;
+            const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
             int s = 0, ph = 0;
             bool released = false;  // griddepcontrol.wait done: records may be copied
-            int npend = 0;          // stages 0..npend-1 wait for their records (source in pend_src)
-            auto issue_x = [&](int st, const uint8_t* src, uint32_t n) {
+            int npend = 0, pstages = 0;
+            auto issue_x = [&](const uint8_t* src, uint32_t dst, uint32_t n, int st) {
                 asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        smem_u32(xbase + static_cast<size_t>(st) * p.sec_bytes)),
-                    "l"(src), "r"(n), "r"(smem_u32(&full[st]))
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                    "l"(src), "r"(n), "r"(full_a + 8 * st)
                     : "memory");
             };
             // The weights of the first ring-full do not depend on x: they are
@@ -572,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 if (released) return;
                 pdl_wait();
                 released = true;
-                for (int i = 0; i < npend; ++i) issue_x(i, pend_src[i], sinfo[i].w);
+                for (int i = 0; i < npend; ++i) issue_x(pend[i].src, pend[i].dst & 0x00FFFFFFu, pend[i].bytes, static_cast<int>(pend[i].dst >> 24));
                 npend = 0;
             };
             unsigned item = atomicAdd(p.queue, 1u);
@@ -583,47 +618,54 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                 const int rel = static_cast<int>(item) - L.item0;
                 const int rt = rel / L.P, seg = rel - rt * L.P;
                 const int bc0 = seg * L.L, bc1 = min(L.BC, bc0 + L.L);
-                if (SFMP_L2_PREFETCH && !released && next < static_cast<unsigned>(p.n_items)) {
-                    // While the pre-pass runs, pull the next item's weights into
-                    // L2 (the ring holds only the first few units of this one).
-                    const Lin& N = p.lin[owner_of(p.item_start, p.nlin, static_cast<int>(next))];
-                    const int rn = static_cast<int>(next) - N.item0, rtn = rn / N.P, sn = rn - rtn * N.P;
-                    const uint64_t* nd = N.unit_desc + static_cast<size_t>(rtn) * N.BC;
-                    for (int bc = sn * N.L; bc < min(N.BC, (sn + 1) * N.L); ++bc) {
-                        const uint64_t d = ldg_keep_u64(nd + bc, keep);
-                        bulk_prefetch_l2(N.payload + (d & 0xFFFFFFFFFFFFull), 4 * kTR + static_cast<uint32_t>((d >> 48) & 0xF) * pbytes);
-                    }
-                }
                 const uint64_t* gdesc = L.unit_desc + static_cast<size_t>(rt) * L.BC;
-                uint64_t dnext = ldg_keep_u64(gdesc + bc0, keep);
-                for (int bc = bc0; bc < bc1; ++bc) {
-                    const uint64_t d = dnext;
-                    if (bc + 1 < bc1) dnext = ldg_keep_u64(gdesc + bc + 1, keep);
-                    if (!released && npend == S) release();  // ring full: records now
-                    mbar_wait_idle(smem_u32(&empty[s]), ph ^ 1);
-                    const int bits = static_cast<int>((d >> 48) & 0xF);
-                    const uint32_t fl = (bc == bc0 ? kFirst : 0u) | (bc == bc1 - 1 ? kLast : 0u);
-                    sinfo[s] = make_uint4(static_cast<uint32_t>(li) | (static_cast<uint32_t>(bits) << 8) | (fl << 16),
-                                          static_cast<uint32_t>(rt), static_cast<uint32_t>(seg), L.sec_bytes);
-                    const uint32_t wbytes = 4 * kTR + bits * pbytes;
-                    mbar_arrive_expect_tx(&full[s], wbytes + L.sec_bytes);  // publishes sinfo[s]
-                    bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d & 0xFFFFFFFFFFFFull), wbytes,
+                const uint32_t sec = L.sec_bytes;
+                uint64_t d0n = ldg_keep_u64(gdesc + bc0, keep);
+                uint64_t d1n = (SU == 2 && bc0 + 1 < bc1) ? ldg_keep_u64(gdesc + bc0 + 1, keep) : 0ull;
+                for (int bc = bc0; bc < bc1; bc += SU) {
+                    const int nu = min(SU, bc1 - bc);
+                    const uint64_t d0 = d0n, d1 = d1n;
+                    if (bc + SU < bc1) {
+                        d0n = ldg_keep_u64(gdesc + bc + SU, keep);
+                        if (SU == 2 && bc + SU + 1 < bc1) d1n = ldg_keep_u64(gdesc + bc + SU + 1, keep);
+                    }
+                    if (!released && pstages == S) release();  // ring full: records now
+                    mbar_wait_idle(empty_a + 8 * s, ph ^ 1);
+                    const int b0 = static_cast<int>((d0 >> 48) & 0xF);
+                    const int b1 = nu > 1 ? static_cast<int>((d1 >> 48) & 0xF) : 0;
+                    const uint32_t fl = (bc == bc0 ? kFirst : 0u) | (bc + nu == bc1 ? kLast : 0u);
+                    sinfo[s] = make_uint4(static_cast<uint32_t>(li) | (static_cast<uint32_t>(b0) << 8) |
+                                              (static_cast<uint32_t>(b1) << 12) | (static_cast<uint32_t>(nu) << 16) |
+                                              (fl << 20),
+                                          static_cast<uint32_t>(rt), static_cast<uint32_t>(seg), 0u);
+                    const uint32_t wbytes = unit_bytes(b0, nb8) + (nu > 1 ? unit_bytes(b1, nb8) : 0u);
+                    mbar_arrive_expect_tx(&full[s], wbytes + nu * sec);  // publishes sinfo[s]
+                    bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d0 & 0xFFFFFFFFFFFFull), wbytes,
                              &full[s], pol);
-                    // the record section of this unit's bit-width layout
-                    const uint8_t* rsrc = L.xrec + static_cast<size_t>(bc) * L.rec_bytes + (bits == L.lo ? 0u : L.sec_bytes);
-                    if (released) issue_x(s, rsrc, L.sec_bytes);
-                    else pend_src[npend++] = rsrc;  // == stage s (no wrap before the release)
+                    // record sections of the units' bit-width layouts ([layout][BC]: one
+                    // copy when both units share a layout)
+                    const int l0 = b0 != L.lo, l1 = b1 != L.lo;
+                    const uint32_t xd = smem_u32(xbase) + s * xstride;
+                    const uint8_t* r0 = L.xrec + static_cast<size_t>(l0 * L.BC + bc) * sec;
+                    const uint8_t* r1 = L.xrec + static_cast<size_t>(l1 * L.BC + bc + 1) * sec;
+                    const bool one = nu == 1 || l0 == l1;
+                    const uint32_t n0 = one ? nu * sec : sec;
+                    if (released) {
+                        issue_x(r0, xd, n0, s);
+                        if (!one) issue_x(r1, xd + sec, sec, s);
+                    } else {
+                        pend[npend++] = PendCopy{r0, xd | (static_cast<uint32_t>(s) << 24), n0};
+                        if (!one) pend[npend++] = PendCopy{r1, (xd + sec) | (static_cast<uint32_t>(s) << 24), sec};
+                        ++pstages;
+                    }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
                 item = next;
-#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
-                ++n_claimed;
-#endif
             }
             release();
             // end of work: one empty stage with the END flag
-            mbar_wait_idle(smem_u32(&empty[s]), ph ^ 1);
-            sinfo[s] = make_uint4(kEnd << 16, 0u, 0u, 0u);
+            mbar_wait_idle(empty_a + 8 * s, ph ^ 1);
+            sinfo[s] = make_uint4(kEnd << 20, 0u, 0u, 0u);
             mbar_arrive(&full[s]);
         }
         __syncwarp();
@@ -632,41 +674,35 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
         const int cw = warp - 1;
         const int g = lane >> 2, q = lane & 3;
         const int r0 = cw * 16 * kMT + g;  // rows r0 + 8*r of the tile
-        const uint32_t stage_w = p.stage_w, sec_stride = p.sec_bytes;
-        // per-lane shared addresses for stage 0; a stage adds s * stage_w / sec_stride
-        const uint32_t prow0 = smem_u32(wbase) + 4 * kTR + r0 * nb8 + q * 4;
-        const uint32_t sz0 = smem_u32(wbase) + 2 * r0;
-        const uint32_t sinfo_a = smem_u32(sinfo);
         const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
-        // record addresses depend on the linear's M: set when the linear changes
-        int chunk_bytes = 0, cur_li = -1;
-        uint32_t lo_off = 0, live_mask = 0;
-        uint32_t xb0[NT], xg0 = 0;
+        // record geometry depends on the linear's M: set when the linear changes
+        int cur_li = -1;
+        uint32_t chunk_bytes = 0, lo_off = 0, xg_off = 0, sec = 0;
+        uint32_t xoff[NT];  // offset of this lane's B-fragment piece 0 of each n-tile in a record
         float yacc[kMT][NT][4];
         float ysa[NT][2], ysb[NT][2];
         int s = 0, ph = 0;
-        uint32_t wo = 0, xo = 0;  // byte offsets of stage s in the weight / record rings
         for (;;) {
-            mbar_wait_a(full_a + 8 * s, ph);
-            const uint4 info = lds_v4(sinfo_a + 16 * s);
-            const uint32_t fl = info.x >> 16;
+            if (SFMP_SPIN) mbar_wait_a(full_a + 8 * s, ph);
+            else mbar_wait_idle(full_a + 8 * s, ph);
+            const uint4 info = sinfo[s];
+            const uint32_t fl = info.x >> 20;
             if (fl & kEnd) break;
-            const int li = static_cast<int>(info.x & 0xFF), bits = static_cast<int>((info.x >> 8) & 0xFF);
+            const int li = static_cast<int>(info.x & 0xFF);
             if (li != cur_li) {
                 cur_li = li;
                 const Lin& L = p.lin[li];
                 const RecGeom GL{L.M, X2};
                 chunk_bytes = GL.chunk_bytes();
                 lo_off = L.lo_off;
-                live_mask = 0;
+                sec = L.sec_bytes;
+                xg_off = GL.xg_off(CH);
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const bool live = nt * 8 + g < L.M;
-                    live_mask |= live ? 1u << nt : 0u;
-                    xb0[nt] = live ? smem_u32(xbase) + GL.run_off(0, nt * 8 + g, q) : smem_u32(zeros) + q * 8;
-                }
-                xg0 = smem_u32(xbase) + GL.xg_off(CH) + 8 * q;
+                for (int nt = 0; nt < NT; ++nt)  // absent tokens read token 0's fragments (never stored)
+                    xoff[nt] = GL.run_off(0, nt * 8 + g < L.M ? nt * 8 + g : 0, q);
             }
+            const uint8_t* ws = wbase + static_cast<size_t>(s) * p.stage_w;
+            const uint8_t* xs = xbase + static_cast<size_t>(s) * xstride;
             if (fl & kFirst) {
 #pragma unroll
                 for (int m = 0; m < kMT; ++m)
@@ -676,57 +712,35 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                         for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {  // output scale of tokens nt*8+2q, +1
-                    const float2 a = lds_f2(xg0 + xo + 4 * kYsIdx + 32 * nt);
-                    const float2 b = lds_f2(xg0 + xo + 4 * (kYsIdx + 16) + 32 * nt);
+                    const float2 a = *reinterpret_cast<const float2*>(xs + xg_off + 4 * kYsIdx + 32 * nt + 8 * q);
+                    const float2 b = *reinterpret_cast<const float2*>(xs + xg_off + 4 * (kYsIdx + 16) + 32 * nt + 8 * q);
                     ysa[nt][0] = a.x;
                     ysa[nt][1] = a.y;
                     ysb[nt][0] = b.x;
                     ysb[nt][1] = b.y;
                 }
             }
-            uint32_t xb[NT];
+#if SFMP_UNROLL_U
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) xb[nt] = xb0[nt] + ((live_mask >> nt) & 1u ? xo : 0u);
-            const uint32_t prow = prow0 + wo;
-            float cacc[kMT][NT][4];
-#pragma unroll
-            for (int m = 0; m < kMT; ++m)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) cacc[m][nt][e] = 0.f;
-#pragma unroll
-            for (int c = 0; c < CH; ++c) {
-                uint32_t xbc[NT];
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) xbc[nt] = xb[nt] + ((live_mask >> nt) & 1u ? c * chunk_bytes : 0);
-                if (bits == LO) {
-                    unit_chunk<LO, NT, X2>(prow + c * 16, xbc, lo_off, nb8, cacc);
+#else
+#pragma unroll 1
+#endif
+            for (int u = 0; u < SU; ++u) {
+                const int bits = static_cast<int>((info.x >> (8 + 4 * u)) & 0xF);
+                if (u > 0 && ((info.x >> 16) & 0xF) < 2) break;
+                const uint8_t* ub = ws + (u ? unit_bytes(info.x >> 8 & 0xF, nb8) : 0u);
+                const uint8_t* xr = xs + u * sec;
+                if (SFMP_NOCOMPUTE) {
+                    if (bits == 0xF) yacc[0][0][0] += 1.f;  // experiment builds: streaming only
+                } else if (bits == LO) {
+                    unit_step<LO, CH, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
                 } else if constexpr (LO < 8) {
-                    unit_chunk<LO + 1, NT, X2>(prow + c * 16, xbc, lo_off, nb8, cacc);
-                }
-            }
-            // per-row affine of this block: y += s*C + z*Xg
-            const uint32_t sz = sz0 + wo, xg = xg0 + xo;
-#pragma unroll
-            for (int m = 0; m < kMT; ++m) {
-                const float sa = lds_h2f(sz + 32 * m), sb = lds_h2f(sz + 32 * m + 16);
-                const float za = lds_h2f(sz + 2 * kTR + 32 * m), zb = lds_h2f(sz + 2 * kTR + 32 * m + 16);
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const float2 xg01 = lds_f2(xg + 32 * nt);
-                    const float* c0 = cacc[m][nt];
-                    yacc[m][nt][0] = fmaf(sa, c0[0], fmaf(za, xg01.x, yacc[m][nt][0]));
-                    yacc[m][nt][1] = fmaf(sa, c0[1], fmaf(za, xg01.y, yacc[m][nt][1]));
-                    yacc[m][nt][2] = fmaf(sb, c0[2], fmaf(zb, xg01.x, yacc[m][nt][2]));
-                    yacc[m][nt][3] = fmaf(sb, c0[3], fmaf(zb, xg01.y, yacc[m][nt][3]));
+                    unit_step<LO + 1, CH, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive_a(empty_a + 8 * s);
-            wo += stage_w;
-            xo += sec_stride;
-            if (++s == S) { s = 0; ph ^= 1; wo = 0; xo = 0; }
+            if (++s == S) { s = 0; ph ^= 1; }
             if (!(fl & kLast)) continue;
 
             // ---- end of a segment: scale back by 2^e_t (exact), store y or the partial ----
@@ -751,13 +765,6 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     }
     // the last CTA out resets the work queue for the next call (stream-ordered)
     __syncthreads();
-#if defined(SFMP_GEMV_TIMELINE) && SFMP_GEMV_TIMELINE
-    if (threadIdx.x == 0 && blockIdx.x < 4096) {
-        g_gemv_tl[blockIdx.x * 4 + 1] = tl_now();
-        g_gemv_tl[blockIdx.x * 4 + 3] = n_claimed;
-    }
-    if (threadIdx.x == 0) TL_K(1, false);
-#endif
     if (threadIdx.x == 0) {
         const unsigned done = atomicAdd(p.queue + 1, 1u);
         if (done == gridDim.x - 1) {
@@ -779,7 +786,6 @@ __global__ void __launch_bounds__(8 * kTR) gemv_fixup_kernel(const Params p) {
     const int stride = static_cast<int>(gridDim.x) * 8;
     int w = static_cast<int>(blockIdx.x) * 8 + static_cast<int>(threadIdx.x >> 7);
     pdl_wait();  // the GEMV grid has completed and its partials are visible
-    if (threadIdx.x == 0) TL_K(2, true);
     for (; w < p.n_fix; w += 2 * stride) {
         const float* pp[2];
         float* yp[2];
@@ -814,24 +820,7 @@ __global__ void __launch_bounds__(8 * kTR) gemv_fixup_kernel(const Params p) {
         for (int h = 0; h < 2; ++h)
             if (P[h]) *yp[h] = acc[h];
     }
-    if (threadIdx.x == 0) TL_K(2, false);
 }
-
-#ifndef SFMP_GEMV_TIMELINE
-#define SFMP_GEMV_TIMELINE 0
-#endif
-#if SFMP_GEMV_TIMELINE
-}  // namespace
-extern "C" int sfmp_debug_gemv_timeline(unsigned long long* host, size_t n) {
-    if (n > 4096 * 4 + 16) n = 4096 * 4 + 16;
-    cudaError_t e = cudaMemcpyFromSymbol(host, g_gemv_tl, n * sizeof(unsigned long long));
-    unsigned long long init[16];
-    for (int i = 0; i < 16; ++i) init[i] = (i & 1) ? 0ull : ~0ull;
-    cudaMemcpyToSymbol(g_gemv_tl, init, sizeof(init), 4096 * 4 * sizeof(unsigned long long));
-    return static_cast<int>(e);
-}
-namespace {
-#endif
 
 // One-time (per device, thread-safe) function attribute setup.
 template <class F>
@@ -954,17 +943,18 @@ struct SmemPlan {
     int stages, ctas;
     size_t smem;
 };
-SmemPlan smem_plan(uint32_t stage_w, uint32_t sec_bytes, int NT) {
+SmemPlan smem_plan(uint32_t stage_w, uint32_t rec_slot, int NT) {
     for (int ctas = ctas_per_sm(NT); ctas >= 1; --ctas) {
         const int budget = (ctas == 1 ? 227 * 1024 : kSmemSM / ctas) - kHdrBytes;
-        const int stages = std::min<int>(4, budget / static_cast<int>(stage_w + sec_bytes));
-        if (stages >= 2) return {stages, ctas, kHdrBytes + static_cast<size_t>(stages) * (stage_w + sec_bytes)};
+        const int stages = std::min<int>(SFMP_MAX_STAGES, budget / static_cast<int>(stage_w + rec_slot));
+        if (stages >= 2) return {stages, ctas, kHdrBytes + static_cast<size_t>(stages) * (stage_w + rec_slot)};
     }
     return {0, 0, 0};
 }
 int layouts_of(const DevModel& m) { return m.ceil_bits > m.floor_bits ? 2 : 1; }
+int units_per_stage(const DevModel& m) { return m.n_b == 128 ? SFMP_SU : 1; }
 uint32_t stage_bytes(const DevModel& m, int ceil_bits) {
-    return static_cast<uint32_t>((4 * kTR + ceil_bits * kTR * (m.n_b / 8) + 127) / 128 * 128);
+    return (units_per_stage(m) * unit_bytes(ceil_bits, static_cast<int>(m.n_b / 8)) + 127) / 128 * 128;
 }
 
 }  // namespace
@@ -985,7 +975,8 @@ size_t gemv_workspace_bytes(const DevModel& m, int M) {
 int gemv_ctas_per_sm(int NT) { return ctas_per_sm(NT); }
 
 bool gemv_feasible(const DevModel& m) {
-    return smem_plan(stage_bytes(m, m.ceil_bits), static_cast<uint32_t>(RecGeom{16, true}.sec_bytes(static_cast<int>(m.n_b / 128))), 2)
+    return smem_plan(stage_bytes(m, m.ceil_bits),
+                     units_per_stage(m) * static_cast<uint32_t>(RecGeom{16, true}.sec_bytes(static_cast<int>(m.n_b / 128))), 2)
                .stages >= 2;
 }
 
@@ -1034,7 +1025,6 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         L.L = units_per_segment(m);
         L.P = segments_per_tile(m);
         L.sec_bytes = static_cast<uint32_t>(G.sec_bytes(CH));
-        L.rec_bytes = nl * L.sec_bytes;
         L.lo_off = static_cast<uint32_t>(G.lo_off());
         L.lo = m.floor_bits;
         L.item0 = items;
@@ -1056,7 +1046,6 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         X.lo = m.floor_bits;
         X.nl = nl;
         X.M = Ms[i];
-        X.rec_bytes = L.rec_bytes;
         X.sec_bytes = L.sec_bytes;
         xwarps += BC * NT;
         xitems += (BC + 7) / 8 * Ms[i];  // pre-pass CTAs: (8 block columns) x tokens
@@ -1070,7 +1059,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     p.item_start[n] = items;
     p.fix_start[n] = fix;
     p.stage_w = stage_bytes(m0, ceil_bits);
-    const SmemPlan sp = smem_plan(p.stage_w, p.sec_bytes, NT);
+    const SmemPlan sp = smem_plan(p.stage_w, units_per_stage(m0) * p.sec_bytes, NT);
     if (sp.stages < 2) return cudaErrorInvalidConfiguration;  // excluded at upload (gemv_feasible)
     p.stages = sp.stages;
     const int grid = std::min(items, m0.num_sms * sp.ctas);

@@ -25,24 +25,29 @@ __device__ __forceinline__ float ldx(const void* x, size_t i) {
 
 // One row segment of one unit: scale/zero widened exactly from fp16
 // (fp16.hpp:58-83) and a code reader restating unpack_block (layout.cpp:77-83).
+// Two unit layouts (sfmp_internal.h): the SFMPPKD1 order (scales | zeros |
+// planes row-major), and the decode GEMV's lane-major order (TR = 128, n_b in
+// {128, 256}; repack.cuh) with <= 4-bit groups repacked.
 struct RowRef {
-    const uint8_t* planes;  // plane 0 of the unit
-    uint64_t plane_bytes;   // TR * n_b / 8
-    uint32_t row_off;       // rr * n_b / 8
-    int bits;
-    bool repacked;
+    const uint8_t* planes;  // plane region of the unit
+    uint32_t bits;
+    bool lane_major;
+    uint32_t rr;            // row within the unit
+    uint64_t plane_bytes;   // (SFMPPKD1 order) TR * n_b / 8
+    uint32_t row_off;       // (SFMPPKD1 order) rr * n_b / 8
     float s, z;
-    // Units of <= 4 bits are stored in the repacked decode layout
-    // (repack.cuh); wider units keep the SFMPPKD1 bit planes.
     __device__ __forceinline__ uint32_t code(uint32_t jj) const {
-        if (repacked && bits <= 4) {
-            uint32_t w[4];
-            for (int i = 0; i < bits; ++i)
-                w[i] = *reinterpret_cast<const uint32_t*>(planes + i * plane_bytes + row_off + (jj >> 5) * 4);
-            return rp_code(w, bits, static_cast<int>(jj & 31));
+        if (lane_major) {
+            uint32_t w[8];
+            const uint8_t* p = planes + lm_word_off(bits, jj >> 7, rr, (jj >> 5) & 3, 0);
+            for (uint32_t i = 0; i < bits; ++i) w[i] = *reinterpret_cast<const uint32_t*>(p + i * 512);
+            if (bits <= 4) return rp_code(w, static_cast<int>(bits), static_cast<int>(jj & 31));
+            uint32_t c = 0;
+            for (uint32_t i = 0; i < bits; ++i) c |= ((w[i] >> (jj & 31)) & 1u) << i;
+            return c;
         }
         uint32_t c = 0;
-        for (int i = 0; i < bits; ++i)
+        for (uint32_t i = 0; i < bits; ++i)
             c |= ((planes[i * plane_bytes + row_off + (jj >> 3)] >> (jj & 7)) & 1u) << i;
         return c;
     }
@@ -54,11 +59,19 @@ __device__ __forceinline__ RowRef row_ref(const UnitGeom& g, uint64_t r, uint32_
     const uint8_t* base = g.payload + (d & 0xFFFFFFFFFFFFull);
     const uint32_t rr = static_cast<uint32_t>(r % g.TR);
     RowRef ref;
-    ref.bits = static_cast<int>((d >> 48) & 0xF);
-    ref.repacked = g.repacked;
-    ref.s = __half2float(*reinterpret_cast<const __half*>(base + 2 * rr));
-    ref.z = __half2float(*reinterpret_cast<const __half*>(base + 2ull * g.TR + 2 * rr));
-    ref.planes = base + 4ull * g.TR;
+    ref.bits = static_cast<uint32_t>((d >> 48) & 0xF);
+    ref.lane_major = g.repacked;
+    ref.rr = rr;
+    if (g.repacked) {
+        const uint32_t so = lm_sz_off(rr);
+        ref.s = __half2float(*reinterpret_cast<const __half*>(base + so));
+        ref.z = __half2float(*reinterpret_cast<const __half*>(base + so + 2));
+        ref.planes = base + 512;
+    } else {
+        ref.s = __half2float(*reinterpret_cast<const __half*>(base + 2 * rr));
+        ref.z = __half2float(*reinterpret_cast<const __half*>(base + 2ull * g.TR + 2 * rr));
+        ref.planes = base + 4ull * g.TR;
+    }
     ref.plane_bytes = static_cast<uint64_t>(g.TR) * (g.n_b >> 3);
     ref.row_off = rr * (g.n_b >> 3);
     return ref;
@@ -151,28 +164,41 @@ GenParams make_params(const DevModel& m) {
 
 }  // namespace
 
-// Host: rewrite every <= 4-bit unit of the unit-major payload from bit planes
-// to the repacked decode layout (repack.cuh), in place, byte count unchanged.
+// Host: rewrite every unit of the unit-major payload into the decode GEMV's
+// lane-major order (repack.cuh: lm_sz_off / lm_word_off), <= 4-bit groups
+// repacked for one-LOP3 unpacking; in place, byte count unchanged.
 void repack_units(const DevModel& d, std::vector<uint8_t>& payload) {
     if (!d.gemv_ok) return;  // only the decode GEMV's geometry (TR=128, n_b in {128, 256})
     const uint32_t TR = d.TR, nb8 = d.n_b / 8, groups = d.n_b / 32;
     const uint64_t PS = static_cast<uint64_t>(TR) * nb8;
+    std::vector<uint8_t> tmp;
     for (uint64_t desc : d.h_unit_desc) {
         const int B = static_cast<int>((desc >> 48) & 0xF);
-        if (B > 4) continue;
-        uint8_t* planes = payload.data() + (desc & 0xFFFFFFFFFFFFull) + 4ull * TR;
-        for (uint32_t r = 0; r < TR; ++r)
+        uint8_t* u = payload.data() + (desc & 0xFFFFFFFFFFFFull);
+        const size_t ub = 4ull * TR + B * PS;
+        tmp.assign(u, u + ub);
+        const uint8_t* planes = tmp.data() + 4ull * TR;
+        for (uint32_t r = 0; r < TR; ++r) {
+            const uint32_t so = lm_sz_off(r);
+            std::memcpy(u + so, tmp.data() + 2 * r, 2);           // s
+            std::memcpy(u + so + 2, tmp.data() + 2 * TR + 2 * r, 2);  // z
             for (uint32_t g = 0; g < groups; ++g) {
-                uint32_t pw[4], codes[32], out[4];
+                uint32_t pw[8], codes[32], out[8];
                 for (int i = 0; i < B; ++i) std::memcpy(&pw[i], planes + i * PS + r * nb8 + g * 4, 4);
-                for (int k = 0; k < 32; ++k) {
-                    uint32_t c = 0;
-                    for (int i = 0; i < B; ++i) c |= ((pw[i] >> k) & 1u) << i;
-                    codes[k] = c;
+                if (B <= 4) {
+                    for (int k = 0; k < 32; ++k) {
+                        uint32_t c = 0;
+                        for (int i = 0; i < B; ++i) c |= ((pw[i] >> k) & 1u) << i;
+                        codes[k] = c;
+                    }
+                    rp_pack(codes, B, out);
+                } else {
+                    for (int i = 0; i < B; ++i) out[i] = pw[i];
                 }
-                rp_pack(codes, B, out);
-                for (int i = 0; i < B; ++i) std::memcpy(planes + i * PS + r * nb8 + g * 4, &out[i], 4);
+                for (int i = 0; i < B; ++i)
+                    std::memcpy(u + 512 + lm_word_off(static_cast<uint32_t>(B), g >> 2, r, g & 3, static_cast<uint32_t>(i)), &out[i], 4);
             }
+        }
     }
 }
 

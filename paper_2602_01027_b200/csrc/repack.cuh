@@ -77,20 +77,31 @@ inline void rp_pack(const uint32_t* codes, int B, uint32_t* out) {
 // no magic offset to cancel.  Wider (5..8-bit) units put c at p = 0.
 __host__ __device__ constexpr int sub_pos(int B, int j) { return B <= 4 ? rp_pos(B, j) : 0; }
 
+// Logical right shift on the FMA pipe (IMAD.HI) instead of the ALU pipe
+// (SHF), which the unpack LOP3s saturate.
+#ifndef SFMP_SHR_IMAD
+#define SFMP_SHR_IMAD 0
+#endif
+template <int K>
+__device__ __forceinline__ uint32_t shr_k(uint32_t w) {
+    if constexpr (SFMP_SHR_IMAD) return __umulhi(w, 1u << (32 - K));
+    else return w >> K;
+}
+
 // Device: 16 f16x2 registers from the B repacked words, codes as subnormals
 // (one LOP3 AND per register; no magic exponent).
 template <int B>
 __device__ __forceinline__ void unpack_rp_sub(const uint32_t* w, uint32_t (&H)[16]) {
     uint32_t sh[B];
 #pragma unroll
-    for (int i = 0; i < B; ++i) sh[i] = w[i] >> (B == 4 ? 8 : B == 3 ? 9 : 10);
+    for (int i = 0; i < B; ++i) sh[i] = shr_k<(B == 4 ? 8 : B == 3 ? 9 : 10)>(w[i]);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if constexpr (B == 3) {
             if (j == 15) {
-                const uint32_t t1 = (w[1] >> 14) & 0x00020002u;
-                const uint32_t t2 = lop3_and_or(w[2] >> 13, 0x00040004u, t1);
-                H[15] = lop3_and_or(w[0] >> 15, 0x00010001u, t2);
+                const uint32_t t1 = shr_k<14>(w[1]) & 0x00020002u;
+                const uint32_t t2 = lop3_and_or(shr_k<13>(w[2]), 0x00040004u, t1);
+                H[15] = lop3_and_or(shr_k<15>(w[0]), 0x00010001u, t2);
                 continue;
             }
         }
@@ -124,6 +135,18 @@ __device__ __forceinline__ void unpack_rp(const uint32_t* w, uint32_t (&H)[16]) 
         const uint32_t mg = rp_magic_bits(B, j);
         H[j] = lop3_and_or(src, m | (m << 16), mg | (mg << 16));
     }
+}
+
+// Lane-major unit order of the decode GEMV (128-row units; gemv_tc.cu): the
+// compute warp cw (rows 32cw..32cw+31) lane (g, q) = 4g + q owns rows
+// 32cw + 8r + g (r = 0..3) and word q of each 16-byte row segment of a
+// 128-column chunk.  s/z: [cw][g][r] (s, z) fp16 pairs, 512 B.  Planes (after
+// the s/z block): [chunk c][cw][plane i][lane][r] 4-byte words.
+__host__ __device__ constexpr uint32_t lm_sz_off(uint32_t row) {
+    return (row >> 5) * 128 + (row & 7) * 16 + ((row >> 3) & 3) * 4;
+}
+__host__ __device__ constexpr uint32_t lm_word_off(uint32_t B, uint32_t c, uint32_t row, uint32_t q, uint32_t i) {
+    return c * (B * 2048) + (row >> 5) * (B * 512) + i * 512 + ((row & 7) * 4 + q) * 16 + ((row >> 3) & 3) * 4;
 }
 
 }  // namespace sfmpk
