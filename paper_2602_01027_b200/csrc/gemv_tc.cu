@@ -78,6 +78,15 @@ constexpr int kSmemSM = 225 * 1024;
 #ifndef SFMP_UNROLL_U
 #define SFMP_UNROLL_U 1
 #endif
+#ifndef SFMP_EXP_NOUNPACK
+#define SFMP_EXP_NOUNPACK 0
+#endif
+#ifndef SFMP_EXP_NOMMA
+#define SFMP_EXP_NOMMA 0
+#endif
+#ifndef SFMP_EXP_NOREC
+#define SFMP_EXP_NOREC 0
+#endif
 #ifndef SFMP_NOCOMPUTE
 #define SFMP_NOCOMPUTE 0
 #endif
@@ -468,7 +477,10 @@ __device__ __forceinline__ void unit_chunk(const uint8_t* pw, const uint8_t* con
     uint32_t A[2 * kMT][16];
 #pragma unroll
     for (int r = 0; r < 2 * kMT; ++r) {
-        if constexpr (B <= 4) unpack_rp_sub<B>(p[r], A[r]);  // repacked layout (repack.cuh)
+        if constexpr (SFMP_EXP_NOUNPACK) {  // experiment builds only: no unpack
+#pragma unroll
+            for (int j = 0; j < 16; ++j) A[r][j] = p[r][j % B];
+        } else if constexpr (B <= 4) unpack_rp_sub<B>(p[r], A[r]);  // repacked layout (repack.cuh)
         else unpack_word_sub<B>(p[r], A[r]);                // bit planes (unpack.cuh)
     }
 #pragma unroll
@@ -484,6 +496,10 @@ __device__ __forceinline__ void unit_chunk(const uint8_t* pw, const uint8_t* con
                 const uint32_t b0 = h ? b.z : b.x, b1 = h ? b.w : b.y;
 #pragma unroll
                 for (int m = 0; m < kMT; ++m) {
+                    if (SFMP_EXP_NOMMA) {  // experiment builds only: no tensor-core work
+                        cacc[m][nt][0] += __uint_as_float(A[2 * m][2 * s] ^ A[2 * m + 1][2 * s + 1] ^ b0 ^ b1);
+                        continue;
+                    }
                     mma_16816(cacc[m][nt], A[2 * m][2 * s], A[2 * m + 1][2 * s], A[2 * m][2 * s + 1],
                               A[2 * m + 1][2 * s + 1], b0, b1);
                     if constexpr (X2)
@@ -639,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                                               (fl << 20),
                                           static_cast<uint32_t>(rt), static_cast<uint32_t>(seg), 0u);
                     const uint32_t wbytes = unit_bytes(b0, nb8) + (nu > 1 ? unit_bytes(b1, nb8) : 0u);
-                    mbar_arrive_expect_tx(&full[s], wbytes + nu * sec);  // publishes sinfo[s]
+                    mbar_arrive_expect_tx(&full[s], wbytes + (SFMP_EXP_NOREC ? 0u : nu * sec));  // publishes sinfo[s]
                     bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d0 & 0xFFFFFFFFFFFFull), wbytes,
                              &full[s], pol);
                     // record sections of the units' bit-width layouts ([layout][BC]: one
@@ -650,7 +666,8 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                     const uint8_t* r1 = L.xrec + static_cast<size_t>(l1 * L.BC + bc + 1) * sec;
                     const bool one = nu == 1 || l0 == l1;
                     const uint32_t n0 = one ? nu * sec : sec;
-                    if (released) {
+                    if (SFMP_EXP_NOREC) {  // experiment builds only: records never copied
+                    } else if (released) {
                         issue_x(r0, xd, n0, s);
                         if (!one) issue_x(r1, xd + sec, sec, s);
                     } else {

@@ -26,20 +26,24 @@ int main() {
     float* d;
     cudaMalloc(&d, 4);
     const int iters = 20000;
+    for (int ch : {1, 2, 4, 8})
     for (int warps : {4, 8, 16, 32}) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
             cudaEventRecord(e0);
-            k<8><<<148, 32 * warps>>>(iters, d);
+            if (ch == 1) k<1><<<148, 32 * warps>>>(iters, d);
+            if (ch == 2) k<2><<<148, 32 * warps>>>(iters, d);
+            if (ch == 4) k<4><<<148, 32 * warps>>>(iters, d);
+            if (ch == 8) k<8><<<148, 32 * warps>>>(iters, d);
             cudaEventRecord(e1);
             cudaDeviceSynchronize();
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
-            double mmas = 148.0 * warps * iters * 8;
+            double mmas = 148.0 * warps * iters * ch;
             if (rep)
-                printf("warps/SM %2d: %.1f TFLOP/s, %.2f ns per MMA per SM-subcore (%s)\n", warps,
+                printf("chains %d warps/SM %2d: %.1f TFLOP/s, %.2f ns per MMA per SM-subcore (%s)\n", ch, warps,
                        mmas * 4096 / (ms * 1e-3) / 1e12, ms * 1e6 / (mmas / 148 / 4), cudaGetErrorString(cudaGetLastError()));
         }
     }
