@@ -9,9 +9,16 @@ GEMM calls, each through the decode GEMV kernel (K1).  Weights are rotated
 over 6 device copies of the layer (576 MB >> 126 MB L2), so every call
 streams its weights from HBM.
 
-N>1 (torchrun): each linear is N-sharded by the snake block-row partition,
-every rank runs its shard, the shard outputs are gathered with NCCL
-all_gather_into_tensor and un-permuted (strong scaling).
+N>1 (torchrun): each linear is N-sharded by the snake block-row partition;
+the whole step is ONE sfmp_gemm_sharded call: every rank runs its shards of
+all 35 problems into one packed buffer, ONE NCCL all-gather (the library's
+own communicator) moves them, ONE kernel un-permutes (strong scaling).
+
+Sub-results ("extras"): configs[0] (4096x4096 @3.5 bits, M=1) with the
+reference's CPU gemv beside it and the drop-in host-buffer call; the reorder
+overhead (mode none) and an n_b=256 point; configs[3] (Llama-3.1-70B linears
+@2.5 bits, decode step and prefill M=2048; sharded with kernel and collective
+time split when N>1); configs[4] (8192x28672 at 2/3/4 bits x M).
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref = /root/reference/proj compiled unmodified; else the C port) on
@@ -295,6 +302,207 @@ def prefill_leg(sfmp, port, models, dev, stream, args):
 
 
 # ---------------------------------------------------------------------------
+# GPU helpers
+# ---------------------------------------------------------------------------
+def graph_us(body, stream, reps, per=1):
+    """Capture body() in a CUDA graph, replay it `reps` times between CUDA
+    events on `stream`; microseconds per body() / per."""
+    import torch
+    with torch.cuda.stream(stream):
+        body()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        body()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / (reps * per)
+
+
+def roof(bytes_, flops, us, hbm, tc):
+    """t* = max(B/BW, FLOP/TC); fraction = t*/t."""
+    t_h, t_t = bytes_ / (hbm * 1e3), flops / (tc * 1e6)
+    return {"us": round(us, 2), "GBps": round(bytes_ / us / 1e3, 1), "TFLOPs": round(flops / us / 1e6, 1),
+            "bound": "hbm" if t_h >= t_t else "tensor", "frac": round(max(t_h, t_t) / us, 4)}
+
+
+def ws_for(sfmp, m, M):
+    import torch
+    n = m.workspace_bytes(16 if M <= 16 else M, sfmp.PATH_GEMV if M <= 16 else sfmp.PATH_AUTO)
+    return torch.zeros(max(n, 128), dtype=torch.uint8, device=f"cuda:{m.device}")
+
+
+# ---------------------------------------------------------------------------
+# sub-results (BASELINE.json configs[0], [3], [4]; SURVEY §8(d) extra points)
+# ---------------------------------------------------------------------------
+def single_linear_points(sfmp, port, dev, stream, hbm, tc, args):
+    """configs[0] (4096x4096, 3.5 bits, rowcol, M=1) with the reference CPU gemv
+    beside it, the drop-in host-buffer call, the reorder overhead (mode none,
+    PAPER.md:487) and an n_b=256 point."""
+    import torch
+    from synth import model_bytes
+    out = {}
+    copies = 32  # 32 x 7.9 MB >> L2
+    x1 = torch.from_numpy(port.gen_activation(1, 4096, 3001)).to(dev).to(torch.bfloat16)
+    for key, kw in (("config0", dict(mode=3)), ("mode_none", dict(mode=0)), ("n_b_256", dict(mode=3, n_b=256))):
+        data = model_bytes(port, 4096, 4096, 3.5, **kw)
+        ms = [sfmp.DeviceModel(data, device=dev.index) for _ in range(copies)]
+        ws = ws_for(sfmp, ms[0], 16)
+        y = torch.empty(1, 4096, device=dev)
+        us = graph_us(lambda: [m.gemm(x1, out=y, workspace=ws, stream=stream) for m in ms], stream, 20, copies)
+        b = algo_bytes(ms[0].info, 1, 4096, 4096)
+        out[key] = {"what": f"4096x4096 @3.5 bits {kw}, M=1, bf16 x", **roof(b, 2.0 * 4096 * 4096, us, hbm, tc)}
+        if key == "n_b_256":
+            xp = torch.from_numpy(port.gen_activation(2048, 4096, 3002)).to(dev).to(torch.bfloat16)
+            yp = torch.empty(2048, 4096, device=dev)
+            wsp = ws_for(sfmp, ms[0], 2048)
+            usp = graph_us(lambda: [m.gemm(xp, out=yp, workspace=wsp, stream=stream) for m in ms[:4]], stream, 5, 4)
+            out[key]["prefill_M2048"] = roof(algo_bytes(ms[0].info, 2048, 4096, 4096), 2.0 * 2048 * 4096 * 4096,
+                                             usp, hbm, tc)
+        if key == "config0":
+            # the drop-in call a reference user makes: host f32 in/out (sfmp_gemm_host,
+            # = sfmp::cuda::gemv in include/sfmp/cuda.hpp), synchronous per call
+            xh = port.gen_activation(1, 4096, 3001)
+            walls, devs = [], []
+            for i in range(60):
+                _, st = ms[i % copies].gemm_host(xh, stats=True)
+                if i >= 10:
+                    walls.append(st["wall_us"])
+                    devs.append(st["device_us"])
+            out["dropin_gemv_host"] = {
+                "what": "configs[0] through sfmp_gemm_host (host f32 x -> host y, H2D + kernels + D2H + sync per "
+                        "call), the call behind sfmp::cuda::gemv", "wall_us_median": round(statistics.median(walls), 2),
+                "device_us_median": round(statistics.median(devs), 2)}
+            try:
+                kind, hs = cpu_handles(port, {"c0": data})
+                if kind == "reference":
+                    r = hs["c0"].bench_gemv(xh[0], 5)
+                    out["config0"]["cpu_reference_gemv_us"] = round(r["median_us"], 1)
+                    out["config0"]["cpu_kind"] = "reference bench_gemv (lutgemm.cpp:137), 1 thread"
+            except Exception as e:  # the CPU leg is informative only
+                out["config0"]["cpu_reference_error"] = str(e)[:100]
+        del ms
+    out["reorder_overhead_pct"] = round(100.0 * (out["config0"]["us"] / out["mode_none"]["us"] - 1.0), 2)
+    torch.cuda.empty_cache()
+    return out
+
+
+def sweep_points(sfmp, port, dev, stream, hbm, tc, args):
+    """configs[4]: 8192x28672 at 2.0/3.0/4.0 bits x M, roofline fraction per point."""
+    import torch
+    from synth import model_bytes, prebuild
+    bits_l, Ms = (2.0, 3.0, 4.0), (1, 16, 64, 256, 2048)
+    prebuild([(8192, 28672, b, {}) for b in bits_l])
+    xs = {M: torch.from_numpy(port.gen_activation(M, 28672, 5000 + M)).to(dev).to(torch.bfloat16) for M in Ms}
+    out = {}
+    for b in bits_l:
+        data = model_bytes(port, 8192, 28672, b)
+        ms = [sfmp.DeviceModel(data, device=dev.index) for _ in range(2)]
+        for M in Ms:
+            y = torch.empty(M, 8192, device=dev)
+            ws = ws_for(sfmp, ms[0], M)
+            us = graph_us(lambda: [m.gemm(xs[M], out=y, workspace=ws, stream=stream) for m in ms], stream,
+                          10 if M <= 64 else 3, 2)
+            out[f"b{b}_M{M}"] = roof(algo_bytes(ms[0].info, M, 8192, 28672), 2.0 * M * 8192 * 28672, us, hbm, tc)
+        del ms
+        torch.cuda.empty_cache()
+    return out
+
+
+def llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args):
+    """configs[3]: the seven Llama-3.1-70B linears @2.5 bits (k/v m_b=128 so they
+    split 8 ways), decode step M in {1,2,4,8,16} as one call, prefill M=2048;
+    N>1: snake-sharded, ONE NCCL all-gather per call -- kernel and collective
+    time reported separately."""
+    import torch
+    from synth import LLAMA_70B, model_bytes, prebuild
+    specs = [(r, c, 2.5, {"m_b": 128 if p in ("k_proj", "v_proj") else 512}) for p, (r, c) in LLAMA_70B.items()]
+    prebuild(specs)
+    blobs = {p: model_bytes(port, r, c, 2.5, m_b=128 if p in ("k_proj", "v_proj") else 512)
+             for p, (r, c) in LLAMA_70B.items()}
+    copies = 2
+    mk = (lambda b: sfmp.DeviceModel(b, device=dev.index)) if world == 1 else \
+        (lambda b: sfmp.DeviceModel(b, device=dev.index, shard=rank, num_shards=world))
+    models = [{p: mk(blobs[p]) for p in PROJS} for _ in range(copies)]
+    out = {"workload": "llama3.1-70b decoder-layer linears @2.5 code bits (3/2 mix), rowcol; decode M in "
+                       "{1,2,4,8,16} (35 problems, one call) and prefill M=2048 (7 problems)",
+           "parallelism": "single GPU" if world == 1 else f"N-sharded x{world}, one NCCL all-gather per call"}
+    xs = {(p, M): torch.from_numpy(port.gen_activation(M, LLAMA_70B[p][1], 6000 + M)).to(dev).to(torch.bfloat16)
+          for p in PROJS for M in MS}
+    keys = [(p, M) for M in MS for p in PROJS]
+    ys = {k: torch.empty(k[1], LLAMA_70B[k[0]][0], device=dev) for k in keys}
+    wsm = {k: ws_for(sfmp, models[0][k[0]], k[1]) for k in keys}
+
+    def run(i, kk, local_only=False, bufs=None):
+        ms = [models[(i + j) % copies][p] for j, (p, M) in enumerate(kk)]
+        if world == 1:
+            sfmp.gemm_grouped(ms, [xs[k] for k in kk], outs=[ys[k] for k in kk], workspaces=[wsm[k] for k in kk],
+                              stream=stream)
+        elif local_only:
+            sfmp.gemm_sharded_local(ms, [xs[k] for k in kk], bufs, [wsm[k] for k in kk], stream=stream)
+        else:
+            sfmp.gemm_sharded(ms, [xs[k] for k in kk], [ys[k] for k in kk], [wsm[k] for k in kk], bufs, comm,
+                              stream=stream)
+
+    buf = None
+    if world > 1:
+        buf = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p, M in keys], [M for p, M in keys]) // 4,
+                          device=dev)
+    us = graph_us(lambda: [run(i, keys, bufs=buf) for i in range(copies)], stream, 10, copies)
+    byts = sum(algo_bytes(models[0][p].info, M, models[0][p].rows, LLAMA_70B[p][1]) for p, M in keys)
+    out["decode_step"] = {"M": MS, **roof(byts, sum(2.0 * M * models[0][p].rows * LLAMA_70B[p][1] for p, M in keys),
+                                          us, hbm, tc)}
+    if world > 1:
+        kus = graph_us(lambda: [run(i, keys, local_only=True, bufs=buf) for i in range(copies)], stream, 10, copies)
+        out["decode_step"].update({"kernel_us": round(kus, 2), "collective_and_unpermute_us": round(us - kus, 2),
+                                   "bytes_gathered_per_rank": buf.numel() * 4 // (1 + world) * world})
+    # prefill
+    Mp = 2048
+    xp = {p: torch.from_numpy(port.gen_activation(Mp, LLAMA_70B[p][1], 7000)).to(dev).to(torch.bfloat16) for p in PROJS}
+    yp = {p: torch.empty(Mp, LLAMA_70B[p][0], device=dev) for p in PROJS}
+    wsp = {p: ws_for(sfmp, models[0][p], Mp) for p in PROJS}
+    if world == 1:
+        per = {}
+        for p in PROJS:
+            t = graph_us(lambda: [models[c][p].gemm(xp[p], out=yp[p], workspace=wsp[p], stream=stream)
+                                  for c in range(copies)], stream, 3, copies)
+            r, c_ = LLAMA_70B[p]
+            per[p] = roof(algo_bytes(models[0][p].info, Mp, r, c_), 2.0 * Mp * r * c_, t, hbm, tc)
+        tot = sum(v["us"] for v in per.values())
+        fl = sum(2.0 * Mp * r * c for r, c in LLAMA_70B.values())
+        out["prefill"] = {"M": Mp, "us": round(tot, 1), "TFLOPs": round(fl / tot / 1e6, 1),
+                          "frac": round(fl / tot / 1e6 / tc, 4), "per_proj": per}
+    else:
+        pk = [(p, Mp) for p in PROJS]
+        pbuf = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p in PROJS], [Mp] * 7) // 4, device=dev)
+
+        def prun(local_only):
+            ms = [models[0][p] for p in PROJS]
+            if local_only:
+                sfmp.gemm_sharded_local(ms, [xp[p] for p in PROJS], pbuf, [wsp[p] for p in PROJS], stream=stream)
+            else:
+                sfmp.gemm_sharded(ms, [xp[p] for p in PROJS], [yp[p] for p in PROJS], [wsp[p] for p in PROJS], pbuf,
+                                  comm, stream=stream)
+        t = graph_us(lambda: prun(False), stream, 3)
+        tk = graph_us(lambda: prun(True), stream, 3)
+        fl = sum(2.0 * Mp * models[0][p].rows * LLAMA_70B[p][1] for p in PROJS)
+        out["prefill"] = {"M": Mp, "us": round(t, 1), "kernel_us": round(tk, 1),
+                          "collective_and_unpermute_us": round(t - tk, 1),
+                          "per_rank_TFLOPs": round(fl / tk / 1e6, 1), "frac_kernel": round(fl / tk / 1e6 / tc, 4),
+                          "problems": len(pk)}
+    del models
+    torch.cuda.empty_cache()
+    return out
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 def main():
@@ -307,12 +515,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--soak-ms", type=float, default=1500.0)
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip configs[0]/[3]/[4] sub-results")
     ap.add_argument("--no-group", action="store_true", help="one launch per linear instead of per decoder layer")
-    ap.add_argument("--group-per-m", action="store_true",
-                    help="one grouped call per M (5 launches) instead of one call for the whole step "
-                         "(the API then issues one launch per n-tile class: M<=8 and M=16)")
     ap.add_argument("--prefill-M", type=int, default=2048)
-    ap.add_argument("--e2e-order", default="", help="comma list: order of the M groups in the e2e step")
+    ap.add_argument("--e2e-order", default="", help="groups of token counts for the e2e step, e.g. '1/4/8/16/2'")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -327,58 +533,57 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        # the library's own NCCL communicator (sfmp_gemm_sharded): id over torch.distributed
+        uid = [sfmp.NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = sfmp.NcclComm(world, rank, local, uid[0])
     port = Port()
     blobs = {p: build_bytes(port, p) for p in PROJS}
-    # 6 device copies of the layer (each shard of it when world > 1)
+    # COPIES device copies of the layer (this rank's shard of it when world > 1)
     models = [{p: (sfmp.DeviceModel(blobs[p], device=local) if world == 1 else
                    sfmp.DeviceModel(blobs[p], device=local, shard=rank, num_shards=world))
                for p in PROJS} for _ in range(COPIES)]
     infos = {p: sfmp.parse_header(blobs[p]) for p in PROJS}
     xs = {(p, M): torch.from_numpy(port.gen_activation(M, SHAPES[p][1], 3000 + M)).to(dev)
           .to(torch.bfloat16) for p in PROJS for M in MS}
-    ys = {(p, M): torch.empty(M, models[0][p].out_rows, device=dev) for p in PROJS for M in MS}
-    ws = {p: models[0][p].workspace(16, sfmp.PATH_GEMV) for p in PROJS}
+    ys = {(p, M): torch.empty(M, SHAPES[p][0], device=dev) for p in PROJS for M in MS}
     # a workspace per (linear, M): problems of one launch must not share one
-    wsm = {(p, M): torch.zeros_like(ws[p]) for p in PROJS for M in MS}
+    wsm = {(p, M): ws_for(sfmp, models[0][p], 16) for p in PROJS for M in MS}
+    keys_all = [(p, M) for M in MS for p in PROJS]
+    gbuf = None
     if world > 1:
-        gath = {(p, M): torch.empty(world, M, models[0][p].out_rows, device=dev)
-                for p in PROJS for M in MS}
-        yfull = {(p, M): torch.empty(M, SHAPES[p][0], device=dev) for p in PROJS for M in MS}
-
+        gbuf = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p, M in keys_all],
+                                                     [M for p, M in keys_all]) // 4, device=dev)
     grouped = not args.no_group
-    across = grouped and not args.group_per_m and world == 1
-    # launches of OUR kernels per step: grouped = (x pre-pass + GEMV) per M;
-    # per-linear = (x pre-pass + GEMV) per call; sharded adds the un-permute
-    n_class = len({M > 8 for M in MS})
-    launches_per_step = ((n_class * 2 if across else len(MS) * 2) if grouped else len(MS) * len(PROJS) * 2) + \
-        (len(MS) * len(PROJS) if world > 1 else 0)
 
-    def step(i, group=grouped):
-        if group and across:
-            # the whole step (7 linears x 5 token counts, 4 weight copies) in one
-            # grouped call: one pre-pass + one GEMV launch per n-tile class
-            keys = [(p, M, (i * len(MS) + mi) % COPIES) for mi, M in enumerate(MS) for p in PROJS]
-            sfmp.gemm_grouped([models[c][p] for p, M, c in keys], [xs[(p, M)] for p, M, c in keys],
-                              outs=[ys[(p, M)] for p, M, c in keys], workspaces=[wsm[(p, M)] for p, M, c in keys])
-            return
-        for mi, M in enumerate(MS):
-            c = (i * len(MS) + mi) % COPIES
-            if group:
-                sfmp.gemm_grouped([models[c][p] for p in PROJS], [xs[(p, M)] for p in PROJS],
-                                  outs=[ys[(p, M)] for p in PROJS], workspaces=[ws[p] for p in PROJS])
+    def call(i, kk, local_only=False):
+        """One API call over the problems kk = [(proj, M)], weight copy rotating with i."""
+        ms = [models[(i * len(MS) + MS.index(M)) % COPIES][p] for p, M in kk]
+        if world == 1:
+            if grouped:
+                sfmp.gemm_grouped(ms, [xs[k] for k in kk], outs=[ys[k] for k in kk], workspaces=[wsm[k] for k in kk])
             else:
-                for p in PROJS:
-                    models[c][p].gemm(xs[(p, M)], out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
-            if world > 1:
-                for p in PROJS:
-                    dist.all_gather_into_tensor(gath[(p, M)], ys[(p, M)])
-                    models[c][p].unpermute_gathered(gath[(p, M)], M, out=yfull[(p, M)])
+                for m, k in zip(ms, kk):
+                    m.gemm(xs[k], out=ys[k], path=sfmp.PATH_GEMV, workspace=wsm[k])
+        elif local_only:
+            sfmp.gemm_sharded_local(ms, [xs[k] for k in kk], gbuf, [wsm[k] for k in kk])
+        else:
+            sfmp.gemm_sharded(ms, [xs[k] for k in kk], [ys[k] for k in kk], [wsm[k] for k in kk], gbuf, comm)
+
+    def step(i):
+        # the whole step (7 linears x 5 token counts) in ONE call: one pre-pass + one
+        # GEMV launch per n-tile class (M <= 8: 28 problems, M = 16: 7); N>1 adds ONE
+        # all-gather of every problem's shard rows and ONE un-permute launch
+        call(i, keys_all)
 
     # correctness spot check against the oracle (rank 0, cheap shapes)
+    n0 = sfmp.launch_count()
     step(0)
+    launches_per_step = sfmp.launch_count() - n0
     torch.cuda.synchronize()
     parity = {}
     if rank == 0:
@@ -386,10 +591,9 @@ def main():
         for p in ("q_proj", "k_proj"):
             w = port.load(blobs[p]).dequantize()
             ref = port.matmul(xs[(p, 16)].float().cpu().numpy(), w, threads=8)
-            got = (yfull if world > 1 else ys)[(p, 16)].cpu().numpy()
-            parity[p] = round(errors(got, ref)[0], 9)
+            parity[p] = round(errors(ys[(p, 16)].cpu().numpy(), ref)[0], 9)
 
-    use_graph = (world == 1) and not args.no_graph
+    use_graph = not args.no_graph
     stream = torch.cuda.Stream(device=dev)
     graphs = []
     if use_graph:
@@ -446,35 +650,29 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
 
-    # ---- secondary: the same step with one launch per linear (no grouping) ----
-    ungrouped_ms = None
-    if world == 1 and grouped and use_graph:
+    hbm, tc, src = peaks()
+    # ---- per-launch roofline: each n-tile class alone (its pre-pass + GEMV + fix-up),
+    # graph replay over the rotating copies, CUDA events on the launching stream ----
+    per_launch = {}
+    if world == 1 and grouped:
+        for name, kk in (("M<=8", [k for k in keys_all if k[1] <= 8]), ("M=16", [k for k in keys_all if k[1] > 8])):
+            with torch.cuda.stream(stream):
+                us = graph_us(lambda: [call(i, kk) for i in range(COPIES)], stream, max(3, args.steps // 5), COPIES)
+            b = sum(algo_bytes(models[0][p].info, M, models[0][p].rows, SHAPES[p][1]) for p, M in kk)
+            per_launch[name] = {"problems": len(kk), "bytes": b, **roof(b, sum(2.0 * M * SHAPES[p][0] * SHAPES[p][1]
+                                                                               for p, M in kk), us, hbm, tc)}
+    kernel_us = None
+    if world > 1:
         with torch.cuda.stream(stream):
-            step(0, group=False)
-        torch.cuda.synchronize()
-        ug = []
-        for i in range(COPIES):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                step(i, group=False)
-            ug.append(g)
-        reps = max(COPIES, args.steps // 2)
-        u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            for i in range(3):
-                ug[i % COPIES].replay()
-            u0.record(stream)
-            for i in range(reps):
-                ug[i % COPIES].replay()
-            u1.record(stream)
-        torch.cuda.synchronize()
-        ungrouped_ms = u0.elapsed_time(u1) / reps
+            kernel_us = graph_us(lambda: [call(i, keys_all, local_only=True) for i in range(COPIES)], stream,
+                                 max(3, args.steps // 5), COPIES)
 
     # ---- e2e: host buffers in, host buffers out, through the public API ----
     # One pinned host buffer holds every x of the step (f32, as the reference's
-    # Vector) and one every y: one H2D + the grouped calls + one D2H per step,
-    # replayed as a CUDA graph, then the host waits for y (the step's result).
-    keys = [(p, M) for M in MS for p in PROJS]
+    # Vector) and one every y; per group of token counts: H2D on a copy stream,
+    # the API call, D2H on a second copy stream (copies overlap the other
+    # groups' compute); CUDA graph per step; the host waits for y every step.
+    keys = keys_all
     xoff, yoff, xo, yo = {}, {}, 0, 0
     for k in keys:
         xoff[k], yoff[k] = xo, yo
@@ -490,29 +688,22 @@ def main():
     dx = {k: dxb[xoff[k]:xoff[k] + k[1] * SHAPES[k[0]][1]].view(k[1], SHAPES[k[0]][1]) for k in keys}
     dy = {k: dyb[yoff[k]:yoff[k] + k[1] * SHAPES[k[0]][0]].view(k[1], SHAPES[k[0]][0]) for k in keys}
     h2d, d2h = xo * 4, yo * 4
-
-    # group boundaries (x / y of one M are contiguous in the host buffers)
     gx = {M: (xoff[(PROJS[0], M)], xoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][1]) for M in MS}
     gy = {M: (yoff[(PROJS[0], M)], yoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][0]) for M in MS}
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-
-    # Group order of the e2e step: a small group first (short exposed H2D), the
-    # largest late enough that its H2D (2.5 MB, the slowest copy) hides under
-    # three groups' compute, a small group last (short exposed D2H).  Measured
-    # (200 steps each, noisy): 1,4,8,16,2 -> 247-283 us; 1,16,8,4,2 -> 270-350;
-    # 1,2,4,8,16 -> 290-348.
-    # --e2e-order: groups separated by '/', token counts by ',' (one grouped call
-    # per group; its H2D / D2H overlap the other groups' compute).  Measured
-    # (200 steps, two runs each): 1/4/8/16/2 244-245 us; 1,2/16/4,8 247-250;
-    # 1,2/4,8/16 259-268; 1/16/2,4,8 262-264; 1,2,4,8/16 296 -- finer groups
-    # overlap the PCIe copies better than fewer, larger launches.
+    # group order: a small group first (short exposed H2D) and last (short exposed D2H);
+    # finer groups overlap the PCIe copies better than fewer, larger launches (round 1)
     E2E_GROUPS = ([[int(v) for v in g.split(",")] for g in args.e2e_order.split("/")] if args.e2e_order
                   else [[1], [4], [8], [16], [2]])
-    E2E_MS = [M for g in E2E_GROUPS for M in g]
-    assert sorted(E2E_MS) == sorted(MS)
+    assert sorted(M for g in E2E_GROUPS for M in g) == sorted(MS)
+    ebufs = {}
+    if world > 1:
+        for gi_, grp in enumerate(E2E_GROUPS):
+            kk = [(p, M) for M in grp for p in PROJS]
+            ebufs[gi_] = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p, M in kk], [M for p, M in kk]) // 4,
+                                     device=dev)
 
     def e2e_body(i):
-        # copies of group k+1 (H2D) and k-1 (D2H) overlap the compute of group k
         cur = torch.cuda.current_stream()
         h2d_s.wait_stream(cur)
         d2h_s.wait_stream(cur)
@@ -527,22 +718,12 @@ def main():
                 ready.append(ev)
         for gi_, grp in enumerate(E2E_GROUPS):
             cur.wait_event(ready[gi_])
-            cs = {M: (i * len(MS) + MS.index(M)) % COPIES for M in grp}
+            kk = [(p, M) for M in grp for p in PROJS]
+            ms = [models[(i * len(MS) + MS.index(M)) % COPIES][p] for p, M in kk]
             if world == 1:
-                if grouped:
-                    keys = [(p, M) for M in grp for p in PROJS]
-                    sfmp.gemm_grouped([models[cs[M]][p] for p, M in keys], [dx[k] for k in keys],
-                                      outs=[dy[k] for k in keys], workspaces=[wsm[k] for k in keys])
-                else:
-                    for M in grp:
-                        for p in PROJS:
-                            models[cs[M]][p].gemm(dx[(p, M)], out=dy[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
+                sfmp.gemm_grouped(ms, [dx[k] for k in kk], outs=[dy[k] for k in kk], workspaces=[wsm[k] for k in kk])
             else:
-                for M in grp:
-                    for p in PROJS:
-                        models[cs[M]][p].gemm(dx[(p, M)], out=ys[(p, M)], path=sfmp.PATH_GEMV, workspace=ws[p])
-                        dist.all_gather_into_tensor(gath[(p, M)], ys[(p, M)])
-                        models[cs[M]][p].unpermute_gathered(gath[(p, M)], M, out=dy[(p, M)])
+                sfmp.gemm_sharded(ms, [dx[k] for k in kk], [dy[k] for k in kk], [wsm[k] for k in kk], ebufs[gi_], comm)
             done = torch.cuda.Event()
             done.record(cur)
             with torch.cuda.stream(d2h_s):
@@ -593,81 +774,97 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
 
+    # ---- sub-results (every rank takes part in the sharded 70B one) ----
+    extras = {}
+    if not args.no_extras:
+        with torch.cuda.stream(stream):
+            extras["llama70b"] = llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args)
+            if world == 1:
+                extras.update(single_linear_points(sfmp, port, dev, stream, hbm, tc, args))
+                extras["sweep_8192x28672"] = sweep_points(sfmp, port, dev, stream, hbm, tc, args)
+
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    hbm, tc, src = peaks()
-    # roofline over the GEMV launches of one step (per-rank bytes when sharded)
-    step_bytes = 0
-    small_bytes = 0  # the M <= 8 class launch
-    per_point = []
-    for p in PROJS:
-        rows_local = models[0][p].rows
-        info_local = models[0][p].info
-        for M in MS:
-            b = algo_bytes(info_local, M, rows_local, SHAPES[p][1])
-            step_bytes += b
-            small_bytes += b if M <= 8 else 0
-    n_launch = (n_class if across else len(MS)) if grouped else len(MS) * len(PROJS)  # GEMV launches per step
+    # roofline over the step (per-rank bytes when sharded)
+    step_bytes = sum(algo_bytes(models[0][p].info, M, models[0][p].rows, SHAPES[p][1]) for p, M in keys_all)
     t_us = t_ms * 1e3
-    # achieved = algorithmic bytes of one GEMV launch / its share of the step
-    # (each launch's time includes its x pre-pass: a lower bound on the kernel)
-    achieved = step_bytes / (t_us * 1e-6) / 1e9
+    step_ach = step_bytes / (t_us * 1e-6) / 1e9
+    dom = per_launch.get("M<=8")
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_gemv_grouped_8b_Mle8.json" if across else
-                        "r01_ncu_gemv_grouped_8b_M1.json")
-    if os.path.exists(prof):
-        try:
-            mb = json.load(open(prof))["metrics"]["dram__bytes_read.sum"].split()[0]
-            wb = json.load(open(prof))["metrics"]["dram__bytes_write.sum"].split()[0]
-            traffic = round((float(mb) + float(wb)) * 1e6)  # ncu --set full, one gemv_kernel launch
-        except Exception:
-            traffic = None
+    for prof in ("r02_ncu_gemv_grouped_8b_Mle8.json", "r01_ncu_gemv_grouped_8b_Mle8.json"):
+        path = os.path.join(ROOT, "profiles", prof)
+        if os.path.exists(path):
+            try:
+                mt = json.load(open(path))["metrics"]
+                traffic = round((float(mt["dram__bytes_read.sum"].split()[0]) +
+                                 float(mt["dram__bytes_write.sum"].split()[0])) * 1e6)
+                traffic_src = prof
+                break
+            except Exception:
+                traffic = None
+    if dom:
+        roofline = {"bound": "hbm", "achieved": dom["GBps"], "peak": hbm, "unit": "GB/s",
+                    "frac": round(dom["GBps"] / hbm, 4), "traffic": traffic,
+                    "kernel": "the step's M<=8 grouped launch (28 problems: x pre-pass + gemv_kernel + fix-up), "
+                              f"{dom['us']} us for {dom['bytes']} algorithmic bytes",
+                    "traffic_note": f"dram read+write of that gemv_kernel launch, profiles/{traffic_src}" if traffic
+                    else None, "per_launch": per_launch,
+                    "step_achieved": round(step_ach, 1), "step_frac": round(step_ach / hbm, 4),
+                    "algorithmic_bytes_per_step": step_bytes, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
+    else:
+        roofline = {"bound": "hbm", "achieved": round(step_ach, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(step_ach / hbm, 4), "traffic": None,
+                    "kernel": "whole step (per-rank bytes / step time)" if world > 1 else "whole step",
+                    "algorithmic_bytes_per_step": step_bytes, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
+        if kernel_us:
+            roofline.update({"kernel_us": round(kernel_us, 2), "collective_and_unpermute_us": round(t_us - kernel_us, 2),
+                             "kernel_frac": round(step_bytes / (kernel_us * 1e-6) / 1e9 / hbm, 4)})
     out = {
         "metric": METRIC, "value": round(t_us, 2), "unit": "us", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 5),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "avg_code_bits": AVG_BITS, "M": MS,
-                   "projections": PROJS, "kernel": "K1 decode GEMV (gemv_kernel) + x pre-pass (xprep_kernel)",
-                   "launch_grouping": (("the whole step is one grouped call (sfmp_gemm_grouped_v, a token count "
-                                        "per problem): one pre-pass + one GEMV launch for the 28 M<=8 problems, "
-                                        "one for the 7 M=16 problems") if across else
-                                       ("the 7 linears of one M share one pre-pass + one GEMV launch "
-                                        "(sfmp_gemm_grouped)")) if grouped else "one launch per linear",
-                   "ungrouped_step_us": round(ungrouped_ms * 1e3, 2) if ungrouped_ms else None,
+        "config": {"workload": WORKLOAD, "avg_code_bits": AVG_BITS, "M": MS, "projections": PROJS,
+                   "kernel": "K1 decode GEMV (gemv_kernel) + x pre-pass (xprep_rows_kernel) + fix-up",
+                   "launch_grouping": ("the whole step is one call (sfmp_gemm_grouped_v): one pre-pass + one GEMV "
+                                       "launch for the 28 M<=8 problems, one for the 7 M=16 problems"
+                                       if grouped else "one launch per linear") +
+                                      ("; sfmp_gemm_sharded: + ONE NCCL all-gather of all 35 problems' shard rows "
+                                       "and ONE un-permute launch" if world > 1 else ""),
                    "l2": f"inputs larger than L2: {COPIES} rotating device copies of the layer "
                          f"({sum(i['payload_bytes'] for i in infos.values()) * COPIES / 1e6:.0f} MB)",
                    "cuda_graph": use_graph,
                    "parallelism": "single GPU" if world == 1 else
-                   f"N-sharded x{world} (snake block rows) + NCCL all-gather + unpermute",
+                   f"N-sharded x{world} (snake block rows), one NCCL all-gather per step (library communicator)",
                    "parity_max_rel_err_M16": parity},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
-                     "algorithmic_bytes_per_step": step_bytes,
-                     "algorithmic_bytes_per_launch": step_bytes // n_launch,
-                     "traffic_note": ("dram read+write of the step's M<=8 gemv_kernel launch (28 problems; "
-                                      f"algorithmic {small_bytes} B), profiles/r01_ncu_gemv_grouped_8b_Mle8.json")
-                     if across else ("dram read+write of one grouped M=1 gemv_kernel launch "
-                                     "(profiles/r01_ncu_gemv_grouped_8b_M1.json)"),
-                     "avg_launch_us": round(t_us / n_launch, 3), "launches_per_step": n_launch},
+        "roofline": roofline,
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "api": ("pinned host x -> H2D per M group on a copy stream, sfmp_gemm_grouped per M, "
-                       "D2H per group on a second copy stream (copies overlap compute); CUDA graph "
-                       "per step, host synchronises on y every step"), "groups": E2E_GROUPS,
+                "d2h_bytes_per_step": d2h,
+                "api": ("pinned host x -> H2D per M group on a copy stream, one sfmp_gemm_grouped_v "
+                        + ("" if world == 1 else "/ sfmp_gemm_sharded ") +
+                        "call per group, D2H per group on a second copy stream (copies overlap compute); CUDA "
+                        "graph per step, host synchronises on y every step"), "groups": E2E_GROUPS,
                 "event_us": round(e2e_event_ms * 1e3, 2), "wall_us": round(e2e_wall_ms * 1e3, 2)},
         "gpu_launches": args.steps * launches_per_step,
+        "gpu_launches_note": f"{launches_per_step} kernels per step, counted by sfmp_launch_count() "
+                             f"when the step was enqueued",
         "clocks": clk,
     }
+    if extras:
+        out["extras"] = extras
     if world == 1 and not args.no_prefill:
         out["prefill"] = prefill_leg(sfmp, port, models, dev, stream, args)
         out["dense_cublas_bf16_step"] = dense_leg(dev, stream, xs, args)
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_sample(port, blobs)
     print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -11,6 +11,8 @@
 // are the reference's own; link libsfmp_b200.so.  See INTEGRATION.md.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -88,14 +90,59 @@ private:
     sfmp_model_info info_{};
 };
 
-// y = W x for host vectors (the reference signature).  GemvStats::lookups has
-// no GPU meaning and stays 0; the timing fields are left untouched.
+// y = W x for host vectors (the reference signature).  GemvStats
+// (lutgemm.hpp:47-52) is filled from the GPU call's own measurements:
+// accumulate_us = device time of the kernels (gather, contraction and
+// scatter are fused into them, so reorder_us = 0); there are no lookup tables
+// (the tensor cores contract the exact codes), so lookups = 0 and
+// lut_build_us = 0.
 inline Vector gemv(const DeviceModel& model, const Vector& x, GemvStats* stats = nullptr) {
-    (void)stats;
     if (x.data.size() != model.info().cols) throw ShapeError("gemv: x.len != model cols");
     std::vector<float> y(model.info().out_rows);
-    check(sfmp_gemm_host(model.handle(), x.data.data(), 1, y.data(), nullptr));
+    sfmp_stats st{};
+    check(sfmp_gemm_host_stats(model.handle(), x.data.data(), 1, y.data(), nullptr, stats ? &st : nullptr));
+    if (stats) {
+        stats->lookups = 0;
+        stats->lut_build_us = 0.0;
+        stats->accumulate_us = st.device_us;
+        stats->reorder_us = 0.0;
+    }
     return Vector(std::move(y));
+}
+
+// The full GPU statistics of one call (device / copy / wall time, bytes, path, launches).
+inline Vector gemv_ex(const DeviceModel& model, const Vector& x, sfmp_stats* stats) {
+    if (x.data.size() != model.info().cols) throw ShapeError("gemv: x.len != model cols");
+    std::vector<float> y(model.info().out_rows);
+    check(sfmp_gemm_host_stats(model.handle(), x.data.data(), 1, y.data(), nullptr, stats));
+    return Vector(std::move(y));
+}
+
+// bench_gemv (lutgemm.cpp:137-179) over the GPU drop-in: the same
+// repetitions, percentiles (index llround(q*(n-1)) of the sorted host
+// wall times) and ConfigError for reps < 1.
+inline BenchResult bench_gemv(const DeviceModel& model, const Vector& x, size_t reps) {
+    if (reps < 1) throw ConfigError("bench_gemv: repetitions must be >= 1");
+    std::vector<double> totals;
+    totals.reserve(reps);
+    for (size_t r = 0; r < reps; ++r) {
+        sfmp_stats st{};
+        (void)gemv_ex(model, x, &st);
+        totals.push_back(st.wall_us);
+    }
+    std::sort(totals.begin(), totals.end());
+    auto pct = [&](double q) { return totals[static_cast<size_t>(std::llround(q * static_cast<double>(totals.size() - 1)))]; };
+    BenchResult res;
+    res.rows = model.info().out_rows;
+    res.cols = model.info().cols;
+    res.reps = reps;
+    res.median_us = pct(0.5);
+    res.p10_us = reps > 1 ? pct(0.10) : std::nan("");
+    res.p90_us = reps > 1 ? pct(0.90) : std::nan("");
+    res.lut_build_us = 0.0;
+    res.reorder_us = 0.0;
+    res.lookups = 0;
+    return res;
 }
 
 // Exact drop-in for sfmp::gemv(const PackedModel&, ...): uploads per call.
@@ -108,6 +155,23 @@ inline Vector gemv(const PackedModel& model, const Vector& x, GemvStats* stats =
 // x_host [M][cols] -> y_host [M][rows], both row-major host arrays.
 inline void gemm_host(const DeviceModel& model, const float* x_host, int64_t M, float* y_host) {
     check(sfmp_gemm_host(model.handle(), x_host, M, y_host, nullptr));
+}
+
+// Sharded decode/prefill of several linears with ONE NCCL all-gather
+// (multi-GPU).  models: this rank's shards (DeviceModel built
+// with sfmp_model_create_shard); xs/ys/workspaces: device pointers;
+// gather_buf: sfmp_sharded_gather_bytes() bytes of device memory;
+// comm: an ncclComm_t with size/rank = shard count/index.
+inline void gemm_sharded(const std::vector<const sfmp_dev_model*>& models, const std::vector<const void*>& xs,
+                         sfmp_dtype dtype, const std::vector<int64_t>& Ms, const std::vector<float*>& ys,
+                         const std::vector<void*>& workspaces, void* gather_buf, size_t gather_bytes, void* comm,
+                         void* stream = nullptr) {
+    const int n = static_cast<int>(models.size());
+    if (xs.size() != models.size() || Ms.size() != models.size() || ys.size() != models.size() ||
+        workspaces.size() != models.size())
+        throw ShapeError("gemm_sharded: argument lists differ in length");
+    check(sfmp_gemm_sharded(models.data(), xs.data(), dtype, Ms.data(), ys.data(), workspaces.data(), nullptr, n,
+                            gather_buf, gather_bytes, comm, stream));
 }
 
 }  // namespace cuda

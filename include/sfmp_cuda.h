@@ -20,8 +20,13 @@
  *    column/row order: the col_perm gather (reorder_activation_in,
  *    reorder.cpp:103-111) and row_perm scatter (reorder_activation_out,
  *    reorder.cpp:113-121) happen inside the kernels.
- *  - Results are deterministic and independent of grid size and stream
- *    (no floating-point atomics; fixed-order split-K).
+ *  - Results are deterministic and independent of the parallel
+ *    decomposition: every output element is summed in a
+ *    canonical order fixed by the matrix shape alone (decode GEMV: fixed
+ *    1024-column K segments added in segment order; prefill GEMM: fixed
+ *    K chunks), so the bits do not depend on the grid, the SM count, the
+ *    stream, the other problems of a grouped call, the shard count, or M.
+ *    No floating-point atomics.
  *  - Everything is stream-ordered on the caller's stream.  Calls on distinct
  *    streams are safe when each passes its own workspace (or workspace=NULL
  *    is used from one stream at a time).
@@ -38,7 +43,8 @@
 extern "C" {
 #endif
 
-#define SFMP_CUDA_ABI_VERSION 1
+#define SFMP_CUDA_ABI_VERSION 2
+#define SFMP_NCCL_ID_BYTES 128
 
 /* Status codes, 1:1 with the reference exception kinds (errors.hpp:9-36). */
 typedef enum sfmp_status {
@@ -183,6 +189,35 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
 sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M,
                            float* y_host, void* stream);
 
+/* ---- call statistics (GemvStats, lutgemm.hpp:47-52; filled at lutgemm.cpp:127-132) ---- */
+typedef struct sfmp_stats {
+    double device_us;       /* kernel time of the call on its stream (CUDA events)              */
+    double h2d_us, d2h_us;  /* host-buffer entry only: copy times (CUDA events)                 */
+    double wall_us;         /* host wall-clock time of the whole call                           */
+    uint64_t bytes;         /* algorithmic HBM bytes: planes + s,z + perms + x + y  */
+    double flops;           /* 2 * M * rows * cols                                              */
+    int32_t path;           /* kernel path taken (sfmp_path)                                     */
+    int32_t launches;       /* kernels the call enqueued                                         */
+} sfmp_stats;
+/* sfmp_gemm_ex that also fills *stats; with stats != NULL the call
+ * synchronises its stream (as the reference's GemvStats timing is blocking). */
+sfmp_status sfmp_gemm_stats(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M,
+                            float* y, void* workspace, size_t workspace_bytes, sfmp_path path,
+                            void* stream, sfmp_stats* stats);
+/* sfmp_gemm_host that also fills *stats (NULL allowed). */
+sfmp_status sfmp_gemm_host_stats(const sfmp_dev_model* model, const float* x_host, int64_t M,
+                                 float* y_host, void* stream, sfmp_stats* stats);
+/* Kernels enqueued by this host thread so far (every entry point counts its
+ * launches; a CUDA-graph capture counts the captured launches once). */
+uint64_t sfmp_launch_count(void);
+
+/* gemv_block (lutgemm.hpp:44-45, lutgemm.cpp:87-93): out[m_b] = the
+ * contribution of block k (block-row-major, as PackedModel::blocks) to its
+ * m_b rows in STORED row order, from the REORDERED activation x_reordered
+ * (device f32, cols entries: x[col_perm[j]], reorder.cpp:103-111). */
+sfmp_status sfmp_gemv_block(const sfmp_dev_model* model, uint64_t block, const float* x_reordered,
+                            float* out, void* stream);
+
 /* K3 (debug/parity): dense f32 W[rows][cols] in ORIGINAL order, bit-exact
  * with dequantize_model (layout.cpp:316-332; quantizer.cpp:50-55). */
 sfmp_status sfmp_dequantize(const sfmp_dev_model* model, float* w, void* stream);
@@ -196,6 +231,39 @@ sfmp_status sfmp_unpack_codes(const sfmp_dev_model* model, uint8_t* codes, void*
  * may be any shard of the same matrix (all shards carry the global map). */
 sfmp_status sfmp_unpermute_gathered(const sfmp_dev_model* model, const float* gathered,
                                     int64_t M, float* y, void* stream);
+
+/* ---- sharded calls: many problems, ONE collective -------- */
+/* models[i] are shards (sfmp_model_create_shard) with the same shard index and
+ * count on one device; problem i has Ms[i] tokens.  Each rank writes its
+ * problems' shard outputs y_local[Ms[i]][shard_rows_i] back to back into the
+ * send block of gather_buf; an all-gather of that block (total floats) into
+ * the receive block that follows it ([num_shards][total]) gives every rank
+ * every row; one kernel scatters them to ys[i][Ms[i]][global rows] in the
+ * ORIGINAL row order.  Bit-identical to the unsharded sfmp_gemm. */
+/* Bytes of gather_buf: (1 + num_shards) * sum_i Ms[i] * shard_rows_i * 4. */
+sfmp_status sfmp_sharded_gather_bytes(const sfmp_dev_model* const* models, const int64_t* Ms, int count,
+                                      size_t* bytes);
+/* Step 1: the shard GEMMs into the send block (one grouped call). */
+sfmp_status sfmp_gemm_sharded_local(const sfmp_dev_model* const* models, const void* const* xs,
+                                    sfmp_dtype dtype, const int64_t* Ms, void* const* workspaces,
+                                    const size_t* workspace_bytes, int count, void* gather_buf,
+                                    void* stream);
+/* Step 3 (after the caller's all-gather of the send block into the receive
+ * block): scatter every problem's rows to ys in original order (one launch). */
+sfmp_status sfmp_sharded_unpermute(const sfmp_dev_model* const* models, const int64_t* Ms, int count,
+                                   const void* gather_buf, float* const* ys, void* stream);
+/* Steps 1-3 with NCCL: nccl_comm is an ncclComm_t whose size/rank equal the
+ * shard count/index.  NCCL failures return SFMP_ERR_NCCL.  Stream-ordered and
+ * CUDA-graph capturable. */
+sfmp_status sfmp_gemm_sharded(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                              const int64_t* Ms, float* const* ys, void* const* workspaces,
+                              const size_t* workspace_bytes, int count, void* gather_buf,
+                              size_t gather_bytes, void* nccl_comm, void* stream);
+/* NCCL helpers for callers without a communicator (libnccl.so.2 is loaded at
+ * run time; in a PyTorch process that is torch's NCCL). id: SFMP_NCCL_ID_BYTES. */
+sfmp_status sfmp_nccl_unique_id(uint8_t* id);
+sfmp_status sfmp_nccl_comm_init(int nranks, const uint8_t* id, int rank, int device, void** comm);
+sfmp_status sfmp_nccl_comm_destroy(void* comm);
 
 #ifdef __cplusplus
 }

@@ -49,6 +49,23 @@ int main(int argc, char** argv) {
         const sfmp::Vector y1 = sfmp::cuda::gemv(pm, sfmp::Vector(xv), nullptr);
         if (y1.data.size() != pm.rows) return 3;
     }
+    // GemvStats filled from the GPU call (lutgemm.hpp:47-52); bench_gemv's ConfigError (lutgemm.cpp:138)
+    bool ok_stats = false, ok_cfg = false;
+    {
+        std::vector<float> xv(n);
+        std::memcpy(xv.data(), xb.data(), n * 4);
+        sfmp::GemvStats st;
+        (void)sfmp::cuda::gemv(dm, sfmp::Vector(xv), &st);
+        ok_stats = st.accumulate_us > 0.0 && st.lookups == 0;
+        const sfmp::BenchResult br = sfmp::cuda::bench_gemv(dm, sfmp::Vector(xv), 5);
+        ok_stats = ok_stats && br.median_us > 0.0 && br.p10_us <= br.median_us && br.median_us <= br.p90_us &&
+                   br.rows == pm.rows;
+        try {
+            (void)sfmp::cuda::bench_gemv(dm, sfmp::Vector(xv), 0);
+        } catch (const sfmp::ConfigError&) {
+            ok_cfg = true;
+        }
+    }
     bool ok_err = false;
     try {
         std::vector<uint8_t> bad = bytes;
@@ -63,6 +80,7 @@ int main(int argc, char** argv) {
     } catch (const sfmp::ShapeError&) {
         ok_shape = true;
     }
-    std::printf("dropin max_rel=%.3e format_error=%d shape_error=%d\n", worst, ok_err, ok_shape);
-    return (worst <= 1e-3 && ok_err && ok_shape) ? 0 : 1;
+    std::printf("dropin max_rel=%.3e format_error=%d shape_error=%d stats=%d config_error=%d\n", worst, ok_err,
+                ok_shape, ok_stats, ok_cfg);
+    return (worst <= 1e-3 && ok_err && ok_shape && ok_stats && ok_cfg) ? 0 : 1;
 }

@@ -40,8 +40,12 @@ EXPORTED_SYMBOLS = (
     "sfmp_model_create_from_parts", "sfmp_model_create_shard", "sfmp_model_destroy",
     "sfmp_model_get_info", "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
     "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered", "sfmp_shard_plan",
-    "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v",
+    "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v", "sfmp_gemm_stats",
+    "sfmp_gemm_host_stats", "sfmp_launch_count", "sfmp_sharded_gather_bytes", "sfmp_gemm_sharded_local",
+    "sfmp_sharded_unpermute", "sfmp_gemm_sharded", "sfmp_nccl_unique_id", "sfmp_nccl_comm_init",
+    "sfmp_nccl_comm_destroy", "sfmp_gemv_block",
 )
+NCCL_ID_BYTES = 128
 
 
 class SfmpError(RuntimeError):
@@ -83,6 +87,16 @@ class ModelInfo(C.Structure):
                 ("avg_code_bits", C.c_double), ("payload_bytes", C.c_uint64),
                 ("device_bytes", C.c_uint64), ("shard", C.c_uint32), ("num_shards", C.c_uint32),
                 ("out_rows", C.c_uint64), ("global_rows", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Stats(C.Structure):
+    """sfmp_stats: the GPU counterpart of GemvStats (lutgemm.hpp:47-52)."""
+    _fields_ = [("device_us", C.c_double), ("h2d_us", C.c_double), ("d2h_us", C.c_double),
+                ("wall_us", C.c_double), ("bytes", C.c_uint64), ("flops", C.c_double),
+                ("path", C.c_int32), ("launches", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -130,11 +144,25 @@ def lib() -> C.CDLL:
     L.sfmp_gemm_grouped.argtypes = [vp, vp, C.c_int, i64, vp, vp, vp, C.c_int, vp]
     L.sfmp_gemm_grouped_v.argtypes = [vp, vp, C.c_int, vp, vp, vp, vp, C.c_int, vp]
     L.sfmp_shard_extract.argtypes = [vp, sz, C.c_uint32, C.c_uint32, vp, C.POINTER(C.c_size_t)]
+    L.sfmp_gemm_stats.argtypes = [vp, vp, C.c_int, i64, vp, vp, sz, C.c_int, vp, C.POINTER(Stats)]
+    L.sfmp_gemm_host_stats.argtypes = [vp, vp, i64, vp, vp, C.POINTER(Stats)]
+    L.sfmp_launch_count.restype = C.c_uint64
+    L.sfmp_sharded_gather_bytes.argtypes = [vp, vp, C.c_int, C.POINTER(sz)]
+    L.sfmp_gemm_sharded_local.argtypes = [vp, vp, C.c_int, vp, vp, vp, C.c_int, vp, vp]
+    L.sfmp_sharded_unpermute.argtypes = [vp, vp, C.c_int, vp, vp, vp]
+    L.sfmp_gemm_sharded.argtypes = [vp, vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, sz, vp, vp]
+    L.sfmp_nccl_unique_id.argtypes = [vp]
+    L.sfmp_nccl_comm_init.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)]
+    L.sfmp_nccl_comm_destroy.argtypes = [vp]
+    L.sfmp_gemv_block.argtypes = [vp, C.c_uint64, vp, vp, vp]
     for name in ("sfmp_parse_header", "sfmp_block_offsets", "sfmp_model_create",
                  "sfmp_model_create_shard", "sfmp_model_destroy", "sfmp_model_get_info",
                  "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
                  "sfmp_dequantize", "sfmp_unpack_codes", "sfmp_unpermute_gathered",
-                 "sfmp_shard_plan", "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v"):
+                 "sfmp_shard_plan", "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v",
+                 "sfmp_gemm_stats", "sfmp_gemm_host_stats", "sfmp_sharded_gather_bytes",
+                 "sfmp_gemm_sharded_local", "sfmp_sharded_unpermute", "sfmp_gemm_sharded",
+                 "sfmp_nccl_unique_id", "sfmp_nccl_comm_init", "sfmp_nccl_comm_destroy", "sfmp_gemv_block"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -157,6 +185,11 @@ def check(status: int) -> None:
     e = SfmpError(f"{lib().sfmp_status_string(status).decode()}: {msg}")
     e.code = status
     raise e
+
+
+def launch_count() -> int:
+    """Kernels enqueued by this host thread through the library so far."""
+    return int(lib().sfmp_launch_count())
 
 
 def device_count() -> int:
@@ -284,14 +317,45 @@ class DeviceModel:
                                  ws.numel() if ws is not None else 0, path, _stream_ptr(stream)))
         return out
 
-    def gemm_host(self, x: np.ndarray) -> np.ndarray:
-        """Reference calling convention: host f32 in, host f32 out (copies inside)."""
+    def gemm_stats(self, x, out=None, path: int = PATH_AUTO, workspace=None, stream=None):
+        """gemm() that also returns the call's sfmp_stats (synchronises the stream)."""
+        import torch
+        if x.dim() == 1:
+            x = x.unsqueeze(0)
+        x = x.contiguous()
+        M = x.shape[0]
+        if out is None:
+            out = torch.empty(M, self.out_rows, dtype=torch.float32, device=x.device)
+        ws = workspace if workspace is not None else self.workspace(M, path)
+        st = Stats()
+        check(lib().sfmp_gemm_stats(self._h, C.c_void_p(x.data_ptr()), _dtype_code(x), M,
+                                    C.c_void_p(out.data_ptr()),
+                                    C.c_void_p(ws.data_ptr()) if ws is not None else None,
+                                    ws.numel() if ws is not None else 0, path, _stream_ptr(stream),
+                                    C.byref(st)))
+        return out, st.as_dict()
+
+    def gemm_host(self, x: np.ndarray, stats: bool = False):
+        """Reference calling convention: host f32 in, host f32 out (copies inside).
+        stats=True also returns the sfmp_stats dict (GemvStats counterpart)."""
         x = np.ascontiguousarray(np.atleast_2d(x), np.float32)
         if x.shape[-1] != self.cols:
             raise ShapeError("gemv: x.len != model cols")
         y = np.empty((x.shape[0], self.out_rows), np.float32)
-        check(lib().sfmp_gemm_host(self._h, x.ctypes.data, x.shape[0], y.ctypes.data, None))
-        return y
+        st = Stats()
+        check(lib().sfmp_gemm_host_stats(self._h, x.ctypes.data, x.shape[0], y.ctypes.data, None,
+                                         C.byref(st) if stats else None))
+        return (y, st.as_dict()) if stats else y
+
+    def gemv_block(self, block: int, x_reordered, stream=None):
+        """gemv_block (lutgemm.cpp:87-93): the m_b-row contribution of block k to
+        y in STORED (reordered) row order, from the reordered x (device f32)."""
+        import torch
+        out = torch.empty(self.info["m_b"], dtype=torch.float32, device=x_reordered.device)
+        x_reordered = x_reordered.contiguous().float()
+        check(lib().sfmp_gemv_block(self._h, block, C.c_void_p(x_reordered.data_ptr()),
+                                    C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
 
     def dequantize(self, stream=None):
         import torch
@@ -349,3 +413,84 @@ def gemv(model: DeviceModel, x, stream=None):
     """sfmp::gemv (lutgemm.hpp:57): one token (or M tokens looped, SPEC.md:551)."""
     y = model.gemm(x, stream=stream)
     return y[0] if x.dim() == 1 else y
+
+
+# ---------------------------------------------------------------------------
+# Sharded calls: several N-sharded linears, ONE collective (DESIGN.md §6)
+# ---------------------------------------------------------------------------
+class NcclComm:
+    """An NCCL communicator created through the library (libnccl.so.2 at run
+    time).  The unique id travels over any channel, e.g. torch.distributed."""
+
+    def __init__(self, nranks: int, rank: int, device: int, uid: bytes):
+        self._h = C.c_void_p()
+        buf = (C.c_uint8 * NCCL_ID_BYTES).from_buffer_copy(uid)
+        check(lib().sfmp_nccl_comm_init(nranks, buf, rank, device, C.byref(self._h)))
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * NCCL_ID_BYTES)()
+        check(lib().sfmp_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib().sfmp_nccl_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def _ptr_array(vals):
+    return (C.c_void_p * len(vals))(*vals)
+
+
+def sharded_gather_bytes(models, Ms) -> int:
+    n = C.c_size_t(0)
+    check(lib().sfmp_sharded_gather_bytes(_ptr_array([m.handle for m in models]),
+                                          (C.c_int64 * len(Ms))(*Ms), len(models), C.byref(n)))
+    return int(n.value)
+
+
+def packed_offsets(models, Ms):
+    """Float offsets of each problem in one rank's send block (+ total)."""
+    off = [0]
+    for m, M in zip(models, Ms):
+        off.append(off[-1] + M * m.out_rows)
+    return off
+
+
+def gemm_sharded_local(models, xs, gather_buf, workspaces, stream=None):
+    """Step 1 of a sharded call: the shard GEMMs into the send block of gather_buf."""
+    n = len(models)
+    xs = [x.contiguous() for x in xs]
+    check(lib().sfmp_gemm_sharded_local(
+        _ptr_array([m.handle for m in models]), _ptr_array([x.data_ptr() for x in xs]), _dtype_code(xs[0]),
+        (C.c_int64 * n)(*[x.shape[0] for x in xs]), _ptr_array([w.data_ptr() for w in workspaces]),
+        (C.c_size_t * n)(*[w.numel() for w in workspaces]), n, C.c_void_p(gather_buf.data_ptr()),
+        _stream_ptr(stream)))
+
+
+def sharded_unpermute(models, Ms, gather_buf, outs, stream=None):
+    """Step 3: every problem's gathered rows to outs[i][M_i, global rows] (one launch)."""
+    n = len(models)
+    check(lib().sfmp_sharded_unpermute(_ptr_array([m.handle for m in models]), (C.c_int64 * n)(*Ms), n,
+                                       C.c_void_p(gather_buf.data_ptr()), _ptr_array([y.data_ptr() for y in outs]),
+                                       _stream_ptr(stream)))
+    return outs
+
+
+def gemm_sharded(models, xs, outs, workspaces, gather_buf, comm: NcclComm, stream=None):
+    """Steps 1-3 with the library's NCCL all-gather (sfmp_gemm_sharded)."""
+    n = len(models)
+    xs = [x.contiguous() for x in xs]
+    check(lib().sfmp_gemm_sharded(
+        _ptr_array([m.handle for m in models]), _ptr_array([x.data_ptr() for x in xs]), _dtype_code(xs[0]),
+        (C.c_int64 * n)(*[x.shape[0] for x in xs]), _ptr_array([y.data_ptr() for y in outs]),
+        _ptr_array([w.data_ptr() for w in workspaces]), (C.c_size_t * n)(*[w.numel() for w in workspaces]), n,
+        C.c_void_p(gather_buf.data_ptr()), gather_buf.numel() * gather_buf.element_size(), comm.handle,
+        _stream_ptr(stream)))
+    return outs

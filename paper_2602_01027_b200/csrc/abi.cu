@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -18,6 +19,7 @@
 #include "sfmp_internal.h"
 
 using sfmpk::DevModel;
+using sfmpk::note_launch;
 
 namespace {
 
@@ -38,16 +40,7 @@ sfmp_status cuda_fail(cudaError_t e, const char* what) {
         if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
     } while (0)
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
+using sfmpk::DeviceGuard;
 
 // ---------------------------------------------------------------------------
 // Host ingest of SFMPPKD1
@@ -345,9 +338,51 @@ sfmp_status shard_plan(const Parsed& p, uint32_t G, std::vector<std::vector<uint
     return SFMP_OK;
 }
 
+// Algorithmic bytes of one call: planes + fp16 s,z + perms + x + y.
+uint64_t algo_bytes(const DevModel& d, int64_t M, sfmp_dtype dt) {
+    const uint64_t esz = dt == SFMP_F32 ? 4 : 2;
+    return d.payload_bytes + ((d.mode & 2) ? 4 * d.cols : 0) + ((d.mode & 1) ? 4 * d.rows : 0) +
+           static_cast<uint64_t>(M) * d.cols * esz + 4ull * M * d.out_rows;
+}
+
+sfmp_path resolve_path(const DevModel& d, int64_t M, const void* x, sfmp_path path) {
+    const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    if (path == SFMP_PATH_AUTO)
+        path = (M > 16 && d.gemm_ok && x_aligned) ? SFMP_PATH_GEMM : (d.gemv_ok ? SFMP_PATH_GEMV : SFMP_PATH_GENERIC);
+    return path;
+}
+
+double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Events around a region of one stream (the stats entry points synchronise).
+struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    EventPair() {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+    }
+    ~EventPair() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+    double us() const {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        return ms * 1e3;
+    }
+};
+
 }  // namespace
 
+namespace sfmpk {
+sfmp_status api_fail(sfmp_status s, const std::string& msg) { return fail(s, msg); }
+}  // namespace sfmpk
+
 extern "C" {
+
+uint64_t sfmp_launch_count(void) { return sfmpk::t_launches; }
 
 int sfmp_abi_version(void) { return SFMP_CUDA_ABI_VERSION; }
 
@@ -619,8 +654,7 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // the tensor-core pre-pass reads x rows with 16-byte vector loads
     const bool x_aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-    if (path == SFMP_PATH_AUTO)
-        path = (M > 16 && d.gemm_ok && x_aligned) ? SFMP_PATH_GEMM : (d.gemv_ok ? SFMP_PATH_GEMV : SFMP_PATH_GENERIC);
+    path = resolve_path(d, M, x, path);
     if (path == SFMP_PATH_GEMM && !x_aligned)
         return fail(SFMP_ERR_INVALID_ARGUMENT, "GEMM path needs x 16-byte aligned");
     cudaError_t e = cudaSuccess;
@@ -744,9 +778,12 @@ sfmp_status sfmp_gemm(const sfmp_dev_model* model, const void* x, sfmp_dtype dty
     return sfmp_gemm_ex(model, x, dtype, M, y, workspace, workspace_bytes, SFMP_PATH_AUTO, stream);
 }
 
-sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M, float* y_host,
-                           void* stream) {
+sfmp_status sfmp_gemm_host_stats(const sfmp_dev_model* model, const float* x_host, int64_t M, float* y_host,
+                                 void* stream, sfmp_stats* stats) {
     if (!model || (!x_host && M) || (!y_host && M)) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    const double w0 = now_us();
+    const uint64_t l0 = sfmpk::t_launches;
+    if (stats) std::memset(stats, 0, sizeof(*stats));
     if (M == 0) return SFMP_OK;
     DevModel& d = *const_cast<DevModel*>(reinterpret_cast<const DevModel*>(model));
     std::lock_guard<std::mutex> lock(d.host_mu);  // the staging buffers are per model
@@ -768,11 +805,74 @@ sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int
     float* dx = reinterpret_cast<float*>(d.d_host_stage);
     float* dy = reinterpret_cast<float*>(d.d_host_stage + xb);
     void* ws = wsb ? d.d_host_stage + xb + yb : nullptr;
+    EventPair e_h2d, e_dev, e_d2h;
+    if (stats) cudaEventRecord(e_h2d.a, st);
     SFMP_CUDA_TRY(cudaMemcpyAsync(dx, x_host, M * d.cols * 4, cudaMemcpyHostToDevice, st));
+    if (stats) {
+        cudaEventRecord(e_h2d.b, st);
+        cudaEventRecord(e_dev.a, st);
+    }
     s = sfmp_gemm(model, dx, SFMP_F32, M, dy, ws, wsb, stream);
     if (s) return s;
+    if (stats) {
+        cudaEventRecord(e_dev.b, st);
+        cudaEventRecord(e_d2h.a, st);
+    }
     SFMP_CUDA_TRY(cudaMemcpyAsync(y_host, dy, M * d.out_rows * 4, cudaMemcpyDeviceToHost, st));
+    if (stats) cudaEventRecord(e_d2h.b, st);
     SFMP_CUDA_TRY(cudaStreamSynchronize(st));
+    if (stats) {
+        stats->h2d_us = e_h2d.us();
+        stats->device_us = e_dev.us();
+        stats->d2h_us = e_d2h.us();
+        stats->bytes = algo_bytes(d, M, SFMP_F32);
+        stats->flops = 2.0 * M * d.rows * d.cols;
+        stats->path = resolve_path(d, M, dx, SFMP_PATH_AUTO);
+        stats->launches = static_cast<int32_t>(sfmpk::t_launches - l0);
+        stats->wall_us = now_us() - w0;
+    }
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M, float* y_host,
+                           void* stream) {
+    return sfmp_gemm_host_stats(model, x_host, M, y_host, stream, nullptr);
+}
+
+sfmp_status sfmp_gemm_stats(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M, float* y,
+                            void* workspace, size_t workspace_bytes, sfmp_path path, void* stream,
+                            sfmp_stats* stats) {
+    if (!stats) return sfmp_gemm_ex(model, x, dtype, M, y, workspace, workspace_bytes, path, stream);
+    std::memset(stats, 0, sizeof(*stats));
+    if (!model) return fail(SFMP_ERR_INVALID_ARGUMENT, "null model");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    DeviceGuard guard(d.device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const double w0 = now_us();
+    const uint64_t l0 = sfmpk::t_launches;
+    EventPair ev;
+    cudaEventRecord(ev.a, st);
+    sfmp_status s = sfmp_gemm_ex(model, x, dtype, M, y, workspace, workspace_bytes, path, stream);
+    if (s) return s;
+    cudaEventRecord(ev.b, st);
+    SFMP_CUDA_TRY(cudaEventSynchronize(ev.b));
+    stats->device_us = ev.us();
+    stats->bytes = M > 0 ? algo_bytes(d, M, dtype) : 0;
+    stats->flops = 2.0 * M * d.rows * d.cols;
+    stats->path = resolve_path(d, M, x, path);
+    stats->launches = static_cast<int32_t>(sfmpk::t_launches - l0);
+    stats->wall_us = now_us() - w0;
+    return SFMP_OK;
+}
+
+sfmp_status sfmp_gemv_block(const sfmp_dev_model* model, uint64_t block, const float* x_reordered, float* out,
+                            void* stream) {
+    if (!model || !x_reordered || !out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
+    const DevModel& d = *reinterpret_cast<const DevModel*>(model);
+    if (block >= d.K) return fail(SFMP_ERR_SHAPE, "gemv_block: block index out of range");
+    DeviceGuard guard(d.device);
+    cudaError_t e = sfmpk::launch_gemv_block(d, block, x_reordered, out, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "gemv_block launch");
     return SFMP_OK;
 }
 
@@ -798,7 +898,7 @@ sfmp_status sfmp_unpermute_gathered(const sfmp_dev_model* model, const float* ga
                                     void* stream) {
     if (!model || (M && (!gathered || !y))) return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
     const DevModel& d = *reinterpret_cast<const DevModel*>(model);
-    if (d.num_shards < 2 || !d.d_gather_map) return fail(SFMP_ERR_CONFIG, "model is not a shard");
+    if (!d.d_gather_map) return fail(SFMP_ERR_CONFIG, "model is not a shard");
     DeviceGuard guard(d.device);
     cudaError_t e = sfmpk::launch_unpermute_gathered(d, gathered, M, y, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "unpermute launch");

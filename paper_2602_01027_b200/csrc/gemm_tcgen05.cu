@@ -31,10 +31,12 @@
 //                   written straight into TMEM as the MMA A operand
 //                   (tcgen05.st), so weights never take a shared-memory trip.
 //    TMEM (512 columns): accumulator 256 columns, 4 A buffers x 64 columns.
-//  * Schedule: work items (tile, K split), round-robin over the CTAs.  The
+//  * Schedule: work items (tile, K split), round-robin over the CTAs, tiles
+//    in a grouped raster order (tile_coords) for L2 reuse of X and W.  The
 //    number of K splits depends on the UNSHARDED matrix shape and M only
-//    (k_splits), so results are bit-identical on any device and for any
-//    shard count; split partials are summed in split order (gemm_reduce_kernel).
+//    (k_splits, a cost model over a virtual 148-SM grid), so results are
+//    bit-identical on any device and for any shard count; split partials are
+//    summed in split order (gemm_reduce_kernel).
 //  * Precision: weights are rounded once to f16 (SURVEY §7 hard part 1:
 //    f16 dequant stays ~5x inside the 1e-3 bar, bf16 would not); the scaled
 //    activations are rounded to f16 (exact for bf16 input); accumulation is
@@ -83,6 +85,7 @@ struct GemmParams {
     int floor_bits, has_extra;
     int SX, SW;              // X / W ring stages
     int ks;                  // K splits per tile (a function of the matrix shape and M alone)
+    int GT;                  // token tiles per raster group (tile order, L2 reuse of X)
     int items;               // tiles * ks
     float* part;             // [items][N][128] f32 split-K partial tiles (ks > 1)
     uint32_t stage_w;        // W stage bytes (one unit)
@@ -270,6 +273,19 @@ __global__ void __launch_bounds__(1024) xprep_gemm_kernel(const void* __restrict
     }
 }
 
+// Tile order (numerics-neutral): groups of GT token tiles; within a group
+// the row tiles are outer and the group's token tiles inner, so the ~148
+// tiles in flight share a bounded X working set (GT token tiles' images) and
+// each weight row tile is read once per group (L2 reuse of both operands).
+__host__ __device__ __forceinline__ void tile_coords(const GemmParams& p, int tile, int& rt, int& tt) {
+    const int per = p.RT * p.GT;
+    const int grp = tile / per;
+    const int r = tile - grp * per;
+    const int gt = min(p.GT, p.TT - grp * p.GT);
+    rt = r / gt;
+    tt = grp * p.GT + (r - rt * gt);
+}
+
 // Work items of this CTA: items b, b+G, b+2G, ... ; item i = (tile i / ks,
 // K split i % ks), split j covering chunks [j*KC/ks, (j+1)*KC/ks).  Every role
 // walks the same sequence.
@@ -293,7 +309,8 @@ __device__ __forceinline__ bool seg_at(const GemmParams& p, int k, GSeg& g) {
 __global__ void __launch_bounds__(128) gemm_reduce_kernel(const GemmParams p) {
     pdl_wait();
     const int tile = blockIdx.y;
-    const int rt = tile / p.TT, tt = tile - rt * p.TT;
+    int rt, tt;
+    tile_coords(p, tile, rt, tt);
     const int N = p.N;
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j0 = blockIdx.x * 32 + wi;
@@ -405,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     // the split-K fix-up (if any) may launch now; it waits for this grid
     pdl_launch_dependents();
 
-    // Work: items (tile, K split), tile = rt * TT + tt, round-robin over the
+    // Work: items (tile, K split), tile -> (rt, tt) by tile_coords, round-robin over the
     // CTAs.  A whole-tile item (ks == 1) stores y; a split item stores its
     // partial tile, summed in split order by gemm_reduce_kernel.
     const int KC = p.KC;
@@ -420,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             int ws = 0, wph = 0;
             GSeg sg;
             for (int k = 0; seg_at(p, k, sg); ++k) {
-                const int rt = sg.tile / p.TT;
+                int rt, tt_unused;
+                tile_coords(p, sg.tile, rt, tt_unused);
                 const uint64_t* off0 = p.woff + static_cast<size_t>(rt) * KC + sg.kc0;
                 uint64_t a_next = __ldg(off0);
                 for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
@@ -438,7 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             pdl_wait();  // X is written by the pre-pass (programmatic dependent launch)
             GSeg sg;
             for (int k = 0; seg_at(p, k, sg); ++k) {
-                const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
+                int rt, tt;
+                tile_coords(p, sg.tile, rt, tt);
                 for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                     for (int h = 0; h < 2; ++h) {
                         mbar_wait_sleep(&xempty[xs], xph ^ 1, 200);
@@ -501,7 +520,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         int accph = 0;
         GSeg sg;
         for (int k = 0; seg_at(p, k, sg); ++k) {
-            const int rt = sg.tile / p.TT, tt = sg.tile - rt * p.TT;
+            int rt, tt;
+            tile_coords(p, sg.tile, rt, tt);
             mbar_wait_sleep(accfull, accph, 200);  // a whole tile of MMAs away: sleep between polls
             accph ^= 1;
             tc_fence_after();
@@ -633,18 +653,38 @@ uint32_t unit_max_bytes(const DevModel& m) {
 
 // K splits per tile: a function of the UNSHARDED matrix shape and M only
 // (never of the device or the shard), so a row's accumulation order -- and its
-// bits -- are the same on any B200, for any shard count.  Split when the
-// whole matrix has fewer tiles than half a virtual 148-SM grid: each split
-// keeps >= 8 K chunks.
+// bits -- are the same on any B200, for any shard count.  Chosen by a cost
+// model over a virtual 148-SM grid: waves x (chunks per item x MMA time per
+// chunk + per-item fill/drain) + the split partials' write/read and the
+// reduce launch.  Measured constants (tools/mma_bench.cu, round 1): one
+// 128-column chunk = 8 MMAs of K=16, ~130 cycles each for N <= 128 and ~138
+// at N = 256.
 constexpr int kVirtualSMs = 148;
 int k_splits(const DevModel& m, int64_t M) {
     const int64_t N = tile_n(M), TT = (M + N - 1) / N;
     const int64_t KC = static_cast<int64_t>(m.cols / 128);
     const int64_t tiles_g = static_cast<int64_t>((m.global_rows + 127) / 128) * TT;
-    if (tiles_g * 2 > kVirtualSMs) return 1;
-    int64_t ks = (kVirtualSMs + tiles_g - 1) / tiles_g;
-    ks = std::min<int64_t>(ks, KC / 8);
-    return static_cast<int>(std::max<int64_t>(1, ks));
+    const double chunk_us = 8.0 * (N > 128 ? 138.0 : 130.0) / 1900.0, item_us = 1.5;
+    int best = 1;
+    double best_t = 1e30;
+    for (int64_t ks = 1; ks <= std::max<int64_t>(1, std::min<int64_t>(KC / 4, 32)); ++ks) {
+        const int64_t items = tiles_g * ks;
+        const double waves = static_cast<double>((items + kVirtualSMs - 1) / kVirtualSMs);
+        double t = waves * (static_cast<double>((KC + ks - 1) / ks) * chunk_us + item_us);
+        if (ks > 1) t += static_cast<double>(items) * N * 128 * 4 * 2 / 6.0e6 + 3.0;  // partials via L2 + reduce
+        if (t < best_t * 0.97) {  // prefer fewer splits unless clearly faster
+            best_t = t;
+            best = static_cast<int>(ks);
+        }
+    }
+    return best;
+}
+
+// Token tiles per raster group: the group's X images stay within ~40 MB of L2.
+int raster_group(const DevModel& m, int64_t M) {
+    const int64_t N = tile_n(M), TT = (M + N - 1) / N;
+    const int64_t ximg = N * static_cast<int64_t>(m.cols) * 2;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(TT, (40ll << 20) / std::max<int64_t>(ximg, 1))));
 }
 
 template <class F>
@@ -669,6 +709,7 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t s
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    note_launch();
     cudaError_t e = cudaLaunchKernelEx(&cfg, k, p);
     if (e != cudaSuccess) return e;
     if (p.ks > 1) {  // split-K fix-up, a programmatic dependent of the GEMM
@@ -678,6 +719,7 @@ cudaError_t launch_np(const GemmParams& p, size_t smem, int grid, cudaStream_t s
         rc.stream = st;
         rc.attrs = attr;
         rc.numAttrs = 1;
+        note_launch();
         e = cudaLaunchKernelEx(&rc, gemm_reduce_kernel, p);
     }
     return e;
@@ -751,6 +793,7 @@ void launch_xprep_rows(const void* x, const DevModel& m, uint8_t* xs, float* ysc
                        int grid, size_t smem, cudaStream_t st) {
     static std::once_flag fl[64];
     once_per_device(fl, [] { cudaFuncSetAttribute(xprep_gemm_rows_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+    note_launch();
     xprep_gemm_rows_kernel<DT><<<grid, 512, smem, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad);
 }
 template <sfmp_dtype DT>
@@ -761,7 +804,10 @@ void launch_xprep_tok(const void* x, const DevModel& m, uint8_t* xs, float* ysc,
         cudaFuncSetAttribute(xprep_gemm_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         cudaFuncSetAttribute(xprep_gemm_kernel<DT>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     });
-    xprep_gemm_kernel<DT><<<Mpad, 128, static_cast<size_t>(cols) * 2, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad);
+    note_launch();
+    // 512 threads: the per-token absmax, convert and gather loops need the
+    // whole CTA (128 threads per 28672-column row ran at ~150 GB/s)
+    xprep_gemm_kernel<DT><<<Mpad, 512, static_cast<size_t>(cols) * 2, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad);
 }
 
 // Workspace: swizzled X images | per-token scales | split-K partial tiles [items][N][128] f32.
@@ -824,9 +870,10 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     const int cols = static_cast<int>(m.cols);
     const int Mpad = p.TT * p.N;
     const size_t elem = dt == SFMP_F32 ? 4 : 2;
-    // persistent pre-pass when the u16 slot table + two rows fit (>= 2 CTAs per SM)
+    // persistent pre-pass when the u16 slot table + two rows fit in one CTA's
+    // shared memory (1..4 CTAs per SM)
     const size_t rsm = 16 + (static_cast<size_t>(cols) * 2 + 15) / 16 * 16 + 2 * static_cast<size_t>(cols) * elem;
-    const bool rows_ok = cols < 65536 && rsm <= 110 * 1024 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const bool rows_ok = cols < 65536 && rsm <= 200 * 1024 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     cudaError_t e0 = cudaSuccess;
     if (rows_ok) {
         const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / rsm)));
@@ -849,6 +896,7 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     // grid at the co-resident cluster count, 132 of 148 SMs: not used.)
     const int64_t ntiles = static_cast<int64_t>(p.RT) * p.TT;
     p.ks = k_splits(m, M);
+    p.GT = raster_group(m, M);
     p.items = static_cast<int>(ntiles * p.ks);
     const int grid = static_cast<int>(std::min<int64_t>(p.items, m.num_sms));
     switch (m.ceil_bits) {

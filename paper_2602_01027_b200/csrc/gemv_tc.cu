@@ -857,6 +857,7 @@ cudaError_t launch_k(cudaLaunchConfig_t& cfg, const Params& p) {
     cudaGetDevice(&dev);
     once_per_device(fl, [&] { err[dev & 63] = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); });
     if (err[dev & 63] != cudaSuccess) return err[dev & 63];
+    note_launch();
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
@@ -911,11 +912,16 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
         c.stream = st;
         c.attrs = a;
         c.numAttrs = 1;
+        note_launch();
         cudaError_t e = cudaLaunchKernelEx(&c, xprep_rows_kernel<DT>, xq);
         if (e != cudaSuccess) return e;
     } else {
-        if (DT != SFMP_F16) rowscale_kernel<DT><<<dim3(16, xp.nlin), 256, 0, st>>>(xp);
+        if (DT != SFMP_F16) {
+            note_launch();
+            rowscale_kernel<DT><<<dim3(16, xp.nlin), 256, 0, st>>>(xp);
+        }
         const int per_cta = 8 / (p.n_b / 128);  // items per pre-pass CTA
+        note_launch();
         xprep_kernel<DT><<<(xwarps + per_cta - 1) / per_cta, 256, 0, st>>>(xp);
     }
     {
@@ -945,6 +951,7 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
     fc.stream = st;
     fc.attrs = pdl;
     fc.numAttrs = 1;
+    note_launch();
     return cudaLaunchKernelEx(&fc, gemv_fixup_kernel, p);
 }
 

@@ -151,6 +151,22 @@ __global__ void unpermute_kernel(const float* gathered, const uint32_t* gmap, fl
     if (dst != 0xFFFFFFFFu) y[t * rows + dst] = gathered[idx];
 }
 
+// gemv_block (lutgemm.cpp:87-93): the contribution of block (br, bc) to its
+// m_b rows in stored order, from the REORDERED activation; one warp per row.
+__global__ void __launch_bounds__(256) gemv_block_kernel(const GenParams p, uint64_t br, uint32_t bc, uint32_t m_b,
+                                                         const float* __restrict__ xr, float* __restrict__ out) {
+    const uint32_t i = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= m_b) return;
+    const RowRef ref = row_ref(p.g, br * m_b + i, bc);
+    float acc = 0.f;
+    for (uint32_t j = lane; j < p.g.n_b; j += 32)
+        acc += __fadd_rn(__fmul_rn(ref.s, static_cast<float>(ref.code(j))), ref.z) * xr[static_cast<uint64_t>(bc) * p.g.n_b + j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[i] = acc;
+}
+
 GenParams make_params(const DevModel& m) {
     GenParams p{};
     p.g = m.geom();
@@ -209,6 +225,7 @@ cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int6
     p.y = y;
     p.M = M;
     const unsigned grid = static_cast<unsigned>((m.rows + 7) / 8);
+    note_launch();
     switch (dt) {
         case SFMP_F32: generic_kernel<SFMP_F32><<<grid, 256, 0, st>>>(p); break;
         case SFMP_F16: generic_kernel<SFMP_F16><<<grid, 256, 0, st>>>(p); break;
@@ -217,9 +234,19 @@ cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int6
     return cudaGetLastError();
 }
 
+cudaError_t launch_gemv_block(const DevModel& m, uint64_t block, const float* xr, float* out, cudaStream_t st) {
+    GenParams p = make_params(m);
+    const uint64_t br = block / m.BC;
+    const uint32_t bc = static_cast<uint32_t>(block % m.BC);
+    note_launch();
+    gemv_block_kernel<<<(m.m_b + 7) / 8, 256, 0, st>>>(p, br, bc, m.m_b, xr, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_dequant(const DevModel& m, float* w, cudaStream_t st) {
     GenParams p = make_params(m);
     const uint64_t n = m.rows * m.cols;
+    note_launch();
     dequant_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, w);
     return cudaGetLastError();
 }
@@ -227,6 +254,7 @@ cudaError_t launch_dequant(const DevModel& m, float* w, cudaStream_t st) {
 cudaError_t launch_unpack(const DevModel& m, uint8_t* codes, cudaStream_t st) {
     GenParams p = make_params(m);
     const uint64_t n = m.rows * m.cols;
+    note_launch();
     unpack_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, codes);
     return cudaGetLastError();
 }
@@ -235,6 +263,7 @@ cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, 
                                       cudaStream_t st) {
     const uint64_t total = static_cast<uint64_t>(m.num_shards) * M * m.shard_rows;
     if (total == 0) return cudaSuccess;
+    note_launch();
     unpermute_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
         gathered, m.d_gather_map, y, M, m.num_shards, m.shard_rows, m.global_rows);
     return cudaGetLastError();

@@ -11,6 +11,25 @@
 
 namespace sfmpk {
 
+// Kernels launched by this host thread (cumulative): every launcher calls
+// note_launch() once per kernel it enqueues (sfmp_launch_count()).
+inline thread_local uint64_t t_launches = 0;
+inline void note_launch() { ++t_launches; }
+
+// Error message of the last failing call on this host thread (abi.cu).
+sfmp_status api_fail(sfmp_status s, const std::string& msg);
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // Device layout.  The SFMPPKD1 block payload
 // is stored UNIT-MAJOR: a unit is TR consecutive reordered rows x one block
 // column (n_b columns), TR = 128 when m_b % 128 == 0, else TR = m_b.  A unit
@@ -93,6 +112,7 @@ bool gemv_feasible(const DevModel& m);
 cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
                            cudaStream_t st);
 cudaError_t launch_dequant(const DevModel& m, float* w, cudaStream_t st);
+cudaError_t launch_gemv_block(const DevModel& m, uint64_t block, const float* xr, float* out, cudaStream_t st);
 cudaError_t launch_unpack(const DevModel& m, uint8_t* codes, cudaStream_t st);
 cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, int64_t M,
                                       float* y, cudaStream_t st);

@@ -23,7 +23,7 @@ def test_library_exports_declared_symbols():
     for name in decl:
         assert hasattr(L, name), name
     assert set(decl) == set(sfmp.EXPORTED_SYMBOLS)
-    assert L.sfmp_abi_version() == 1
+    assert L.sfmp_abi_version() == 2
 
 
 def test_library_is_sm100a_only():
