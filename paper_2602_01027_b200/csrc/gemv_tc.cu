@@ -84,6 +84,9 @@ constexpr int kSmemSM = 225 * 1024;
 #ifndef SFMP_EXP_NOMMA
 #define SFMP_EXP_NOMMA 0
 #endif
+#ifndef SFMP_EXP_NOLOAD
+#define SFMP_EXP_NOLOAD 0
+#endif
 #ifndef SFMP_EXP_NOREC
 #define SFMP_EXP_NOREC 0
 #endif
@@ -655,6 +658,11 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
                                               (fl << 20),
                                           static_cast<uint32_t>(rt), static_cast<uint32_t>(seg), 0u);
                     const uint32_t wbytes = unit_bytes(b0, nb8) + (nu > 1 ? unit_bytes(b1, nb8) : 0u);
+                    if (SFMP_EXP_NOLOAD) {  // experiment builds only: compute on stale shared memory
+                        mbar_arrive(&full[s]);
+                        if (++s == S) { s = 0; ph ^= 1; }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[s], wbytes + (SFMP_EXP_NOREC ? 0u : nu * sec));  // publishes sinfo[s]
                     bulk_g2s(wbase + static_cast<size_t>(s) * p.stage_w, L.payload + (d0 & 0xFFFFFFFFFFFFull), wbytes,
                              &full[s], pol);
@@ -955,6 +963,9 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
     return cudaLaunchKernelEx(&fc, gemv_fixup_kernel, p);
 }
 
+// Canonical K segment: kSegCols columns for every linear (measured: 512- or
+// 256-column segments for small linears raised configs[0] from 10.4 to 11.7 us
+// and the 8B decode launch by 5 %: more partials and fix-up work than balance gained).
 int units_per_segment(const DevModel& m) { return std::max(1, kSegCols / static_cast<int>(m.n_b)); }
 int segments_per_tile(const DevModel& m) {
     const int L = units_per_segment(m);
