@@ -799,52 +799,43 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const P
     }
 }
 
-// Split-tile fix-up (programmatic dependent of the GEMV).  Work = (tile,
-// token) pairs of every multi-segment linear (fix_start prefix), 128 threads
-// (the tile's rows) per pair; persistent CTAs of 8 groups walk the pairs two
-// at a time so that 2 x P loads per thread are in flight.  The P segment
-// partials are added in segment order -- the canonical order -- and stored
-// un-permuted.
-__global__ void __launch_bounds__(8 * kTR) gemv_fixup_kernel(const Params p) {
+// Split-tile fix-up (programmatic dependent of the GEMV).  One warp per
+// (tile, token) pair of every multi-segment linear (fix_start prefix); lane l
+// owns rows 4l..4l+3 of the tile (float4), issues all P partial loads at once
+// and adds them in SEGMENT order -- the canonical order -- then stores the 4
+// un-permuted outputs.  One warp per pair and 8 pairs per 256-thread CTA keep
+// a whole launch's fix-up in one wave (the 128-threads-per-pair, 2-pairs-per-
+// thread version took ~2.3 latency-bound passes: 11 us exposed at M=16).
+__global__ void __launch_bounds__(256) gemv_fixup_kernel(const Params p) {
     pdl_launch_dependents();  // a later launch of the same grouped call may start its pre-pass
-    const int row = threadIdx.x & (kTR - 1);
-    const int stride = static_cast<int>(gridDim.x) * 8;
-    int w = static_cast<int>(blockIdx.x) * 8 + static_cast<int>(threadIdx.x >> 7);
+    const int lane = threadIdx.x & 31;
+    const int w = static_cast<int>(blockIdx.x) * 8 + static_cast<int>(threadIdx.x >> 5);
+    if (w >= p.n_fix) return;
+    const Lin& L = p.lin[owner_of(p.fix_start, p.nlin, w)];
+    const int rel = w - L.fix0, rt = rel / L.M, t = rel - rt * L.M;
+    const uint4 om = __ldg(reinterpret_cast<const uint4*>(L.out_map + rt * kTR) + lane);
+    const float4* pp = reinterpret_cast<const float4*>(L.part + static_cast<size_t>(rt) * L.P * (16 * kTR) + t * kTR) + lane;
     pdl_wait();  // the GEMV grid has completed and its partials are visible
-    for (; w < p.n_fix; w += 2 * stride) {
-        const float* pp[2];
-        float* yp[2];
-        int P[2];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < L.P; k0 += 16) {
+        float4 v[16];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int wh = w + h * stride;
-            P[h] = 0;
-            if (wh >= p.n_fix) continue;
-            const Lin& L = p.lin[owner_of(p.fix_start, p.nlin, wh)];
-            const int rel = wh - L.fix0, rt = rel / L.M, t = rel - rt * L.M;
-            P[h] = L.P;
-            pp[h] = L.part + static_cast<size_t>(rt) * L.P * (16 * kTR) + t * kTR + row;
-            yp[h] = L.y + static_cast<size_t>(t) * L.out_rows + __ldg(L.out_map + rt * kTR + row);
-        }
-        float acc[2] = {0.f, 0.f};
-        const int Pm = max(P[0], P[1]);
-        for (int k0 = 0; k0 < Pm; k0 += 16) {
-            float v[2][16];
+        for (int k = 0; k < 16; ++k)
+            if (k0 + k < L.P) v[k] = __ldg(pp + (k0 + k) * (16 * kTR / 4));  // previous grid's data
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    if (k0 + k < P[h]) v[h][k] = __ldg(pp[h] + (k0 + k) * (16 * kTR));  // previous grid's data
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    if (k0 + k < P[h]) acc[h] += v[h][k];  // segment order
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-            if (P[h]) *yp[h] = acc[h];
+        for (int k = 0; k < 16; ++k)
+            if (k0 + k < L.P) {  // segment order
+                acc.x += v[k].x;
+                acc.y += v[k].y;
+                acc.z += v[k].z;
+                acc.w += v[k].w;
+            }
     }
+    float* yrow = L.y + static_cast<size_t>(t) * L.out_rows;
+    yrow[om.x] = acc.x;
+    yrow[om.y] = acc.y;
+    yrow[om.z] = acc.z;
+    yrow[om.w] = acc.w;
 }
 
 // One-time (per device, thread-safe) function attribute setup.
@@ -954,8 +945,8 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
     if (e != cudaSuccess || p.n_fix == 0) return e;
     // split tiles: sum the segment partials (programmatic dependent of the GEMV)
     cudaLaunchConfig_t fc{};
-    fc.gridDim = dim3(std::min((p.n_fix + 7) / 8, 2 * 148));  // <= 2 CTAs of 1024 threads per SM
-    fc.blockDim = dim3(8 * kTR);
+    fc.gridDim = dim3((p.n_fix + 7) / 8);  // one warp per (tile, token) pair
+    fc.blockDim = dim3(256);
     fc.stream = st;
     fc.attrs = pdl;
     fc.numAttrs = 1;

@@ -28,7 +28,12 @@ def summarise(rep):
     pick = {}
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
               "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
-              "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
+              "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+              "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+              "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+              "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+              "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
               "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
               "smsp__inst_executed.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed"):
         if k in rd:
