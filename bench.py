@@ -416,24 +416,25 @@ def sweep_points(sfmp, port, dev, stream, hbm, tc, args):
     return out
 
 
-def llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args):
+def llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args, sharded=None):
     """configs[3]: the seven Llama-3.1-70B linears @2.5 bits (k/v m_b=128 so they
     split 8 ways), decode step M in {1,2,4,8,16} as one call, prefill M=2048;
     N>1: snake-sharded, ONE NCCL all-gather per call -- kernel and collective
     time reported separately."""
     import torch
     from synth import LLAMA_70B, model_bytes, prebuild
+    sharded = sharded if sharded is None else sharded
     specs = [(r, c, 2.5, {"m_b": 128 if p in ("k_proj", "v_proj") else 512}) for p, (r, c) in LLAMA_70B.items()]
     prebuild(specs)
     blobs = {p: model_bytes(port, r, c, 2.5, m_b=128 if p in ("k_proj", "v_proj") else 512)
              for p, (r, c) in LLAMA_70B.items()}
     copies = 2
-    mk = (lambda b: sfmp.DeviceModel(b, device=dev.index)) if world == 1 else \
+    mk = (lambda b: sfmp.DeviceModel(b, device=dev.index)) if not sharded else \
         (lambda b: sfmp.DeviceModel(b, device=dev.index, shard=rank, num_shards=world))
     models = [{p: mk(blobs[p]) for p in PROJS} for _ in range(copies)]
     out = {"workload": "llama3.1-70b decoder-layer linears @2.5 code bits (3/2 mix), rowcol; decode M in "
                        "{1,2,4,8,16} (35 problems, one call) and prefill M=2048 (7 problems)",
-           "parallelism": "single GPU" if world == 1 else f"N-sharded x{world}, one NCCL all-gather per call"}
+           "parallelism": "single GPU" if not sharded else f"N-sharded x{world}, one NCCL all-gather per call"}
     xs = {(p, M): torch.from_numpy(port.gen_activation(M, LLAMA_70B[p][1], 6000 + M)).to(dev).to(torch.bfloat16)
           for p in PROJS for M in MS}
     keys = [(p, M) for M in MS for p in PROJS]
@@ -442,7 +443,7 @@ def llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args):
 
     def run(i, kk, local_only=False, bufs=None):
         ms = [models[(i + j) % copies][p] for j, (p, M) in enumerate(kk)]
-        if world == 1:
+        if not sharded:
             sfmp.gemm_grouped(ms, [xs[k] for k in kk], outs=[ys[k] for k in kk], workspaces=[wsm[k] for k in kk],
                               stream=stream)
         elif local_only:
@@ -452,14 +453,14 @@ def llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args):
                               stream=stream)
 
     buf = None
-    if world > 1:
+    if sharded:
         buf = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p, M in keys], [M for p, M in keys]) // 4,
                           device=dev)
     us = graph_us(lambda: [run(i, keys, bufs=buf) for i in range(copies)], stream, 10, copies)
     byts = sum(algo_bytes(models[0][p].info, M, models[0][p].rows, LLAMA_70B[p][1]) for p, M in keys)
     out["decode_step"] = {"M": MS, **roof(byts, sum(2.0 * M * models[0][p].rows * LLAMA_70B[p][1] for p, M in keys),
                                           us, hbm, tc)}
-    if world > 1:
+    if sharded:
         kus = graph_us(lambda: [run(i, keys, local_only=True, bufs=buf) for i in range(copies)], stream, 10, copies)
         out["decode_step"].update({"kernel_us": round(kus, 2), "collective_and_unpermute_us": round(us - kus, 2),
                                    "bytes_gathered_per_rank": buf.numel() * 4 // (1 + world) * world})
@@ -468,7 +469,7 @@ def llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args):
     xp = {p: torch.from_numpy(port.gen_activation(Mp, LLAMA_70B[p][1], 7000)).to(dev).to(torch.bfloat16) for p in PROJS}
     yp = {p: torch.empty(Mp, LLAMA_70B[p][0], device=dev) for p in PROJS}
     wsp = {p: ws_for(sfmp, models[0][p], Mp) for p in PROJS}
-    if world == 1:
+    if not sharded:
         per = {}
         for p in PROJS:
             t = graph_us(lambda: [models[c][p].gemm(xp[p], out=yp[p], workspace=wsp[p], stream=stream)
@@ -519,6 +520,9 @@ def main():
     ap.add_argument("--no-group", action="store_true", help="one launch per linear instead of per decoder layer")
     ap.add_argument("--prefill-M", type=int, default=2048)
     ap.add_argument("--e2e-order", default="", help="groups of token counts for the e2e step, e.g. '1/4/8/16/2'")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the sharded path (shard models, sfmp_gemm_sharded, library NCCL communicator) even "
+                         "at N=1 (1-way shards): exercises the multi-GPU code path on one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -535,16 +539,19 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     comm = None
+    sharded = world > 1 or args.force_sharded
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         # the library's own NCCL communicator (sfmp_gemm_sharded): id over torch.distributed
         uid = [sfmp.NcclComm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = sfmp.NcclComm(world, rank, local, uid[0])
+    elif sharded:
+        comm = sfmp.NcclComm(1, 0, local, sfmp.NcclComm.unique_id())
     port = Port()
     blobs = {p: build_bytes(port, p) for p in PROJS}
     # COPIES device copies of the layer (this rank's shard of it when world > 1)
-    models = [{p: (sfmp.DeviceModel(blobs[p], device=local) if world == 1 else
+    models = [{p: (sfmp.DeviceModel(blobs[p], device=local) if not sharded else
                    sfmp.DeviceModel(blobs[p], device=local, shard=rank, num_shards=world))
                for p in PROJS} for _ in range(COPIES)]
     infos = {p: sfmp.parse_header(blobs[p]) for p in PROJS}
@@ -555,7 +562,7 @@ def main():
     wsm = {(p, M): ws_for(sfmp, models[0][p], 16) for p in PROJS for M in MS}
     keys_all = [(p, M) for M in MS for p in PROJS]
     gbuf = None
-    if world > 1:
+    if sharded:
         gbuf = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p, M in keys_all],
                                                      [M for p, M in keys_all]) // 4, device=dev)
     grouped = not args.no_group
@@ -563,7 +570,7 @@ def main():
     def call(i, kk, local_only=False):
         """One API call over the problems kk = [(proj, M)], weight copy rotating with i."""
         ms = [models[(i * len(MS) + MS.index(M)) % COPIES][p] for p, M in kk]
-        if world == 1:
+        if not sharded:
             if grouped:
                 sfmp.gemm_grouped(ms, [xs[k] for k in kk], outs=[ys[k] for k in kk], workspaces=[wsm[k] for k in kk])
             else:
@@ -654,7 +661,7 @@ def main():
     # ---- per-launch roofline: each n-tile class alone (its pre-pass + GEMV + fix-up),
     # graph replay over the rotating copies, CUDA events on the launching stream ----
     per_launch = {}
-    if world == 1 and grouped:
+    if not sharded and grouped:
         for name, kk in (("M<=8", [k for k in keys_all if k[1] <= 8]), ("M=16", [k for k in keys_all if k[1] > 8])):
             with torch.cuda.stream(stream):
                 us = graph_us(lambda: [call(i, kk) for i in range(COPIES)], stream, max(3, args.steps // 5), COPIES)
@@ -662,7 +669,7 @@ def main():
             per_launch[name] = {"problems": len(kk), "bytes": b, **roof(b, sum(2.0 * M * SHAPES[p][0] * SHAPES[p][1]
                                                                                for p, M in kk), us, hbm, tc)}
     kernel_us = None
-    if world > 1:
+    if sharded:
         with torch.cuda.stream(stream):
             kernel_us = graph_us(lambda: [call(i, keys_all, local_only=True) for i in range(COPIES)], stream,
                                  max(3, args.steps // 5), COPIES)
@@ -697,7 +704,7 @@ def main():
                   else [[1], [4], [8], [16], [2]])
     assert sorted(M for g in E2E_GROUPS for M in g) == sorted(MS)
     ebufs = {}
-    if world > 1:
+    if sharded:
         for gi_, grp in enumerate(E2E_GROUPS):
             kk = [(p, M) for M in grp for p in PROJS]
             ebufs[gi_] = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p, M in kk], [M for p, M in kk]) // 4,
@@ -720,7 +727,7 @@ def main():
             cur.wait_event(ready[gi_])
             kk = [(p, M) for M in grp for p in PROJS]
             ms = [models[(i * len(MS) + MS.index(M)) % COPIES][p] for p, M in kk]
-            if world == 1:
+            if not sharded:
                 sfmp.gemm_grouped(ms, [dx[k] for k in kk], outs=[dy[k] for k in kk], workspaces=[wsm[k] for k in kk])
             else:
                 sfmp.gemm_sharded(ms, [dx[k] for k in kk], [dy[k] for k in kk], [wsm[k] for k in kk], ebufs[gi_], comm)
@@ -778,8 +785,8 @@ def main():
     extras = {}
     if not args.no_extras:
         with torch.cuda.stream(stream):
-            extras["llama70b"] = llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args)
-            if world == 1:
+            extras["llama70b"] = llama70b_points(sfmp, port, dev, stream, hbm, tc, world, rank, comm, args, sharded)
+            if not sharded:
                 extras.update(single_linear_points(sfmp, port, dev, stream, hbm, tc, args))
                 extras["sweep_8192x28672"] = sweep_points(sfmp, port, dev, stream, hbm, tc, args)
 
@@ -819,7 +826,7 @@ def main():
     else:
         roofline = {"bound": "hbm", "achieved": round(step_ach, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(step_ach / hbm, 4), "traffic": None,
-                    "kernel": "whole step (per-rank bytes / step time)" if world > 1 else "whole step",
+                    "kernel": "whole step (per-rank bytes / step time)" if sharded else "whole step",
                     "algorithmic_bytes_per_step": step_bytes, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
         if kernel_us:
             roofline.update({"kernel_us": round(kernel_us, 2), "collective_and_unpermute_us": round(t_us - kernel_us, 2),
@@ -835,18 +842,18 @@ def main():
                                        "launch for the 28 M<=8 problems, one for the 7 M=16 problems"
                                        if grouped else "one launch per linear") +
                                       ("; sfmp_gemm_sharded: + ONE NCCL all-gather of all 35 problems' shard rows "
-                                       "and ONE un-permute launch" if world > 1 else ""),
+                                       "and ONE un-permute launch" if sharded else ""),
                    "l2": f"inputs larger than L2: {COPIES} rotating device copies of the layer "
                          f"({sum(i['payload_bytes'] for i in infos.values()) * COPIES / 1e6:.0f} MB)",
                    "cuda_graph": use_graph,
-                   "parallelism": "single GPU" if world == 1 else
+                   "parallelism": "single GPU" if not sharded else
                    f"N-sharded x{world} (snake block rows), one NCCL all-gather per step (library communicator)",
                    "parity_max_rel_err_M16": parity},
         "roofline": roofline,
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "api": ("pinned host x -> H2D per M group on a copy stream, one sfmp_gemm_grouped_v "
-                        + ("" if world == 1 else "/ sfmp_gemm_sharded ") +
+                        + ("" if not sharded else "/ sfmp_gemm_sharded ") +
                         "call per group, D2H per group on a second copy stream (copies overlap compute); CUDA "
                         "graph per step, host synchronises on y every step"), "groups": E2E_GROUPS,
                 "event_us": round(e2e_event_ms * 1e3, 2), "wall_us": round(e2e_wall_ms * 1e3, 2)},
@@ -857,7 +864,7 @@ def main():
     }
     if extras:
         out["extras"] = extras
-    if world == 1 and not args.no_prefill:
+    if not sharded and not args.no_prefill:
         out["prefill"] = prefill_leg(sfmp, port, models, dev, stream, args)
         out["dense_cublas_bf16_step"] = dense_leg(dev, stream, xs, args)
     if world == 1 and not args.no_cpu_baseline:

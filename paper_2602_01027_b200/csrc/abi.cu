@@ -320,8 +320,14 @@ uint32_t snake_owner(uint64_t br, uint32_t G) {
 }
 
 // Snake block-row partition + global gather map.
+// Each shard's rows are held in ascending ORIGINAL row order (local position
+// = rank of the row's original index among the shard's rows): the shard's
+// y_local rows then map to increasing output rows, so the un-permutation of
+// gathered shards reads G sequential streams and writes y coalesced.
+// rank_of[g][j] = local position of the shard's j-th stored (reordered) row.
 sfmp_status shard_plan(const Parsed& p, uint32_t G, std::vector<std::vector<uint64_t>>& owned,
-                       std::vector<uint32_t>& gmap, uint64_t& SR) {
+                       std::vector<uint32_t>& gmap, uint64_t& SR,
+                       std::vector<std::vector<uint32_t>>* rank_of = nullptr) {
     if (G < 1) return fail(SFMP_ERR_CONFIG, "num_shards must be >= 1");
     const uint64_t GR = p.rows / p.m_b;
     if (GR < G) return fail(SFMP_ERR_SHAPE, "fewer block rows than shards (repack with a smaller m_b)");
@@ -332,9 +338,20 @@ sfmp_status shard_plan(const Parsed& p, uint32_t G, std::vector<std::vector<uint
     SR = maxb * p.m_b;
     const std::vector<uint32_t> rp = row_order(p);
     gmap.assign(G * SR, 0xFFFFFFFFu);
-    for (uint32_t g = 0; g < G; ++g)
+    if (rank_of) rank_of->assign(G, {});
+    std::vector<std::pair<uint32_t, uint32_t>> rows;
+    for (uint32_t g = 0; g < G; ++g) {
+        rows.clear();
         for (size_t i = 0; i < owned[g].size(); ++i)
-            for (uint32_t r = 0; r < p.m_b; ++r) gmap[g * SR + i * p.m_b + r] = rp[owned[g][i] * p.m_b + r];
+            for (uint32_t r = 0; r < p.m_b; ++r)
+                rows.emplace_back(rp[owned[g][i] * p.m_b + r], static_cast<uint32_t>(i * p.m_b + r));
+        std::sort(rows.begin(), rows.end());
+        if (rank_of) (*rank_of)[g].assign(rows.size(), 0);
+        for (size_t k = 0; k < rows.size(); ++k) {
+            gmap[g * SR + k] = rows[k].first;
+            if (rank_of) (*rank_of)[g][rows[k].second] = static_cast<uint32_t>(k);
+        }
+    }
     return SFMP_OK;
 }
 
@@ -522,12 +539,14 @@ sfmp_status sfmp_shard_extract(const uint8_t* bytes, size_t len, uint32_t shard,
     if (s) return s;
     std::vector<std::vector<uint64_t>> owned;
     std::vector<uint32_t> gmap;
+    std::vector<std::vector<uint32_t>> rank_of;
     uint64_t SR = 0;
-    if ((s = shard_plan(p, num_shards, owned, gmap, SR))) return s;
+    if ((s = shard_plan(p, num_shards, owned, gmap, SR, &rank_of))) return s;
     const std::vector<uint64_t>& br = owned[shard];
     const uint64_t BC = p.cols / p.n_b, rows = br.size() * p.m_b, K = br.size() * BC;
-    const uint8_t mode = static_cast<uint8_t>(p.mode & 2);  // local rows are in shard order
-    uint64_t need = 38 + (mode & 2 ? 4 * p.cols : 0) + 8 + K;
+    // row permutation: stored row j -> its local output position (ascending original order)
+    const uint8_t mode = static_cast<uint8_t>((p.mode & 2) | 1);
+    uint64_t need = 38 + 4 * rows + (mode & 2 ? 4 * p.cols : 0) + 8 + K;
     for (uint64_t b : br)
         for (uint64_t bc = 0; bc < BC; ++bc) {
             const uint64_t k = b * BC + bc;
@@ -553,6 +572,7 @@ sfmp_status sfmp_shard_extract(const uint8_t* bytes, size_t len, uint32_t shard,
     put(&mb, 4);
     put(&nb, 4);
     put(hdr, 4);
+    put(rank_of[shard].data(), rows * 4);
     if (mode & 2) put(p.col_perm, p.cols * 4);
     put(&K, 8);
     for (uint64_t b : br) put(p.bits + b * BC, BC);
@@ -575,19 +595,27 @@ sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device
     if (s) return s;
     std::vector<std::vector<uint64_t>> owned;
     std::vector<uint32_t> gmap;
+    std::vector<std::vector<uint32_t>> rank_of;
     uint64_t SR = 0;
-    if ((s = shard_plan(p, num_shards, owned, gmap, SR))) return s;
-    std::vector<uint32_t> local(owned[shard].size() * p.m_b);
-    std::iota(local.begin(), local.end(), 0u);
+    if ((s = shard_plan(p, num_shards, owned, gmap, SR, &rank_of))) return s;
     DevModel* d = nullptr;
-    s = build_model(bytes, p, device, owned[shard], local, SR, &d);
+    s = build_model(bytes, p, device, owned[shard], rank_of[shard], SR, &d);
     if (s) return s;
     d->shard = shard;
     d->num_shards = num_shards;
     d->shard_rows = SR;
     {
+        // inverse map: original row -> shard g << 24 | local position (SR < 2^24)
+        if (SR >= (1ull << 24) || num_shards > 255) {
+            free_model(d);
+            return fail(SFMP_ERR_UNSUPPORTED, "sharding supports < 2^24 rows per shard and < 256 shards");
+        }
+        std::vector<uint32_t> inv(p.rows, 0xFFFFFFFFu);
+        for (uint64_t k = 0; k < gmap.size(); ++k)
+            if (gmap[k] != 0xFFFFFFFFu) inv[gmap[k]] = static_cast<uint32_t>(((k / SR) << 24) | (k % SR));
         DeviceGuard guard(device);
         s = dev_upload(*d, &d->d_gather_map, gmap.data(), gmap.size() * 4);
+        if (!s) s = dev_upload(*d, &d->d_gather_inv, inv.data(), inv.size() * 4);
     }
     if (s) {
         free_model(d);

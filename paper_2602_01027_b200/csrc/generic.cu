@@ -138,17 +138,30 @@ __global__ void unpack_kernel(GenParams p, uint8_t* codes) {
     codes[idx] = static_cast<uint8_t>(row_ref(p.g, r, bc).code(jj));
 }
 
-// gathered[g][t][i] -> y[t][gather_map[g*SR+i]] (padding rows map to ~0u).
-__global__ void unpermute_kernel(const float* gathered, const uint32_t* gmap, float* y, int64_t M,
-                                 uint32_t G, uint64_t SR, uint64_t rows) {
-    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t total = static_cast<uint64_t>(G) * M * SR;
-    if (idx >= total) return;
-    const uint64_t i = idx % SR;
-    const uint64_t t = (idx / SR) % M;
-    const uint64_t g = idx / (SR * M);
-    const uint32_t dst = gmap[g * SR + i];
-    if (dst != 0xFFFFFFFFu) y[t * rows + dst] = gathered[idx];
+// y[t][r] = gathered[g][t][i] with g << 24 | i = inv[r] (inverse gather map):
+// CTA (row chunk, token); 4 rows per thread with one 16-byte write.  Writes
+// are coalesced and, since every shard's rows are in ascending original
+// order, the reads follow G sequential streams.
+__global__ void __launch_bounds__(256) unpermute_kernel(const float* __restrict__ gathered, const uint32_t* __restrict__ inv,
+                                                        float* __restrict__ y, int64_t M, uint64_t SR, uint64_t rows) {
+    const uint64_t t = blockIdx.y;
+    const uint64_t r0 = (static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
+    if (r0 >= rows) return;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        v[j] = 0.f;
+        if (r0 + j < rows) {
+            const uint32_t k = __ldg(inv + r0 + j);
+            v[j] = __ldg(gathered + ((k >> 24) * M + t) * SR + (k & 0xFFFFFFu));
+        }
+    }
+    float* yr = y + t * rows + r0;
+    if (r0 + 4 <= rows && (reinterpret_cast<uintptr_t>(yr) & 15) == 0) {
+        *reinterpret_cast<float4*>(yr) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+        for (int j = 0; j < 4 && r0 + j < rows; ++j) yr[j] = v[j];
+    }
 }
 
 // gemv_block (lutgemm.cpp:87-93): the contribution of block (br, bc) to its
@@ -261,11 +274,11 @@ cudaError_t launch_unpack(const DevModel& m, uint8_t* codes, cudaStream_t st) {
 
 cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, int64_t M, float* y,
                                       cudaStream_t st) {
-    const uint64_t total = static_cast<uint64_t>(m.num_shards) * M * m.shard_rows;
-    if (total == 0) return cudaSuccess;
+    if (M == 0 || m.global_rows == 0) return cudaSuccess;
+    if (M > 65535) return cudaErrorInvalidValue;
     note_launch();
-    unpermute_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-        gathered, m.d_gather_map, y, M, m.num_shards, m.shard_rows, m.global_rows);
+    unpermute_kernel<<<dim3(static_cast<unsigned>((m.global_rows + 1023) / 1024), static_cast<unsigned>(M)), 256, 0, st>>>(
+        gathered, m.d_gather_inv, y, M, m.shard_rows, m.global_rows);
     return cudaGetLastError();
 }
 

@@ -74,6 +74,7 @@ struct DevModel {
     uint64_t global_rows = 0;
     uint64_t shard_rows = 0;
     uint32_t* d_gather_map = nullptr;  // [num_shards*shard_rows] -> original row (or ~0 pad)
+    uint32_t* d_gather_inv = nullptr;  // [global_rows] original row -> shard << 24 | local position
 
     // K2 row-tile layout (gemm_tcgen05.cu): units of 128 output rows x 128
     // reordered columns, per-row bit-widths, gl_row_tiles (even) x cols/128.

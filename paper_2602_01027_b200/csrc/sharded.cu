@@ -29,35 +29,48 @@ namespace {
 
 constexpr int kMaxProb = 64;
 struct UnpermParams {
-    const uint32_t* gmap[kMaxProb];  // [G * SR] original row of (shard g, local row) or ~0
-    float* y[kMaxProb];               // [M][rows] original order
-    uint64_t off[kMaxProb + 1];       // first float of each problem in one shard's packed block (+ total)
+    const uint32_t* inv[kMaxProb];  // [rows] original row -> g * SR + local position
+    float* y[kMaxProb];             // [M][rows] original order
+    uint64_t off[kMaxProb];         // first float of each problem in one shard's packed block
+    int poff[kMaxProb + 1];         // first (problem, token) pair of each problem (+ total)
     uint32_t SR[kMaxProb];
     uint32_t rows[kMaxProb];
+    uint64_t total;                 // floats of one shard's packed block
     int n;
-    uint32_t G;
 };
 
-// gathered[g][total] -> y_i[t][gmap_i[g*SR_i + r]] for every problem i.
-__global__ void __launch_bounds__(256) unpermute_grouped_kernel(const float* __restrict__ gathered,
+// y_i[t][r] = recv[g][off_i + t*SR_i + k] with g << 24 | k = inv_i[r] for
+// every problem i.  CTA = (1024-row chunk, (problem, token) pair); the pair
+// is found once per CTA.  Coalesced 16-byte writes; each shard's rows are in
+// ascending original order, so the reads follow G sequential streams.
+__global__ void __launch_bounds__(256) unpermute_grouped_kernel(const float* __restrict__ recv,
                                                                 const UnpermParams p) {
-    const uint64_t total = p.off[p.n];
-    const uint64_t n_all = total * p.G;
-    for (uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n_all;
-         idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t g = static_cast<uint32_t>(idx / total);
-        const uint64_t o = idx - static_cast<uint64_t>(g) * total;
-        int lo = 0, hi = p.n - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (p.off[mid] <= o) lo = mid;
-            else hi = mid - 1;
+    const int pair = static_cast<int>(blockIdx.y);
+    int lo = 0, hi = p.n - 1;  // problem owning this (problem, token) pair
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p.poff[mid] <= pair) lo = mid;
+        else hi = mid - 1;
+    }
+    const uint64_t t = static_cast<uint64_t>(pair - p.poff[lo]);
+    const uint32_t rows = p.rows[lo], SR = p.SR[lo];
+    const uint64_t r0 = (static_cast<uint64_t>(blockIdx.x) * 256 + threadIdx.x) * 4;
+    if (r0 >= rows) return;
+    const float* src = recv + p.off[lo] + t * SR;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        v[j] = 0.f;
+        if (r0 + j < rows) {
+            const uint32_t k = __ldg(p.inv[lo] + r0 + j);
+            v[j] = __ldg(src + static_cast<uint64_t>(k >> 24) * p.total + (k & 0xFFFFFFu));
         }
-        const uint64_t e = o - p.off[lo];
-        const uint32_t SR = p.SR[lo];
-        const uint64_t t = e / SR, r = e - t * SR;
-        const uint32_t dst = __ldg(p.gmap[lo] + static_cast<uint64_t>(g) * SR + r);
-        if (dst != 0xFFFFFFFFu) p.y[lo][t * p.rows[lo] + dst] = __ldg(gathered + idx);
+    }
+    float* yr = p.y[lo] + t * rows + r0;
+    if (r0 + 4 <= rows && (reinterpret_cast<uintptr_t>(yr) & 15) == 0) {
+        *reinterpret_cast<float4*>(yr) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+        for (int j = 0; j < 4 && r0 + j < rows; ++j) yr[j] = v[j];
     }
 }
 
@@ -177,20 +190,24 @@ sfmp_status sfmp_sharded_unpermute(const sfmp_dev_model* const* models, const in
     const uint64_t total = sfmpk::packed_floats(ms, Ms, &off);
     if (total == 0) return SFMP_OK;
     p.n = count;
-    p.G = ms[0]->num_shards;
+    p.total = total;
+    uint64_t d = 0, maxrows = 0;
     for (int i = 0; i < count; ++i) {
         if (Ms[i] && !ys[i]) return api_fail(SFMP_ERR_INVALID_ARGUMENT, "null y");
-        p.gmap[i] = ms[i]->d_gather_map;
+        p.inv[i] = ms[i]->d_gather_inv;
         p.y[i] = ys[i];
         p.off[i] = off[i];
+        p.poff[i] = static_cast<int>(d);
         p.SR[i] = static_cast<uint32_t>(ms[i]->shard_rows);
         p.rows[i] = static_cast<uint32_t>(ms[i]->global_rows);
+        d += static_cast<uint64_t>(Ms[i]);
+        maxrows = std::max<uint64_t>(maxrows, ms[i]->global_rows);
     }
-    p.off[count] = total;
+    p.poff[count] = static_cast<int>(d);
+    if (d > 65535) return api_fail(SFMP_ERR_CONFIG, "sharded call: at most 65535 (problem, token) pairs");
     sfmpk::DeviceGuard guard(ms[0]->device);
     const float* recv = static_cast<const float*>(gather_buf) + total;  // [G][total] after the send block
-    const uint64_t n_all = total * p.G;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n_all + 255) / 256, 148ull * 16));
+    const dim3 grid(static_cast<unsigned>((maxrows + 1023) / 1024), static_cast<unsigned>(d));
     sfmpk::note_launch();
     sfmpk::unpermute_grouped_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(recv, p);
     const cudaError_t e = cudaGetLastError();
