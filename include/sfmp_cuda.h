@@ -150,6 +150,15 @@ sfmp_status sfmp_shard_extract(const uint8_t* bytes, size_t len, uint32_t shard,
                                uint8_t* out, size_t* out_len);
 sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device,
                                     uint32_t shard, uint32_t num_shards, sfmp_dev_model** out);
+/* Model creation flags.  Default (0): both device layouts -- the decode
+ * GEMV's unit-major layout and the prefill GEMM's row-tile layout (~2x the
+ * SFMPPKD1 payload).  SFMP_MODEL_DECODE_ONLY keeps only the decode layout
+ * (~1.0x): M > 16 then runs the decode GEMV in 16-token chunks. */
+#define SFMP_MODEL_DECODE_ONLY 1u
+sfmp_status sfmp_model_create_ex(const uint8_t* bytes, size_t len, int device, uint32_t flags,
+                                 sfmp_dev_model** out);
+sfmp_status sfmp_model_create_shard_ex(const uint8_t* bytes, size_t len, int device, uint32_t shard,
+                                       uint32_t num_shards, uint32_t flags, sfmp_dev_model** out);
 sfmp_status sfmp_model_destroy(sfmp_dev_model* model);
 sfmp_status sfmp_model_get_info(const sfmp_dev_model* model, sfmp_model_info* info);
 

@@ -43,8 +43,9 @@ EXPORTED_SYMBOLS = (
     "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v", "sfmp_gemm_stats",
     "sfmp_gemm_host_stats", "sfmp_launch_count", "sfmp_sharded_gather_bytes", "sfmp_gemm_sharded_local",
     "sfmp_sharded_unpermute", "sfmp_gemm_sharded", "sfmp_nccl_unique_id", "sfmp_nccl_comm_init",
-    "sfmp_nccl_comm_destroy", "sfmp_gemv_block",
+    "sfmp_nccl_comm_destroy", "sfmp_gemv_block", "sfmp_model_create_ex", "sfmp_model_create_shard_ex",
 )
+MODEL_DECODE_ONLY = 1
 NCCL_ID_BYTES = 128
 
 
@@ -155,6 +156,8 @@ def lib() -> C.CDLL:
     L.sfmp_nccl_comm_init.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)]
     L.sfmp_nccl_comm_destroy.argtypes = [vp]
     L.sfmp_gemv_block.argtypes = [vp, C.c_uint64, vp, vp, vp]
+    L.sfmp_model_create_ex.argtypes = [vp, sz, C.c_int, C.c_uint32, C.POINTER(vp)]
+    L.sfmp_model_create_shard_ex.argtypes = [vp, sz, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp)]
     for name in ("sfmp_parse_header", "sfmp_block_offsets", "sfmp_model_create",
                  "sfmp_model_create_shard", "sfmp_model_destroy", "sfmp_model_get_info",
                  "sfmp_workspace_size", "sfmp_gemm", "sfmp_gemm_ex", "sfmp_gemm_host",
@@ -162,7 +165,8 @@ def lib() -> C.CDLL:
                  "sfmp_shard_plan", "sfmp_shard_extract", "sfmp_gemm_grouped", "sfmp_gemm_grouped_v",
                  "sfmp_gemm_stats", "sfmp_gemm_host_stats", "sfmp_sharded_gather_bytes",
                  "sfmp_gemm_sharded_local", "sfmp_sharded_unpermute", "sfmp_gemm_sharded",
-                 "sfmp_nccl_unique_id", "sfmp_nccl_comm_init", "sfmp_nccl_comm_destroy", "sfmp_gemv_block"):
+                 "sfmp_nccl_unique_id", "sfmp_nccl_comm_init", "sfmp_nccl_comm_destroy", "sfmp_gemv_block",
+                 "sfmp_model_create_ex", "sfmp_model_create_shard_ex"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -255,14 +259,15 @@ class DeviceModel:
     """A packed model resident on one B200 (sfmp_model_create)."""
 
     def __init__(self, data: bytes, device: int = 0, shard: int | None = None,
-                 num_shards: int = 1):
+                 num_shards: int = 1, flags: int = 0):
+        """flags: MODEL_DECODE_ONLY keeps only the decode layout (~1x payload)."""
         self._h = C.c_void_p()
         self._data_len = len(data)
         if shard is None:
-            check(lib().sfmp_model_create(data, len(data), device, C.byref(self._h)))
+            check(lib().sfmp_model_create_ex(data, len(data), device, flags, C.byref(self._h)))
         else:
-            check(lib().sfmp_model_create_shard(data, len(data), device, shard, num_shards,
-                                                C.byref(self._h)))
+            check(lib().sfmp_model_create_shard_ex(data, len(data), device, shard, num_shards, flags,
+                                                   C.byref(self._h)))
         info = ModelInfo()
         check(lib().sfmp_model_get_info(self._h, C.byref(info)))
         self.info = info.as_dict()

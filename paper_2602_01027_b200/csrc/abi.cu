@@ -211,7 +211,7 @@ sfmp_status build_gemv_schedule(DevModel& d) {
 // local reordered row -> column of y.
 sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
                         const std::vector<uint64_t>& brows, const std::vector<uint32_t>& out_map,
-                        uint64_t out_rows, DevModel** out) {
+                        uint64_t out_rows, DevModel** out, uint32_t flags = 0) {
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -280,7 +280,7 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
     if ((s = dev_upload(*d, &d->d_col_perm, cp.data(), cp.size() * 4))) return s;
     if ((s = dev_upload(*d, &d->d_out_map, out_map.data(), out_map.size() * 4))) return s;
     if ((s = build_gemv_schedule(*d))) return s;
-    {
+    if (!(flags & SFMP_MODEL_DECODE_ONLY) || !d->gemv_ok) {  // the prefill GEMM's own layout
         std::vector<uint8_t> wl;
         std::vector<uint64_t> woff;
         if (sfmpk::build_gemm_layout(*d, payload, out_map, wl, woff)) {
@@ -458,7 +458,12 @@ sfmp_status sfmp_block_offsets(const uint8_t* bytes, size_t len, uint64_t* offse
 }
 
 sfmp_status sfmp_model_create(const uint8_t* bytes, size_t len, int device, sfmp_dev_model** out) {
+    return sfmp_model_create_ex(bytes, len, device, 0, out);
+}
+
+sfmp_status sfmp_model_create_ex(const uint8_t* bytes, size_t len, int device, uint32_t flags, sfmp_dev_model** out) {
     if (!out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out");
+    if (flags & ~static_cast<uint32_t>(SFMP_MODEL_DECODE_ONLY)) return fail(SFMP_ERR_INVALID_ARGUMENT, "unknown model flags");
     *out = nullptr;
     Parsed p;
     sfmp_status s = parse(bytes, len, p);
@@ -466,7 +471,7 @@ sfmp_status sfmp_model_create(const uint8_t* bytes, size_t len, int device, sfmp
     std::vector<uint64_t> brows(p.rows / p.m_b);
     std::iota(brows.begin(), brows.end(), 0ull);
     DevModel* d = nullptr;
-    s = build_model(bytes, p, device, brows, row_order(p), p.rows, &d);
+    s = build_model(bytes, p, device, brows, row_order(p), p.rows, &d, flags);
     if (s) return s;
     *out = reinterpret_cast<sfmp_dev_model*>(d);
     return SFMP_OK;
@@ -587,7 +592,13 @@ sfmp_status sfmp_shard_extract(const uint8_t* bytes, size_t len, uint32_t shard,
 
 sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device, uint32_t shard,
                                     uint32_t num_shards, sfmp_dev_model** out) {
+    return sfmp_model_create_shard_ex(bytes, len, device, shard, num_shards, 0, out);
+}
+
+sfmp_status sfmp_model_create_shard_ex(const uint8_t* bytes, size_t len, int device, uint32_t shard,
+                                       uint32_t num_shards, uint32_t flags, sfmp_dev_model** out) {
     if (!out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out");
+    if (flags & ~static_cast<uint32_t>(SFMP_MODEL_DECODE_ONLY)) return fail(SFMP_ERR_INVALID_ARGUMENT, "unknown model flags");
     *out = nullptr;
     if (num_shards < 1 || shard >= num_shards) return fail(SFMP_ERR_CONFIG, "bad shard index/count");
     Parsed p;
@@ -599,7 +610,7 @@ sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device
     uint64_t SR = 0;
     if ((s = shard_plan(p, num_shards, owned, gmap, SR, &rank_of))) return s;
     DevModel* d = nullptr;
-    s = build_model(bytes, p, device, owned[shard], rank_of[shard], SR, &d);
+    s = build_model(bytes, p, device, owned[shard], rank_of[shard], SR, &d, flags);
     if (s) return s;
     d->shard = shard;
     d->num_shards = num_shards;

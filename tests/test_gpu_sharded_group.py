@@ -206,3 +206,23 @@ def test_two_processes_gloo_real_shard_kernels(gpu, port, tmp_path):
         procs.append(subprocess.Popen([sys.executable, str(script)], env=env))
     codes = [p.wait(timeout=300) for p in procs]
     assert codes == [0, 0]
+
+
+def test_decode_only_model_memory(gpu, port):
+    """SFMP_MODEL_DECODE_ONLY: one resident weight layout (<= 1.1x the SFMPPKD1
+    payload); decode bits equal the default model's; M > 16 runs the decode
+    GEMV in 16-token chunks within the parity bar; the GEMM path is refused."""
+    import torch
+    data = model_bytes(port, 4096, 4096, 3.25)
+    full = gpu.DeviceModel(data)
+    lean = gpu.DeviceModel(data, flags=gpu.MODEL_DECODE_ONLY)
+    assert lean.info["device_bytes"] <= 1.1 * lean.info["payload_bytes"], lean.info
+    assert full.info["device_bytes"] > 1.8 * full.info["payload_bytes"]
+    x = torch.from_numpy(activations(port, 5, 4096, seed=4)).cuda().to(torch.bfloat16)
+    assert torch.equal(lean.gemm(x), full.gemm(x, path=gpu.PATH_GEMV))
+    x40 = activations(port, 40, 4096, seed=6)
+    y = lean.gemm(torch.from_numpy(x40).cuda()).cpu().numpy()
+    ref = port.matmul(x40, port.load(data).dequantize(), threads=8)
+    assert errors(y, ref)[0] <= 1e-3
+    with pytest.raises(gpu.UnsupportedError):
+        lean.gemm(torch.from_numpy(x40).cuda(), path=gpu.PATH_GEMM)
