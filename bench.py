@@ -668,6 +668,37 @@ def main():
             b = sum(algo_bytes(models[0][p].info, M, models[0][p].rows, SHAPES[p][1]) for p, M in kk)
             per_launch[name] = {"problems": len(kk), "bytes": b, **roof(b, sum(2.0 * M * SHAPES[p][0] * SHAPES[p][1]
                                                                                for p, M in kk), us, hbm, tc)}
+    # ---- §8(f)1: RMSNorm fused into the activation pre-pass vs a separate norm ----
+    fused_norm = None
+    if not sharded and grouped and not args.no_extras:
+        import torch.nn.functional as F
+        normed = ("q_proj", "k_proj", "v_proj", "gate_proj", "up_proj")  # o/down take other inputs
+        gam = {p: (0.9 + 0.2 * torch.rand(SHAPES[p][1], device=dev)).to(torch.bfloat16) for p in PROJS}
+        norms = [(gam[p], 1e-5) if p in normed else None for p, M in keys_all]
+
+        def fused(i):
+            ms = [models[(i * len(MS) + MS.index(M)) % COPIES][p] for p, M in keys_all]
+            sfmp.gemm_grouped(ms, [xs[k] for k in keys_all], outs=[ys[k] for k in keys_all],
+                              workspaces=[wsm[k] for k in keys_all], norms=norms)
+
+        xn = {}
+
+        def unfused(i):
+            # the separate norm kernels a model would run first: one per shared input
+            for M in MS:
+                for p in ("q_proj", "gate_proj"):
+                    xn[(p, M)] = F.rms_norm(xs[(p, M)], (SHAPES[p][1],), gam[p], 1e-5)
+            ms = [models[(i * len(MS) + MS.index(M)) % COPIES][p] for p, M in keys_all]
+            src = [xn[("q_proj" if p in ("q_proj", "k_proj", "v_proj") else "gate_proj", M)] if p in normed
+                   else xs[(p, M)] for p, M in keys_all]
+            sfmp.gemm_grouped(ms, src, outs=[ys[k] for k in keys_all], workspaces=[wsm[k] for k in keys_all])
+        with torch.cuda.stream(stream):
+            fu = graph_us(lambda: [fused(i) for i in range(COPIES)], stream, max(3, args.steps // 5), COPIES)
+            un = graph_us(lambda: [unfused(i) for i in range(COPIES)], stream, max(3, args.steps // 5), COPIES)
+        fused_norm = {"what": "8B decode step with the pre-attention / pre-MLP RMSNorm: fused into the activation "
+                              "pre-pass (sfmp_gemm_grouped_v_norm) vs torch rms_norm kernels + the grouped call",
+                      "fused_us": round(fu, 2), "separate_us": round(un, 2)}
+
     kernel_us = None
     if sharded:
         with torch.cuda.stream(stream):
@@ -862,6 +893,8 @@ def main():
                              f"when the step was enqueued",
         "clocks": clk,
     }
+    if fused_norm:
+        extras["fused_rmsnorm"] = fused_norm
     if extras:
         out["extras"] = extras
     if not sharded and not args.no_prefill:

@@ -88,7 +88,8 @@ typedef struct sfmp_model_info {
     uint64_t blocks_high;          /* blocks at ceil_bits (when ceil != floor)            */
     double avg_code_bits;          /* sum_k bits_k / K                                    */
     uint64_t payload_bytes;        /* bytes of the block region (scales+zeros+planes)     */
-    uint64_t device_bytes;         /* device memory held by the model                     */
+    uint64_t device_bytes;         /* device memory of the weight layouts + indices (the
+                                      model's default workspace is not counted)           */
     uint32_t shard, num_shards;    /* (0,1) for an unsharded model                        */
     uint64_t out_rows;             /* length of one output row of y written by sfmp_gemm  */
     uint64_t global_rows;          /* rows of the whole (unsharded) matrix                */
@@ -193,6 +194,26 @@ sfmp_status sfmp_gemm_grouped(const sfmp_dev_model* const* models, const void* c
 sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
                                 const int64_t* Ms, float* const* ys, void* const* workspaces,
                                 const size_t* workspace_bytes, int count, void* stream);
+/* RMSNorm fused into the activation pre-pass (the "fused activation producer"
+ * of SURVEY §8(f)1): x is the UNNORMALISED hidden state h and the GEMM uses
+ *     x[t][j] = h[t][j] / sqrt(mean_j h[t][j]^2 + eps) * gamma[j]   (f32)
+ * (the Llama pre-attention / pre-MLP norm).  The pre-pass already stages
+ * every token row to gather it by col_perm, so the norm costs no extra pass
+ * over x.  gamma = NULL means 1.  SFMP_ERR_UNSUPPORTED for the generic path
+ * and for rows too wide for the staged decode pre-pass (> 192 KB). */
+typedef struct sfmp_prenorm {
+    const void* gamma;       /* [cols] device pointer, or NULL */
+    sfmp_dtype gamma_dtype;
+    float eps;
+    int32_t enabled;         /* 0: x is used as given (lets a grouped call mix normed and plain inputs) */
+} sfmp_prenorm;
+sfmp_status sfmp_gemm_norm(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M, float* y,
+                           void* workspace, size_t workspace_bytes, const sfmp_prenorm* norm, void* stream);
+/* sfmp_gemm_grouped_v with one norm per problem (norms[count]). */
+sfmp_status sfmp_gemm_grouped_v_norm(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                                     const int64_t* Ms, float* const* ys, void* const* workspaces,
+                                     const size_t* workspace_bytes, int count, const sfmp_prenorm* norms,
+                                     void* stream);
 /* Host-buffer convenience with the reference's calling convention: x and y
  * are HOST arrays; copies, kernel and synchronisation happen inside. */
 sfmp_status sfmp_gemm_host(const sfmp_dev_model* model, const float* x_host, int64_t M,

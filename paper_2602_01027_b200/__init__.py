@@ -44,6 +44,7 @@ EXPORTED_SYMBOLS = (
     "sfmp_gemm_host_stats", "sfmp_launch_count", "sfmp_sharded_gather_bytes", "sfmp_gemm_sharded_local",
     "sfmp_sharded_unpermute", "sfmp_gemm_sharded", "sfmp_nccl_unique_id", "sfmp_nccl_comm_init",
     "sfmp_nccl_comm_destroy", "sfmp_gemv_block", "sfmp_model_create_ex", "sfmp_model_create_shard_ex",
+    "sfmp_gemm_norm", "sfmp_gemm_grouped_v_norm",
 )
 MODEL_DECODE_ONLY = 1
 NCCL_ID_BYTES = 128
@@ -103,6 +104,22 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class PreNorm(C.Structure):
+    """sfmp_prenorm: RMSNorm fused into the activation pre-pass."""
+    _fields_ = [("gamma", C.c_void_p), ("gamma_dtype", C.c_int), ("eps", C.c_float), ("enabled", C.c_int32)]
+
+
+def _prenorm(norm):
+    """norm = (gamma tensor or None, eps) -> PreNorm; None -> a disabled entry."""
+    if norm is None:
+        return PreNorm(None, F32, 0.0, 0)
+    gamma, eps = norm
+    if gamma is None:
+        return PreNorm(None, F32, float(eps), 1)
+    gamma = gamma.contiguous()
+    return PreNorm(gamma.data_ptr(), _dtype_code(gamma), float(eps), 1)
+
+
 _lib = None
 
 
@@ -156,6 +173,8 @@ def lib() -> C.CDLL:
     L.sfmp_nccl_comm_init.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)]
     L.sfmp_nccl_comm_destroy.argtypes = [vp]
     L.sfmp_gemv_block.argtypes = [vp, C.c_uint64, vp, vp, vp]
+    L.sfmp_gemm_norm.argtypes = [vp, vp, C.c_int, i64, vp, vp, sz, C.POINTER(PreNorm), vp]
+    L.sfmp_gemm_grouped_v_norm.argtypes = [vp, vp, C.c_int, vp, vp, vp, vp, C.c_int, C.POINTER(PreNorm), vp]
     L.sfmp_model_create_ex.argtypes = [vp, sz, C.c_int, C.c_uint32, C.POINTER(vp)]
     L.sfmp_model_create_shard_ex.argtypes = [vp, sz, C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(vp)]
     for name in ("sfmp_parse_header", "sfmp_block_offsets", "sfmp_model_create",
@@ -166,7 +185,8 @@ def lib() -> C.CDLL:
                  "sfmp_gemm_stats", "sfmp_gemm_host_stats", "sfmp_sharded_gather_bytes",
                  "sfmp_gemm_sharded_local", "sfmp_sharded_unpermute", "sfmp_gemm_sharded",
                  "sfmp_nccl_unique_id", "sfmp_nccl_comm_init", "sfmp_nccl_comm_destroy", "sfmp_gemv_block",
-                 "sfmp_model_create_ex", "sfmp_model_create_shard_ex"):
+                 "sfmp_model_create_ex", "sfmp_model_create_shard_ex", "sfmp_gemm_norm",
+                 "sfmp_gemm_grouped_v_norm"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -304,8 +324,9 @@ class DeviceModel:
             self._ws[key] = torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
         return self._ws.get(key)
 
-    def gemm(self, x, out=None, path: int = PATH_AUTO, workspace=None, stream=None):
-        """y[M, out_rows] (f32) = x[M, cols] . W^T, x/y torch CUDA tensors, original order."""
+    def gemm(self, x, out=None, path: int = PATH_AUTO, workspace=None, stream=None, norm=None):
+        """y[M, out_rows] (f32) = x[M, cols] . W^T, x/y torch CUDA tensors, original order.
+        norm=(gamma, eps): x is the unnormalised hidden state, RMSNorm fused (sfmp_gemm_norm)."""
         import torch
         if x.dim() == 1:
             x = x.unsqueeze(0)
@@ -316,6 +337,15 @@ class DeviceModel:
         if out is None:
             out = torch.empty(M, self.out_rows, dtype=torch.float32, device=x.device)
         ws = workspace if workspace is not None else self.workspace(M, path)
+        if norm is not None:
+            if path != PATH_AUTO:
+                raise ConfigError("a fused norm takes the automatic path")
+            pn = _prenorm(norm)
+            check(lib().sfmp_gemm_norm(self._h, C.c_void_p(x.data_ptr()), _dtype_code(x), M,
+                                       C.c_void_p(out.data_ptr()),
+                                       C.c_void_p(ws.data_ptr()) if ws is not None else None,
+                                       ws.numel() if ws is not None else 0, C.byref(pn), _stream_ptr(stream)))
+            return out
         check(lib().sfmp_gemm_ex(self._h, C.c_void_p(x.data_ptr()), _dtype_code(x), M,
                                  C.c_void_p(out.data_ptr()),
                                  C.c_void_p(ws.data_ptr()) if ws is not None else None,
@@ -386,7 +416,7 @@ class DeviceModel:
         return out
 
 
-def gemm_grouped(models, xs, outs=None, workspaces=None, stream=None):
+def gemm_grouped(models, xs, outs=None, workspaces=None, stream=None, norms=None):
     """Independent linears in one call: y_i = x_i . W_i^T, x_i [M_i, cols_i] of one
     dtype (M_i may differ: sfmp_gemm_grouped_v).  Decode problems (M_i <= 16) of
     one n-tile class (M <= 8 or 9..16) with distinct workspaces share one
@@ -410,6 +440,10 @@ def gemm_grouped(models, xs, outs=None, workspaces=None, stream=None):
     wp = P(*[(w.data_ptr() if w is not None else None) for w in workspaces])
     wb = (C.c_size_t * n)(*[(w.numel() if w is not None else 0) for w in workspaces])
     mp = (C.c_int64 * n)(*Ms)
+    if norms is not None:  # one (gamma, eps) per problem: RMSNorm fused into the pre-pass
+        pn = (PreNorm * n)(*[_prenorm(v) for v in norms])
+        check(lib().sfmp_gemm_grouped_v_norm(hs, xp, dt, mp, yp, wp, wb, n, pn, _stream_ptr(stream)))
+        return outs
     check(lib().sfmp_gemm_grouped_v(hs, xp, dt, mp, yp, wp, wb, n, _stream_ptr(stream)))
     return outs
 

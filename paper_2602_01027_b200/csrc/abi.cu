@@ -300,6 +300,7 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
     if (ws) {
         if ((s = dev_upload<float>(*d, &d->d_ws, nullptr, ws))) return s;
         d->ws_bytes = ws;
+        d->device_bytes -= ws;  // device_bytes: weight layouts and indices only
     }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "upload sync");
     *out = d.release();
@@ -367,6 +368,26 @@ sfmp_path resolve_path(const DevModel& d, int64_t M, const void* x, sfmp_path pa
     if (path == SFMP_PATH_AUTO)
         path = (M > 16 && d.gemm_ok && x_aligned) ? SFMP_PATH_GEMM : (d.gemv_ok ? SFMP_PATH_GEMV : SFMP_PATH_GENERIC);
     return path;
+}
+
+sfmp_status gemm_impl(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M, float* y,
+                      void* workspace, size_t workspace_bytes, sfmp_path path, void* stream,
+                      const sfmpk::PreNorm* norm);
+sfmp_status grouped_impl(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                         const int64_t* Ms, float* const* ys, void* const* workspaces, const size_t* workspace_bytes,
+                         int count, void* stream, const sfmpk::PreNorm* norms);
+
+sfmp_status to_prenorm(const sfmp_prenorm* n, sfmpk::PreNorm& out) {
+    out = sfmpk::PreNorm{};
+    if (!n || !n->enabled) return SFMP_OK;
+    if (n->gamma_dtype != SFMP_F32 && n->gamma_dtype != SFMP_F16 && n->gamma_dtype != SFMP_BF16)
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "bad gamma dtype");
+    if (!(n->eps >= 0.f)) return fail(SFMP_ERR_INVALID_ARGUMENT, "eps must be >= 0");
+    out.gamma = n->gamma;
+    out.gdt = n->gamma_dtype;
+    out.eps = n->eps;
+    out.on = 1;
+    return SFMP_OK;
 }
 
 double now_us() {
@@ -680,6 +701,23 @@ sfmp_status sfmp_workspace_size(const sfmp_dev_model* model, int64_t M, sfmp_pat
 sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M,
                          float* y, void* workspace, size_t workspace_bytes, sfmp_path path,
                          void* stream) {
+    return gemm_impl(model, x, dtype, M, y, workspace, workspace_bytes, path, stream, nullptr);
+}
+
+sfmp_status sfmp_gemm_norm(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M, float* y,
+                           void* workspace, size_t workspace_bytes, const sfmp_prenorm* norm, void* stream) {
+    sfmpk::PreNorm pn;
+    sfmp_status s = to_prenorm(norm, pn);
+    if (s) return s;
+    return gemm_impl(model, x, dtype, M, y, workspace, workspace_bytes, SFMP_PATH_AUTO, stream, norm ? &pn : nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+sfmp_status gemm_impl(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M, float* y,
+                      void* workspace, size_t workspace_bytes, sfmp_path path, void* stream,
+                      const sfmpk::PreNorm* norm) {
     if (!model) return fail(SFMP_ERR_INVALID_ARGUMENT, "null model");
     if (M < 0) return fail(SFMP_ERR_SHAPE, "negative M");
     if (M == 0) return SFMP_OK;
@@ -708,7 +746,7 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
             for (int64_t t0 = 0; t0 < M && e == cudaSuccess; t0 += 16) {
                 const int mt = static_cast<int>(std::min<int64_t>(16, M - t0));
                 e = sfmpk::launch_gemv(d, static_cast<const uint8_t*>(x) + t0 * d.cols * esz, dtype, mt,
-                                       y + t0 * d.out_rows, ws, st);
+                                       y + t0 * d.out_rows, ws, st, norm);
             }
             break;
         }
@@ -717,15 +755,25 @@ sfmp_status sfmp_gemm_ex(const sfmp_dev_model* model, const void* x, sfmp_dtype 
             const size_t need = sfmpk::gemm_workspace_bytes(d, M);
             if (need && (!workspace || workspace_bytes < need))
                 return fail(SFMP_ERR_CONFIG, "GEMM path needs a workspace (sfmp_workspace_size)");
-            e = sfmpk::launch_gemm(d, x, dtype, M, y, workspace, st);
+            e = sfmpk::launch_gemm(d, x, dtype, M, y, workspace, st, norm);
             break;
         }
-        case SFMP_PATH_GENERIC: e = sfmpk::launch_generic(d, x, dtype, M, y, st); break;
+        case SFMP_PATH_GENERIC:
+            if (norm && norm->on) return fail(SFMP_ERR_UNSUPPORTED, "fused RMSNorm needs the GEMV or GEMM path");
+            e = sfmpk::launch_generic(d, x, dtype, M, y, st);
+            break;
         default: return fail(SFMP_ERR_INVALID_ARGUMENT, "bad path");
+    }
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return fail(SFMP_ERR_UNSUPPORTED, "fused RMSNorm: the x row does not fit the staged pre-pass");
     }
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     return SFMP_OK;
 }
+}  // namespace
+
+extern "C" {
 
 sfmp_status sfmp_gemm_grouped(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
                               int64_t M, float* const* ys, void* const* workspaces, const size_t* workspace_bytes,
@@ -739,6 +787,28 @@ sfmp_status sfmp_gemm_grouped(const sfmp_dev_model* const* models, const void* c
 sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
                                 const int64_t* Ms, float* const* ys, void* const* workspaces,
                                 const size_t* workspace_bytes, int count, void* stream) {
+    return grouped_impl(models, xs, dtype, Ms, ys, workspaces, workspace_bytes, count, stream, nullptr);
+}
+
+sfmp_status sfmp_gemm_grouped_v_norm(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                                     const int64_t* Ms, float* const* ys, void* const* workspaces,
+                                     const size_t* workspace_bytes, int count, const sfmp_prenorm* norms,
+                                     void* stream) {
+    if (count < 0 || (count && !norms)) return fail(SFMP_ERR_INVALID_ARGUMENT, "null norms");
+    std::vector<sfmpk::PreNorm> pn(count > 0 ? count : 1);
+    for (int i = 0; i < count; ++i) {
+        sfmp_status s = to_prenorm(&norms[i], pn[i]);
+        if (s) return s;
+    }
+    return grouped_impl(models, xs, dtype, Ms, ys, workspaces, workspace_bytes, count, stream, pn.data());
+}
+
+}  // extern "C"
+
+namespace {
+sfmp_status grouped_impl(const sfmp_dev_model* const* models, const void* const* xs, sfmp_dtype dtype,
+                         const int64_t* Ms, float* const* ys, void* const* workspaces, const size_t* workspace_bytes,
+                         int count, void* stream, const sfmpk::PreNorm* norms) {
     if (count < 0 || (count && (!models || !xs || !ys || !workspaces || !Ms)))
         return fail(SFMP_ERR_INVALID_ARGUMENT, "null argument");
     if (count == 0) return SFMP_OK;
@@ -796,14 +866,20 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
                 for (const void* w : used_ws) disjoint = disjoint && w != workspaces[k];
             const bool overlap = prev_decode && disjoint;
             cudaError_t e = sfmpk::launch_gemv_group(ms.data() + i, xs + i, ys + i, wss.data(), mi.data(), j - i, dtype,
-                                                     static_cast<cudaStream_t>(stream), overlap);
+                                                     static_cast<cudaStream_t>(stream), overlap,
+                                                     norms ? norms + i : nullptr);
+            if (e == cudaErrorNotSupported) {
+                cudaGetLastError();
+                return fail(SFMP_ERR_UNSUPPORTED, "fused RMSNorm: the x row does not fit the staged pre-pass");
+            }
             if (e != cudaSuccess) return cuda_fail(e, "grouped GEMV launch");
             for (int k = i; k < j; ++k) used_ws.push_back(workspaces[k]);
             prev_decode = true;
         } else {
             // workspace_bytes == NULL: the caller vouches for the sizes
-            sfmp_status s = sfmp_gemm(models[i], xs[i], dtype, Ms[i], ys[i], workspaces[i],
-                                      workspace_bytes ? workspace_bytes[i] : (workspaces[i] ? SIZE_MAX : 0), stream);
+            sfmp_status s = gemm_impl(models[i], xs[i], dtype, Ms[i], ys[i], workspaces[i],
+                                      workspace_bytes ? workspace_bytes[i] : (workspaces[i] ? SIZE_MAX : 0),
+                                      SFMP_PATH_AUTO, stream, norms ? norms + i : nullptr);
             if (s) return s;
             prev_decode = false;  // the next decode launch follows a non-grouped kernel
         }
@@ -811,6 +887,9 @@ sfmp_status sfmp_gemm_grouped_v(const sfmp_dev_model* const* models, const void*
     }
     return SFMP_OK;
 }
+}  // namespace
+
+extern "C" {
 
 sfmp_status sfmp_gemm(const sfmp_dev_model* model, const void* x, sfmp_dtype dtype, int64_t M, float* y,
                       void* workspace, size_t workspace_bytes, void* stream) {

@@ -50,6 +50,7 @@
 #include <mutex>
 #include <type_traits>
 
+#include "prenorm.cuh"
 #include "ptx.cuh"
 #include "sfmp_internal.h"
 #include "tc.cuh"
@@ -137,7 +138,7 @@ template <sfmp_dtype DT>
 __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __restrict__ x,
                                                               const uint32_t* __restrict__ xslot,
                                                               uint8_t* __restrict__ xs, float* __restrict__ ysc, int M,
-                                                              int N, int KC, int cols, int Mpad) {
+                                                              int N, int KC, int cols, int Mpad, const PreNorm norm) {
     using T = std::conditional_t<DT == SFMP_F32, float, uint16_t>;
     extern __shared__ __align__(16) uint8_t xsm[];
     __shared__ float red[16];
@@ -175,12 +176,21 @@ __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __rest
         uint8_t* dst = xs + static_cast<size_t>(tt) * KC * 2 * N * 128 + r * 128;
         const T* xr = reinterpret_cast<const T*>(rowbuf + buf * static_cast<size_t>(row_bytes));
         if (t < M) mbar_wait(&bar[buf], static_cast<uint32_t>(k >> 1) & 1u);
-        float sc = 1.f;
-        if constexpr (DT != SFMP_F16) {
+        float sc = 1.f, inv = 1.f;  // inv: fused RMSNorm (prenorm.cuh)
+        if (DT != SFMP_F16 || norm.on) {
             float m = 0.f;
-            if (t < M)
-                for (int i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(x_as_float<DT>(xr[i])));
-            const int e = token_exp(block_max(m, red));
+            if (norm.on) {
+                inv = row_inv_rms([&](int i) { return t < M ? x_as_float<DT>(xr[i]) : 0.f; }, cols, norm.eps, red);
+                if (t < M)
+                    for (int i = threadIdx.x; i < cols; i += blockDim.x)
+                        m = fmaxf(m, fabsf(x_as_float<DT>(xr[i]) * gamma_at(norm, i)));
+                m = block_max(m, red) * inv;
+            } else {
+                if (t < M)
+                    for (int i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(x_as_float<DT>(xr[i])));
+                m = block_max(m, red);
+            }
+            const int e = token_exp(m);
             sc = ldexpf(1.f, -e);
             if (threadIdx.x == 0) ysc[t] = t < M ? ldexpf(1.f, e) : 0.f;
         } else {
@@ -195,9 +205,13 @@ __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __rest
                 uint32_t o[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const T lo = xr[iv[e] & 0xFFFFu], hi = xr[iv[e] >> 16];
-                    if constexpr (DT == SFMP_F16) {
+                    const uint32_t clo = iv[e] & 0xFFFFu, chi = iv[e] >> 16;
+                    const T lo = xr[clo], hi = xr[chi];
+                    if (DT == SFMP_F16 && !norm.on) {
                         o[e] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+                    } else if (norm.on) {
+                        o[e] = h2_as_u32(__floats2half2_rn((x_as_float<DT>(lo) * inv) * gamma_at(norm, clo) * sc,
+                                                           (x_as_float<DT>(hi) * inv) * gamma_at(norm, chi) * sc));
                     } else {
                         o[e] = h2_as_u32(__floats2half2_rn(x_as_float<DT>(lo) * sc, x_as_float<DT>(hi) * sc));
                     }
@@ -227,7 +241,7 @@ __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __rest
 template <sfmp_dtype DT>
 __global__ void __launch_bounds__(1024) xprep_gemm_kernel(const void* __restrict__ x, const uint32_t* __restrict__ xslot,
                                                          uint8_t* __restrict__ xs, float* __restrict__ ysc, int M, int N,
-                                                         int KC, int cols, int Mpad) {
+                                                         int KC, int cols, int Mpad, const PreNorm norm) {
     using T = std::conditional_t<DT == SFMP_F32, float, uint16_t>;
     extern __shared__ __align__(16) __half xrow[];
     __shared__ float red[32];
@@ -237,18 +251,27 @@ __global__ void __launch_bounds__(1024) xprep_gemm_kernel(const void* __restrict
         uint8_t* dst = xs + static_cast<size_t>(tt) * KC * 2 * N * 128 + r * 128;
         if (t < M) {
             const T* src = static_cast<const T*>(x) + static_cast<size_t>(t) * cols;
-            float sc = 1.f;
-            if constexpr (DT != SFMP_F16) {
+            float sc = 1.f, inv = 1.f;  // inv: fused RMSNorm (prenorm.cuh)
+            if (DT != SFMP_F16 || norm.on) {
                 float m = 0.f;
-                for (int i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(x_as_float<DT>(src[i])));
-                const int e = token_exp(block_max(m, red));
+                if (norm.on) {
+                    inv = row_inv_rms([&](int i) { return x_as_float<DT>(src[i]); }, cols, norm.eps, red);
+                    for (int i = threadIdx.x; i < cols; i += blockDim.x)
+                        m = fmaxf(m, fabsf(x_as_float<DT>(src[i]) * gamma_at(norm, i)));
+                    m = block_max(m, red) * inv;
+                } else {
+                    for (int i = threadIdx.x; i < cols; i += blockDim.x) m = fmaxf(m, fabsf(x_as_float<DT>(src[i])));
+                    m = block_max(m, red);
+                }
+                const int e = token_exp(m);
                 sc = ldexpf(1.f, -e);
                 if (threadIdx.x == 0) ysc[t] = ldexpf(1.f, e);
             } else if (threadIdx.x == 0) {
                 ysc[t] = 1.f;
             }
             for (int i = threadIdx.x; i < cols; i += blockDim.x) {
-                if constexpr (DT == SFMP_F16) xrow[i] = __ushort_as_half(src[i]);
+                if (DT == SFMP_F16 && !norm.on) xrow[i] = __ushort_as_half(src[i]);
+                else if (norm.on) xrow[i] = __float2half_rn((x_as_float<DT>(src[i]) * inv) * gamma_at(norm, i) * sc);
                 else xrow[i] = __float2half_rn(x_as_float<DT>(src[i]) * sc);
             }
             __syncthreads();
@@ -790,15 +813,15 @@ bool gemm_supported(const DevModel& m) {
 
 template <sfmp_dtype DT>
 void launch_xprep_rows(const void* x, const DevModel& m, uint8_t* xs, float* ysc, const GemmParams& p, int cols, int Mpad,
-                       int grid, size_t smem, cudaStream_t st) {
+                       int grid, size_t smem, cudaStream_t st, const PreNorm& norm) {
     static std::once_flag fl[64];
     once_per_device(fl, [] { cudaFuncSetAttribute(xprep_gemm_rows_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
     note_launch();
-    xprep_gemm_rows_kernel<DT><<<grid, 512, smem, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad);
+    xprep_gemm_rows_kernel<DT><<<grid, 512, smem, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad, norm);
 }
 template <sfmp_dtype DT>
 void launch_xprep_tok(const void* x, const DevModel& m, uint8_t* xs, float* ysc, const GemmParams& p, int cols, int Mpad,
-                      cudaStream_t st) {
+                      cudaStream_t st, const PreNorm& norm) {
     static std::once_flag fl[64];
     once_per_device(fl, [] {
         cudaFuncSetAttribute(xprep_gemm_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -807,7 +830,8 @@ void launch_xprep_tok(const void* x, const DevModel& m, uint8_t* xs, float* ysc,
     note_launch();
     // 512 threads: the per-token absmax, convert and gather loops need the
     // whole CTA (128 threads per 28672-column row ran at ~150 GB/s)
-    xprep_gemm_kernel<DT><<<Mpad, 512, static_cast<size_t>(cols) * 2, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad);
+    xprep_gemm_kernel<DT><<<Mpad, 512, static_cast<size_t>(cols) * 2, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad,
+                                                                           norm);
 }
 
 // Workspace: swizzled X images | per-token scales | split-K partial tiles [items][N][128] f32.
@@ -830,7 +854,8 @@ size_t gemm_workspace_bytes(const DevModel& m, int64_t M) {
 }
 
 cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y, void* ws,
-                        cudaStream_t st) {
+                        cudaStream_t st, const PreNorm* norm_in) {
+    const PreNorm norm = norm_in ? *norm_in : PreNorm{};
     GemmParams p{};
     p.N = tile_n(M);
     p.M = static_cast<int>(M);
@@ -879,15 +904,15 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
         const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / rsm)));
         const int rgrid = static_cast<int>(std::min<int64_t>(Mpad, static_cast<int64_t>(per_sm) * m.num_sms));
         switch (dt) {
-            case SFMP_F32: launch_xprep_rows<SFMP_F32>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st); break;
-            case SFMP_F16: launch_xprep_rows<SFMP_F16>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st); break;
-            default: launch_xprep_rows<SFMP_BF16>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st); break;
+            case SFMP_F32: launch_xprep_rows<SFMP_F32>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st, norm); break;
+            case SFMP_F16: launch_xprep_rows<SFMP_F16>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st, norm); break;
+            default: launch_xprep_rows<SFMP_BF16>(x, m, xs, ysc, p, cols, Mpad, rgrid, rsm, st, norm); break;
         }
     } else {
         switch (dt) {
-            case SFMP_F32: launch_xprep_tok<SFMP_F32>(x, m, xs, ysc, p, cols, Mpad, st); break;
-            case SFMP_F16: launch_xprep_tok<SFMP_F16>(x, m, xs, ysc, p, cols, Mpad, st); break;
-            default: launch_xprep_tok<SFMP_BF16>(x, m, xs, ysc, p, cols, Mpad, st); break;
+            case SFMP_F32: launch_xprep_tok<SFMP_F32>(x, m, xs, ysc, p, cols, Mpad, st, norm); break;
+            case SFMP_F16: launch_xprep_tok<SFMP_F16>(x, m, xs, ysc, p, cols, Mpad, st, norm); break;
+            default: launch_xprep_tok<SFMP_BF16>(x, m, xs, ysc, p, cols, Mpad, st, norm); break;
         }
     }
     e0 = cudaGetLastError();

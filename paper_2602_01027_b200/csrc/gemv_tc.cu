@@ -50,6 +50,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "prenorm.cuh"
 #include "ptx.cuh"
 #include "repack.cuh"
 #include "unpack.cuh"
@@ -157,6 +158,7 @@ struct XLin {
     int lo, nl;     // floor bit-width, number of layout sections (1 or 2)
     int M;          // tokens of this linear
     uint32_t sec_bytes;
+    PreNorm norm;   // fused RMSNorm of the token rows (on = 0: x as given)
 };
 struct XParams {
     XLin lin[kMaxLin];
@@ -326,7 +328,18 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
         }
     }
     __syncthreads();
-    const int e = token_exponent(row_absmax(xr, cols, [](T v) { return XT<DT>::f(v); }, red));
+    // fused RMSNorm (prenorm.cuh): x = h * inv_rms * gamma, folded into the scale
+    float inv = 1.f;
+    int e;
+    if (XL.norm.on) {
+        __shared__ float nred[32];
+        inv = row_inv_rms([&](int i) { return XT<DT>::f(xr[i]); }, cols, XL.norm.eps, nred);
+        float m = 0.f;
+        for (int i = threadIdx.x; i < cols; i += 256) m = fmaxf(m, fabsf(XT<DT>::f(xr[i]) * gamma_at(XL.norm, i)));
+        e = token_exponent(block_reduce<true>(m, nred) * inv);
+    } else {
+        e = token_exponent(row_absmax(xr, cols, [](T v) { return XT<DT>::f(v); }, red));
+    }
     const float2 sc = pow2_pair(-e);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp >= nbc) return;
@@ -342,8 +355,12 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int e2 = 0; e2 < 2; ++e2)
-                v[j * 2 + e2] = XT<DT>::f(xr[cpw[c * 128 + kb + 4 * j + 16 * e2]]) * sc.x * sc.y;
+            for (int e2 = 0; e2 < 2; ++e2) {
+                const uint32_t col = cpw[c * 128 + kb + 4 * j + 16 * e2];
+                float h = XT<DT>::f(xr[col]);
+                if (XL.norm.on) h = (h * inv) * gamma_at(XL.norm, col);
+                v[j * 2 + e2] = h * sc.x * sc.y;
+            }
         write_fragments<X2>(rec0, lstride, G, c, t, q, s8, v, XL.lo, XL.nl);
         xs += (v[0] + v[1]) + (v[2] + v[3]);
     }
@@ -886,6 +903,9 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
     for (int i = 0; i < xp.nlin; ++i) maxM = std::max(maxM, xp.lin[i].M);
     const int NT = maxM > 8 ? 2 : 1;
     const size_t row_smem = static_cast<size_t>(8) * p.n_b * 4 + static_cast<size_t>(max_cols) * elem;
+    bool any_norm = false;  // the wide-row fallback does not fuse the norm
+    for (int i = 0; i < xp.nlin; ++i) any_norm = any_norm || xp.lin[i].norm.on;
+    if (any_norm && row_smem > static_cast<size_t>(kXprepRowLimit)) return cudaErrorNotSupported;
     if (row_smem <= static_cast<size_t>(kXprepRowLimit)) {
         static std::once_flag fl[64];
         once_per_device(fl, [] {
@@ -1011,7 +1031,8 @@ bool gemv_groupable(const DevModel& a, const DevModel& b) {
 }
 
 cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, float* const* ys, uint8_t* const* wss,
-                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st, bool overlap_prev) {
+                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st, bool overlap_prev,
+                              const PreNorm* norms) {
     if (n < 1 || n > kMaxLin) return cudaErrorInvalidValue;
     const DevModel& m0 = *ms[0];
     int M = 0;
@@ -1073,6 +1094,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         X.nl = nl;
         X.M = Ms[i];
         X.sec_bytes = L.sec_bytes;
+        if (norms) X.norm = norms[i];
         xwarps += BC * NT;
         xitems += (BC + 7) / 8 * Ms[i];  // pre-pass CTAs: (8 block columns) x tokens
         max_cols = std::max(max_cols, X.cols);
@@ -1097,13 +1119,13 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
 }
 
 cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, float* y, float* ws,
-                        cudaStream_t st) {
+                        cudaStream_t st, const PreNorm* norm) {
     const DevModel* ms[1] = {&m};
     const void* xs[1] = {x};
     float* ys[1] = {y};
     uint8_t* wss[1] = {reinterpret_cast<uint8_t*>(ws)};
     const int Ms[1] = {M};
-    return launch_gemv_group(ms, xs, ys, wss, Ms, 1, dt, st, false);
+    return launch_gemv_group(ms, xs, ys, wss, Ms, 1, dt, st, false, norm);
 }
 
 }  // namespace sfmpk

@@ -98,14 +98,23 @@ struct DevModel {
     UnitGeom geom() const { return UnitGeom{d_payload, d_unit_desc, TR, n_b, BC, gemv_ok}; }
 };
 
+// RMSNorm fused into the activation pre-pass (prenorm.cuh); on = 0: identity.
+struct PreNorm {
+    const void* gamma = nullptr;  // [cols] norm weight (nullptr: 1)
+    int gdt = 0;                  // its sfmp_dtype
+    float eps = 0.f;
+    int on = 0;
+};
+
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_gemv(const DevModel& m, const void* x, sfmp_dtype dt, int M, float* y,
-                        float* ws, cudaStream_t st);
+                        float* ws, cudaStream_t st, const PreNorm* norm = nullptr);
 size_t gemv_workspace_bytes(const DevModel& m, int M);
 // Several independent linears in one xprep + one GEMV launch (same n_b, floor bits, device).
 bool gemv_groupable(const DevModel& a, const DevModel& b);
 cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, float* const* ys, uint8_t* const* wss,
-                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st, bool overlap_prev);
+                              const int* Ms, int n, sfmp_dtype dt, cudaStream_t st, bool overlap_prev,
+                              const PreNorm* norms = nullptr);
 int gemv_ctas_per_sm(int NT);
 // Two pipeline stages of the widest unit + activation record fit in shared memory.
 bool gemv_feasible(const DevModel& m);
@@ -126,6 +135,6 @@ bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const s
                        std::vector<uint8_t>& wl, std::vector<uint64_t>& woff);
 size_t gemm_workspace_bytes(const DevModel& m, int64_t M);
 cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
-                        void* ws, cudaStream_t st);
+                        void* ws, cudaStream_t st, const PreNorm* norm = nullptr);
 
 }  // namespace sfmpk
