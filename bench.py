@@ -390,6 +390,29 @@ def single_linear_points(sfmp, port, dev, stream, hbm, tc, args):
                 out["config0"]["cpu_reference_error"] = str(e)[:100]
         del ms
     out["reorder_overhead_pct"] = round(100.0 * (out["config0"]["us"] / out["mode_none"]["us"] - 1.0), 2)
+    # the paper's kernel comparison: ours vs the
+    # paper-faithful LUT GEMV on the GPU (K6) vs dense bf16 cuBLAS, M=1
+    cmp = {}
+    for name, (r, c, b) in (("4096x4096_b3.5", (4096, 4096, 3.5)), ("8192x28672_b3.0", (8192, 28672, 3.0))):
+        data = model_bytes(port, r, c, b)
+        ncp = max(2, int(400e6 // (r * c * b / 8)) + 1)
+        ms = [sfmp.DeviceModel(data, device=dev.index, flags=sfmp.MODEL_LUT_LAYOUT) for _ in range(min(ncp, 8))]
+        x32 = torch.from_numpy(port.gen_activation(1, c, 3100)).to(dev)
+        xb = x32.to(torch.bfloat16)
+        y = torch.empty(1, r, device=dev)
+        ws = ws_for(sfmp, ms[0], 16)
+        ours = graph_us(lambda: [m.gemm(xb, out=y, workspace=ws, stream=stream) for m in ms], stream, 10, len(ms))
+        lut = graph_us(lambda: [m.gemm(x32, out=y, path=sfmp.PATH_LUT, stream=stream) for m in ms], stream, 3,
+                       len(ms))
+        Wd = [torch.randn(r, c, device=dev, dtype=torch.bfloat16) for _ in range(max(2, int(400e6 // (2 * r * c)) + 1))]
+        yd = torch.empty(1, r, device=dev, dtype=torch.bfloat16)
+        dense = graph_us(lambda: [torch.matmul(xb, w.t(), out=yd) for w in Wd], stream, 10, len(Wd))
+        byts = algo_bytes(ms[0].info, 1, r, c)
+        cmp[name] = {"ours_us": round(ours, 2), "lut_gpu_us": round(lut, 2), "dense_bf16_cublas_us": round(dense, 2),
+                     "ours_frac_hbm": round(byts / ours / 1e3 / hbm, 4)}
+        del ms, Wd
+        torch.cuda.empty_cache()
+    out["kernel_comparison_M1"] = cmp
     torch.cuda.empty_cache()
     return out
 

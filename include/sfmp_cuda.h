@@ -72,7 +72,9 @@ typedef enum sfmp_path {
     SFMP_PATH_AUTO = 0,
     SFMP_PATH_GEMV = 1,     /* K1: decode GEMV, M <= 16, HBM-bound            */
     SFMP_PATH_GEMM = 2,     /* K2: tcgen05/TMEM prefill GEMM                   */
-    SFMP_PATH_GENERIC = 3   /* any m_b/n_b/M; simple CUDA-core kernel          */
+    SFMP_PATH_GENERIC = 3,  /* any m_b/n_b/M; simple CUDA-core kernel          */
+    SFMP_PATH_LUT = 4       /* the paper's LUT GEMV (lutgemm.cpp:11-71) on the GPU: a comparison
+                               line, f32 x only, needs SFMP_MODEL_LUT_LAYOUT   */
 } sfmp_path;
 
 /* Opaque device-resident model (owns payload, offsets, perms, bit map). */
@@ -156,6 +158,8 @@ sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device
  * SFMPPKD1 payload).  SFMP_MODEL_DECODE_ONLY keeps only the decode layout
  * (~1.0x): M > 16 then runs the decode GEMV in 16-token chunks. */
 #define SFMP_MODEL_DECODE_ONLY 1u
+/* Also keep the SFMPPKD1 block payloads as stored, for SFMP_PATH_LUT. */
+#define SFMP_MODEL_LUT_LAYOUT 2u
 sfmp_status sfmp_model_create_ex(const uint8_t* bytes, size_t len, int device, uint32_t flags,
                                  sfmp_dev_model** out);
 sfmp_status sfmp_model_create_shard_ex(const uint8_t* bytes, size_t len, int device, uint32_t shard,

@@ -32,7 +32,7 @@ LIB_PATH = os.environ.get("SFMP_LIB") or os.path.join(HERE, "libsfmp_b200.so")
 OK, E_SHAPE, E_CONFIG, E_MAGIC, E_VERSION, E_TRUNC, E_INVARIANT, E_IO, E_CUDA, E_NCCL, E_ARG, \
     E_NOMEM, E_UNSUPPORTED = range(13)
 F32, F16, BF16 = 0, 1, 2
-PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_GENERIC = 0, 1, 2, 3
+PATH_AUTO, PATH_GEMV, PATH_GEMM, PATH_GENERIC, PATH_LUT = 0, 1, 2, 3, 4
 
 EXPORTED_SYMBOLS = (
     "sfmp_abi_version", "sfmp_status_string", "sfmp_last_error", "sfmp_device_count",
@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "sfmp_gemm_norm", "sfmp_gemm_grouped_v_norm",
 )
 MODEL_DECODE_ONLY = 1
+MODEL_LUT_LAYOUT = 2
 NCCL_ID_BYTES = 128
 
 

@@ -280,6 +280,25 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
     if ((s = dev_upload(*d, &d->d_col_perm, cp.data(), cp.size() * 4))) return s;
     if ((s = dev_upload(*d, &d->d_out_map, out_map.data(), out_map.size() * 4))) return s;
     if ((s = build_gemv_schedule(*d))) return s;
+    if ((flags & SFMP_MODEL_LUT_LAYOUT) && p.m_b % 32 == 0 && p.m_b <= 1024 && p.n_b % 128 == 0) {
+        // K6 comparison layout: the block payloads as stored, 16-byte aligned
+        std::vector<uint8_t> lp;
+        std::vector<uint64_t> lo;
+        std::vector<uint8_t> lb;
+        const uint64_t BCn = p.cols / p.n_b;
+        for (uint64_t br : brows)
+            for (uint64_t bc = 0; bc < BCn; ++bc) {
+                const uint64_t k = br * BCn + bc;
+                const uint64_t n = (k + 1 < p.K ? p.off[k + 1] : p.payload_end) - p.off[k];
+                lo.push_back(lp.size());
+                lb.push_back(p.bits[k]);
+                lp.insert(lp.end(), bytes + p.off[k], bytes + p.off[k] + n);
+                lp.resize((lp.size() + 15) / 16 * 16, 0);
+            }
+        if ((s = dev_upload(*d, &d->d_lut, lp.data(), lp.size()))) return s;
+        if ((s = dev_upload(*d, &d->d_lut_off, lo.data(), lo.size() * 8))) return s;
+        if ((s = dev_upload(*d, &d->d_lut_bits, lb.data(), lb.size()))) return s;
+    }
     if (!(flags & SFMP_MODEL_DECODE_ONLY) || !d->gemv_ok) {  // the prefill GEMM's own layout
         std::vector<uint8_t> wl;
         std::vector<uint64_t> woff;
@@ -484,7 +503,8 @@ sfmp_status sfmp_model_create(const uint8_t* bytes, size_t len, int device, sfmp
 
 sfmp_status sfmp_model_create_ex(const uint8_t* bytes, size_t len, int device, uint32_t flags, sfmp_dev_model** out) {
     if (!out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out");
-    if (flags & ~static_cast<uint32_t>(SFMP_MODEL_DECODE_ONLY)) return fail(SFMP_ERR_INVALID_ARGUMENT, "unknown model flags");
+    if (flags & ~static_cast<uint32_t>(SFMP_MODEL_DECODE_ONLY | SFMP_MODEL_LUT_LAYOUT))
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "unknown model flags");
     *out = nullptr;
     Parsed p;
     sfmp_status s = parse(bytes, len, p);
@@ -619,7 +639,8 @@ sfmp_status sfmp_model_create_shard(const uint8_t* bytes, size_t len, int device
 sfmp_status sfmp_model_create_shard_ex(const uint8_t* bytes, size_t len, int device, uint32_t shard,
                                        uint32_t num_shards, uint32_t flags, sfmp_dev_model** out) {
     if (!out) return fail(SFMP_ERR_INVALID_ARGUMENT, "null out");
-    if (flags & ~static_cast<uint32_t>(SFMP_MODEL_DECODE_ONLY)) return fail(SFMP_ERR_INVALID_ARGUMENT, "unknown model flags");
+    if (flags & ~static_cast<uint32_t>(SFMP_MODEL_DECODE_ONLY | SFMP_MODEL_LUT_LAYOUT))
+        return fail(SFMP_ERR_INVALID_ARGUMENT, "unknown model flags");
     *out = nullptr;
     if (num_shards < 1 || shard >= num_shards) return fail(SFMP_ERR_CONFIG, "bad shard index/count");
     Parsed p;
@@ -758,6 +779,13 @@ sfmp_status gemm_impl(const sfmp_dev_model* model, const void* x, sfmp_dtype dty
             e = sfmpk::launch_gemm(d, x, dtype, M, y, workspace, st, norm);
             break;
         }
+        case SFMP_PATH_LUT:
+            if (!sfmpk::lut_supported(d))
+                return fail(SFMP_ERR_UNSUPPORTED, "LUT path needs SFMP_MODEL_LUT_LAYOUT, m_b % 32 == 0 (<= 1024), n_b % 128 == 0");
+            if (dtype != SFMP_F32 || (norm && norm->on))
+                return fail(SFMP_ERR_UNSUPPORTED, "the LUT comparison path takes f32 x without a fused norm");
+            e = sfmpk::launch_lut(d, static_cast<const float*>(x), M, y, st);
+            break;
         case SFMP_PATH_GENERIC:
             if (norm && norm->on) return fail(SFMP_ERR_UNSUPPORTED, "fused RMSNorm needs the GEMV or GEMM path");
             e = sfmpk::launch_generic(d, x, dtype, M, y, st);

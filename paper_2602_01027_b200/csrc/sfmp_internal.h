@@ -84,6 +84,12 @@ struct DevModel {
     uint64_t gl_bytes = 0;
     uint32_t* d_xslot = nullptr;  // [cols] col_perm in the K order of the GEMM B operand
 
+    // K6 LUT comparison kernel (lut.cu): the SFMPPKD1 block payloads as stored,
+    // each block 16-byte aligned; built only with SFMP_MODEL_LUT_LAYOUT
+    uint8_t* d_lut = nullptr;
+    uint64_t* d_lut_off = nullptr;
+    uint8_t* d_lut_bits = nullptr;
+
     bool gemv_ok = false;
     bool gemm_ok = false;
 
@@ -122,6 +128,8 @@ bool gemv_feasible(const DevModel& m);
 cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
                            cudaStream_t st);
 cudaError_t launch_dequant(const DevModel& m, float* w, cudaStream_t st);
+bool lut_supported(const DevModel& m);
+cudaError_t launch_lut(const DevModel& m, const float* x, int64_t M, float* y, cudaStream_t st);
 cudaError_t launch_gemv_block(const DevModel& m, uint64_t block, const float* xr, float* out, cudaStream_t st);
 cudaError_t launch_unpack(const DevModel& m, uint8_t* codes, cudaStream_t st);
 cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, int64_t M,
