@@ -104,7 +104,11 @@ constexpr int kSmemSM = 225 * 1024;
 #define SFMP_CTAS2 3
 #endif
 constexpr int kCtasNT1 = SFMP_CTAS1, kCtasNT2 = SFMP_CTAS2;  // resident CTAs per SM (M <= 8 / 9..16)
-__host__ __device__ constexpr int ctas_per_sm(int NT) { return NT == 1 ? kCtasNT1 : kCtasNT2; }
+// M <= 16 with floor bits <= 3 and 16-bit x fits 96 registers without spills,
+// so 4 CTAs per SM (measured: M=16 launch 47.6 -> 46.0 us); wider or f32 variants keep 3.
+__host__ __device__ constexpr int ctas_per_sm(int NT, int LO = 8, bool X2 = true) {
+    return NT == 1 ? kCtasNT1 : (LO <= 3 && !X2 ? kCtasNT2 + 1 : kCtasNT2);
+}
 
 // One linear of a (possibly grouped) launch.
 constexpr int kMaxLin = 40;
@@ -594,7 +598,7 @@ struct PendCopy {
 // (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
 // two unpack paths and its hot loop stays resident in the instruction cache.
 template <int NT, int CH, int LO, bool X2>
-__global__ void __launch_bounds__(kThreads, ctas_per_sm(NT)) gemv_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel(const Params p) {
     constexpr int SU = CH == 1 ? SFMP_SU : 1;
     constexpr int nb8 = CH * 16;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -989,8 +993,8 @@ struct SmemPlan {
     int stages, ctas;
     size_t smem;
 };
-SmemPlan smem_plan(uint32_t stage_w, uint32_t rec_slot, int NT) {
-    for (int ctas = ctas_per_sm(NT); ctas >= 1; --ctas) {
+SmemPlan smem_plan(uint32_t stage_w, uint32_t rec_slot, int NT, int LO = 8, bool X2 = true) {
+    for (int ctas = ctas_per_sm(NT, LO, X2); ctas >= 1; --ctas) {
         const int budget = (ctas == 1 ? 227 * 1024 : kSmemSM / ctas) - kHdrBytes;
         const int stages = std::min<int>(SFMP_MAX_STAGES, budget / static_cast<int>(stage_w + rec_slot));
         if (stages >= 2) return {stages, ctas, kHdrBytes + static_cast<size_t>(stages) * (stage_w + rec_slot)};
@@ -1107,7 +1111,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     p.item_start[n] = items;
     p.fix_start[n] = fix;
     p.stage_w = stage_bytes(m0, ceil_bits);
-    const SmemPlan sp = smem_plan(p.stage_w, units_per_stage(m0) * p.sec_bytes, NT);
+    const SmemPlan sp = smem_plan(p.stage_w, units_per_stage(m0) * p.sec_bytes, NT, m0.floor_bits, X2);
     if (sp.stages < 2) return cudaErrorInvalidConfiguration;  // excluded at upload (gemv_feasible)
     p.stages = sp.stages;
     const int grid = std::min(items, m0.num_sms * sp.ctas);
