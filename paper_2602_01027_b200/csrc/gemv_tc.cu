@@ -68,6 +68,9 @@ constexpr int kThreads = 32 * (1 + kNCW);  // producer | compute warps
 #define SFMP_SEG_COLS 1024
 #endif
 constexpr int kSegCols = SFMP_SEG_COLS;  // canonical K segment (columns)
+// the decode pre-pass scales x per (token, 8 block columns); a segment must
+// never straddle two such groups (n_b in {128, 256})
+static_assert(kSegCols == 1024 || kSegCols == 512 || kSegCols == 256, "segment inside one pre-pass scale group");
 constexpr int kHdrBytes = 1024;   // barriers | stage info | pending record copies
 constexpr int kSmemSM = 225 * 1024;
 #ifndef SFMP_MAX_STAGES
@@ -84,6 +87,9 @@ constexpr int kSmemSM = 225 * 1024;
 #endif
 #ifndef SFMP_EXP_NOMMA
 #define SFMP_EXP_NOMMA 0
+#endif
+#ifndef SFMP_EXP_EMPTY
+#define SFMP_EXP_EMPTY 0
 #endif
 #ifndef SFMP_EXP_NOLOAD
 #define SFMP_EXP_NOLOAD 0
@@ -156,8 +162,7 @@ struct XLin {
     const void* x;
     const uint32_t* col_perm;
     uint8_t* xrec;
-    float* escale;  // per-token exponents from rowscale_kernel (wide-row pre-pass)
-    int BC, cols, warp0;
+    int BC, cols;
     int item0;      // first pre-pass CTA of this linear (one per token x 8 block columns)
     int lo, nl;     // floor bit-width, number of layout sections (1 or 2)
     int M;          // tokens of this linear
@@ -215,7 +220,7 @@ struct XT<SFMP_BF16> {
     using T = __nv_bfloat16;
     static __device__ __forceinline__ float f(__nv_bfloat16 v) { return __bfloat162float(v); }
 };
-constexpr int kXprepRowLimit = 192 * 1024;  // staged x row bytes (larger rows: xprep_kernel)
+constexpr int kXprepRowLimit = 192 * 1024;  // staged x row bytes of the fused-norm pre-pass
 
 // Per-token power-of-two scale: e such that max|x| * 2^-e lies in
 // [2^-10, 2^-9), so the largest record value (slot factor 2^24) lies in
@@ -378,99 +383,82 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
     if (xp.wait_prev) pdl_wait();
 }
 
-// Per-token exponents for the wide-row pre-pass: one CTA per (token, linear).
+// K4 (decode flavour, default): one CTA per (token t, 8 block columns of one
+// linear).  The 8 block columns' col_perm slices are staged in shared memory
+// (coalesced), then warp w gathers its block column's activations for token
+// t straight from x (x[t][col_perm[.]], reorder.cpp:103-111), lane (s, q)
+// owning the 4 k-slots 32q + 8(s&1) + 4j + 16e + (s>>1) of each 128-column
+// chunk.  The output scale 2^e is per (token, 8 block columns): max|x| of
+// the CTA's 1024 (or 2048) values -> [2^-10, 2^-9), written into each of its
+// records' tails and applied by the GEMV per unit (exact powers of two), so no
+// CTA reads the whole row.  Column sums X_g (lutgemm.cpp:113-115) use the
+// scaled values.
 template <sfmp_dtype DT>
-__global__ void __launch_bounds__(256) rowscale_kernel(const XParams xp) {
-    __shared__ float red[8];
-    const XLin& XL = xp.lin[blockIdx.y];
-    const int t = blockIdx.x;
-    if (t >= XL.M) return;
+__global__ void __launch_bounds__(256) xprep_gather_kernel(const XParams xp) {
     using T = typename XT<DT>::T;
-    const T* xrow = static_cast<const T*>(XL.x) + static_cast<size_t>(t) * XL.cols;
-    const float m = row_absmax(xrow, XL.cols, [](T v) { return XT<DT>::f(v); }, red);
-    if (threadIdx.x == 0) XL.escale[t] = static_cast<float>(token_exponent(m));
-}
-
-// Fallback for x rows above kXprepRowLimit bytes: one item per (block column,
-// n-tile); its CH 128-column chunks go to CH warps of one CTA, whose column
-// sums are combined in chunk order through shared memory.  Lane (n,q) owns
-// token nt*8+n and k-slots 32q + 4h + a (+16).
-template <sfmp_dtype DT>
-__global__ void __launch_bounds__(256) xprep_kernel(const XParams xp) {
     constexpr bool X2 = DT == SFMP_F32;
-    pdl_launch_dependents();
-    __shared__ float red[8][8];
-    const int n_b = xp.n_b;
-    const int NT = RecGeom{xp.M, X2}.nt_count();
-    const int CH = n_b >> 7;  // 1..2
-    const int warp = threadIdx.x >> 5, c = warp % CH;
-    int w = blockIdx.x * (8 / CH) + warp / CH;  // item
-    int li = 0;
-    while (li + 1 < xp.nlin && w >= xp.lin[li + 1].warp0) ++li;
+    pdl_launch_dependents();  // let the GEMV start streaming weights right away
+    __shared__ __align__(16) uint32_t cp[8 * 256];  // [nbc][n_b] column indices
+    __shared__ float red[8];
+    const int n_b = xp.n_b, CH = n_b >> 7;
+    int it = blockIdx.x, li = 0;  // compact grid: (linear, token, 8 block columns)
+    while (li + 1 < xp.nlin && it >= xp.lin[li + 1].item0) ++li;
     const XLin& XL = xp.lin[li];
-    w -= XL.warp0;
     const int M = XL.M;
-    const RecGeom G{M, X2};
-    const int BC = XL.BC, cols = XL.cols;
-    const bool item_ok = w < BC * NT;
-    const int bc = w / NT, nt = w - bc * NT;
-    const int lane = threadIdx.x & 31, q = lane & 3, n = lane >> 2;
-    const int t = nt * 8 + n;
-    const bool live = item_ok && t < M;
-    const size_t lstride = static_cast<size_t>(BC) * XL.sec_bytes;
-    uint8_t* rec0 = XL.xrec + static_cast<size_t>(bc) * XL.sec_bytes;
-    const int e = live ? static_cast<int>(XL.escale[t]) : 0;
-    const float2 sc = pow2_pair(-e);
-    float xs = 0.f;
-    if (item_ok) {
-        const uint4 idx4 = ldg_keep_v4(reinterpret_cast<const uint4*>(XL.col_perm + bc * n_b + c * 128) + lane,
-                                       policy_evict_last());
-        uint32_t gi[32];
+    it -= XL.item0;
+    const int nit = (XL.BC + 7) / 8;
+    const int t = it / nit;
+    it -= t * nit;
+    const int bc0 = it * 8, nbc = min(8, XL.BC - bc0);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(XL.col_perm + static_cast<size_t>(bc0) * n_b);
+        const uint64_t keep = policy_evict_last();
+        for (int i = threadIdx.x; i < nbc * n_b / 4; i += 256) reinterpret_cast<uint4*>(cp)[i] = ldg_keep_v4(src + i, keep);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s8 = lane >> 2, q = lane & 3;
+    const int kb = 32 * q + 8 * (s8 & 1) + (s8 >> 1);
+    const T* xrow = static_cast<const T*>(XL.x) + static_cast<size_t>(t) * XL.cols;
+    const uint32_t* cpw = cp + warp * n_b;
+    float v[2][4];
+    float m = 0.f;
 #pragma unroll
-        for (int s8 = 0; s8 < 8; ++s8) {
-            const int a = s8 >> 1;
-            const uint32_t comp = a == 0 ? idx4.x : a == 1 ? idx4.y : a == 2 ? idx4.z : idx4.w;
+    for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int e2 = 0; e2 < 2; ++e2) {
-                    const int wk = 4 * (2 * (s8 & 1) + j) + a + 16 * e2;
-                    gi[s8 * 4 + j * 2 + e2] = __shfl_sync(0xffffffffu, comp, 8 * q + (wk >> 2));
-                }
-        }
-        if (live) {
-            using T = typename XT<DT>::T;
-            const T* xrow = static_cast<const T*>(XL.x) + static_cast<size_t>(t) * cols;
-#pragma unroll
-            for (int s8 = 0; s8 < 8; ++s8) {
-                float v[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) v[k] = XT<DT>::f(xrow[gi[s8 * 4 + k]]) * sc.x * sc.y;
-                write_fragments<X2>(rec0, lstride, G, c, t, q, s8, v, XL.lo, XL.nl);
-                xs += (v[0] + v[1]) + (v[2] + v[3]);
+        for (int j = 0; j < 4; ++j) {
+            v[c][j] = 0.f;
+            if (warp < nbc && c < CH) {
+                v[c][j] = XT<DT>::f(xrow[cpw[c * 128 + kb + 4 * (j >> 1) + 16 * (j & 1)]]);
+                m = fmaxf(m, fabsf(v[c][j]));
             }
         }
-        xs += __shfl_xor_sync(0xffffffffu, xs, 1);
-        xs += __shfl_xor_sync(0xffffffffu, xs, 2);
-    }
-    if (CH > 1) {
-        if (q == 0) red[warp][n] = xs;
-        __syncthreads();
-        if (c != 0) return;
-        if (q == 0) {
-            xs = 0.f;
-            for (int k = 0; k < CH; ++k) xs += red[warp + k][n];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    m = 0.f;
+    for (int w = 0; w < 8; ++w) m = fmaxf(m, red[w]);
+    if (warp < nbc) {
+        const int e = token_exponent(m);
+        const float2 sc = pow2_pair(-e);
+        const int bc = bc0 + warp;
+        const RecGeom G{M, X2};
+        const size_t lstride = static_cast<size_t>(XL.BC) * XL.sec_bytes;
+        uint8_t* rec0 = XL.xrec + static_cast<size_t>(bc) * XL.sec_bytes;
+        float xs = 0.f;
+        for (int c = 0; c < CH; ++c) {
+            float u[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) u[j] = v[c][j] * sc.x * sc.y;
+            write_fragments<X2>(rec0, lstride, G, c, t, q, s8, u, XL.lo, XL.nl);
+            xs += (u[0] + u[1]) + (u[2] + u[3]);
         }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        if (lane == 0) write_tail(rec0, lstride, G, CH, t, M, xs, e, XL.nl);
     }
-    if (item_ok && q == 0) {
-        const float2 ys = pow2_pair(e);
-        for (int l = 0; l < XL.nl; ++l) {
-            float* xg = reinterpret_cast<float*>(rec0 + l * lstride + G.xg_off(CH));
-            xg[t] = live ? xs : 0.f;
-            xg[kYsIdx + t] = live ? ys.x : 0.f;
-            xg[kYsIdx + 16 + t] = live ? ys.y : 0.f;
-        }
-    }
+    if (xp.wait_prev) pdl_wait();  // see xprep_rows_kernel
 }
 
 // Decode layout of a unit (upload time, sfmp_internal.h "lane-major"): a
@@ -612,6 +600,10 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
     uint8_t* xbase = wbase + static_cast<size_t>(S) * p.stage_w;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (SFMP_EXP_EMPTY) {  // experiment builds only: the launch's fixed costs without the GEMV
+        pdl_launch_dependents();
+        return;
+    }
     // a programmatic dependent (the fix-up of this launch, or the next launch
     // of the same grouped call, whose problems are independent of ours) may
     // start now: it waits for this grid's completion before it reads our data
@@ -757,7 +749,8 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
 #pragma unroll
                         for (int e = 0; e < 4; ++e) yacc[m][nt][e] = 0.f;
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {  // output scale of tokens nt*8+2q, +1
+                for (int nt = 0; nt < NT; ++nt) {  // the segment's output scale of tokens nt*8+2q, +1
+                    // (one scale per (token, 8 block columns) -- a segment never straddles two)
                     const float2 a = *reinterpret_cast<const float2*>(xs + xg_off + 4 * kYsIdx + 32 * nt + 8 * q);
                     const float2 b = *reinterpret_cast<const float2*>(xs + xg_off + 4 * (kYsIdx + 16) + 32 * nt + 8 * q);
                     ysa[nt][0] = a.x;
@@ -789,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
             if (++s == S) { s = 0; ph ^= 1; }
             if (!(fl & kLast)) continue;
 
-            // ---- end of a segment: scale back by 2^e_t (exact), store y or the partial ----
+            // ---- end of a segment: scale back by 2^e (exact), store y or the partial ----
             const Lin& L = p.lin[li];
             const int rt = static_cast<int>(info.y), seg = static_cast<int>(info.z);
             const bool whole = L.P == 1;
@@ -802,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
                     for (int e = 0; e < 4; ++e) {
                         const int t = nt * 8 + 2 * q + (e & 1);
                         if (t >= L.M) continue;
-                        const float v = (yacc[m][nt][e] * ysa[nt][e & 1]) * ysb[nt][e & 1];
+                        const float v = (yacc[m][nt][e] * ysa[nt][e & 1]) * ysb[nt][e & 1];  // exact
                         const int row = r0 + 16 * m + 8 * (e >> 1);
                         if (whole) dst[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = v;  // un-permuted
                         else dst[t * kTR + row] = v;  // [t][128 rows], coalesced
@@ -896,7 +889,7 @@ cudaError_t launch_nc(cudaLaunchConfig_t& cfg, const Params& p, int lo) {
 }
 
 template <sfmp_dtype DT>
-cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems, int max_cols, int grid, size_t smem,
+cudaError_t launch_t(const Params& p, const XParams& xp, int xitems, int max_cols, int grid, size_t smem,
                      int lo, cudaStream_t st, bool overlap_prev) {
     constexpr bool X2 = DT == SFMP_F32;
     const size_t elem = DT == SFMP_F32 ? 4 : 2;
@@ -907,10 +900,30 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
     for (int i = 0; i < xp.nlin; ++i) maxM = std::max(maxM, xp.lin[i].M);
     const int NT = maxM > 8 ? 2 : 1;
     const size_t row_smem = static_cast<size_t>(8) * p.n_b * 4 + static_cast<size_t>(max_cols) * elem;
-    bool any_norm = false;  // the wide-row fallback does not fuse the norm
+    bool any_norm = false;
     for (int i = 0; i < xp.nlin; ++i) any_norm = any_norm || xp.lin[i].norm.on;
-    if (any_norm && row_smem > static_cast<size_t>(kXprepRowLimit)) return cudaErrorNotSupported;
-    if (row_smem <= static_cast<size_t>(kXprepRowLimit)) {
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    // overlap_prev: a later launch of one grouped call (independent problems,
+    // workspaces disjoint from the earlier launches'): the pre-pass may start
+    // while the previous GEMV still runs, and this call's GEMV then fills the
+    // previous one's tail.
+    a[0].val.programmaticStreamSerializationAllowed = overlap_prev ? 1 : 0;
+    XParams xq = xp;
+    xq.wait_prev = overlap_prev ? 1 : 0;
+    cudaLaunchConfig_t c{};
+    c.gridDim = dim3(xitems);
+    c.blockDim = dim3(256);
+    c.stream = st;
+    c.attrs = a;
+    c.numAttrs = 1;
+    if (!any_norm) {
+        note_launch();
+        cudaError_t e = cudaLaunchKernelEx(&c, xprep_gather_kernel<DT>, xq);
+        if (e != cudaSuccess) return e;
+    } else {
+        // the fused RMSNorm needs each token's whole row: the staged pre-pass
+        if (row_smem > static_cast<size_t>(kXprepRowLimit)) return cudaErrorNotSupported;
         static std::once_flag fl[64];
         once_per_device(fl, [] {
             cudaFuncSetAttribute(xprep_rows_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXprepRowLimit);
@@ -919,33 +932,10 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xwarps, int xitems,
             cudaFuncSetAttribute(xprep_rows_kernel<DT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  cudaSharedmemCarveoutMaxShared);
         });
-        // overlap_prev: a later launch of one grouped call (independent problems,
-        // workspaces disjoint from the earlier launches'): the pre-pass may start
-        // while the previous GEMV still runs, and this call's GEMV then fills the
-        // previous one's tail.
-        cudaLaunchAttribute a[1];
-        a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        a[0].val.programmaticStreamSerializationAllowed = overlap_prev ? 1 : 0;
-        XParams xq = xp;
-        xq.wait_prev = overlap_prev ? 1 : 0;
-        cudaLaunchConfig_t c{};
-        c.gridDim = dim3(xitems);
-        c.blockDim = dim3(256);
         c.dynamicSmemBytes = row_smem;
-        c.stream = st;
-        c.attrs = a;
-        c.numAttrs = 1;
         note_launch();
         cudaError_t e = cudaLaunchKernelEx(&c, xprep_rows_kernel<DT>, xq);
         if (e != cudaSuccess) return e;
-    } else {
-        if (DT != SFMP_F16) {
-            note_launch();
-            rowscale_kernel<DT><<<dim3(16, xp.nlin), 256, 0, st>>>(xp);
-        }
-        const int per_cta = 8 / (p.n_b / 128);  // items per pre-pass CTA
-        note_launch();
-        xprep_kernel<DT><<<(xwarps + per_cta - 1) / per_cta, 256, 0, st>>>(xp);
     }
     {
         cudaError_t e = cudaGetLastError();
@@ -1055,7 +1045,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     xp.M = M;
     p.n_b = xp.n_b = static_cast<int>(m0.n_b);
     p.sec_bytes = static_cast<uint32_t>(RecGeom{M, X2}.sec_bytes(CH));  // stage stride: the largest
-    int ceil_bits = 0, items = 0, fix = 0, xwarps = 0, xitems = 0, max_cols = 0;
+    int ceil_bits = 0, items = 0, fix = 0, xitems = 0, max_cols = 0;
     for (int i = 0; i < n; ++i) {
         const DevModel& m = *ms[i];
         ceil_bits = std::max(ceil_bits, m.ceil_bits);
@@ -1084,22 +1074,18 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         items += static_cast<int>(m.RT) * L.P;
         L.fix0 = fix;
         if (L.P > 1) fix += static_cast<int>(m.RT) * Ms[i];  // (tile, token) fix-up pairs
-        uint8_t* tail = wss[i] + gemv_rec_bytes(m) + gemv_part_bytes(m);  // queue[4] | pad | exponents[16] | counters
         XLin& X = xp.lin[i];
         X.x = xs[i];
         X.col_perm = m.d_col_perm;
         X.xrec = wss[i];
-        X.escale = reinterpret_cast<float*>(tail + 64);
         X.BC = BC;
         X.cols = static_cast<int>(m.cols);
-        X.warp0 = xwarps;
         X.item0 = xitems;
         X.lo = m.floor_bits;
         X.nl = nl;
         X.M = Ms[i];
         X.sec_bytes = L.sec_bytes;
         if (norms) X.norm = norms[i];
-        xwarps += BC * NT;
         xitems += (BC + 7) / 8 * Ms[i];  // pre-pass CTAs: (8 block columns) x tokens
         max_cols = std::max(max_cols, X.cols);
     }
@@ -1116,9 +1102,9 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     p.stages = sp.stages;
     const int grid = std::min(items, m0.num_sms * sp.ctas);
     switch (dt) {
-        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xwarps, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
-        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xwarps, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
-        default: return launch_t<SFMP_BF16>(p, xp, xwarps, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
+        case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
+        case SFMP_F16: return launch_t<SFMP_F16>(p, xp, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
+        default: return launch_t<SFMP_BF16>(p, xp, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);
     }
 }
 
