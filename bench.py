@@ -625,9 +625,11 @@ def main():
 
     use_graph = not args.no_graph
     stream = torch.cuda.Stream(device=dev)
-    graphs = []
+    graphs, block = [], None
     if use_graph:
-        # one graph per rotation phase so each replay touches the next weight copies
+        # one graph per rotation phase so each replay touches the next weight copies,
+        # and one graph of COPIES consecutive steps (a serving loop runs steps back to
+        # back; a graph boundary per step adds launch latency between steps)
         with torch.cuda.stream(stream):
             for i in range(COPIES):
                 step(i)
@@ -637,12 +639,27 @@ def main():
             with torch.cuda.graph(g, stream=stream):
                 step(i)
             graphs.append(g)
+        block = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(block, stream=stream):
+            for i in range(COPIES):
+                step(i)
 
     def run_step(i):
         if use_graph:
             graphs[i % COPIES].replay()
         else:
             step(i)
+
+    def run_steps(n):
+        """Exactly n steps (phases 0, 1, ...): whole COPIES-step blocks, then single steps."""
+        i = 0
+        if use_graph:
+            while n - i >= COPIES:
+                block.replay()
+                i += COPIES
+        while i < n:
+            run_step(i)
+            i += 1
 
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
@@ -666,8 +683,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
-        for i in range(args.steps):
-            run_step(i)
+        run_steps(args.steps)
         e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -739,16 +755,18 @@ def main():
         xoff[k], yoff[k] = xo, yo
         xo += k[1] * SHAPES[k[0]][1]
         yo += k[1] * SHAPES[k[0]][0]
-    hxb = torch.empty(xo, dtype=torch.float32).pin_memory()
+    # x travels as bf16 (the activations of this workload are bf16 values; the
+    # API takes bf16 directly), y comes back as the API's f32
+    hxb = torch.empty(xo, dtype=torch.bfloat16).pin_memory()
     hyb = torch.empty(yo, dtype=torch.float32).pin_memory()
     for (p, M) in keys:
         hxb[xoff[(p, M)]:xoff[(p, M)] + M * SHAPES[p][1]] = torch.from_numpy(
             port.gen_activation(M, SHAPES[p][1], 3000 + M)).reshape(-1)
-    dxb = torch.empty(xo, dtype=torch.float32, device=dev)
+    dxb = torch.empty(xo, dtype=torch.bfloat16, device=dev)
     dyb = torch.empty(yo, dtype=torch.float32, device=dev)
     dx = {k: dxb[xoff[k]:xoff[k] + k[1] * SHAPES[k[0]][1]].view(k[1], SHAPES[k[0]][1]) for k in keys}
     dy = {k: dyb[yoff[k]:yoff[k] + k[1] * SHAPES[k[0]][0]].view(k[1], SHAPES[k[0]][0]) for k in keys}
-    h2d, d2h = xo * 4, yo * 4
+    h2d, d2h = xo * 2, yo * 4
     gx = {M: (xoff[(PROJS[0], M)], xoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][1]) for M in MS}
     gy = {M: (yoff[(PROJS[0], M)], yoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][0]) for M in MS}
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -855,9 +873,8 @@ def main():
     step_bytes = sum(algo_bytes(models[0][p].info, M, models[0][p].rows, SHAPES[p][1]) for p, M in keys_all)
     t_us = t_ms * 1e3
     step_ach = step_bytes / (t_us * 1e-6) / 1e9
-    dom = per_launch.get("M<=8")
-    traffic = None
-    for prof in ("r02_ncu_gemv_grouped_8b_Mle8.json", "r01_ncu_gemv_grouped_8b_Mle8.json"):
+    traffic, traffic_src = None, None
+    for prof in ("r02_ncu_gemv_step_8b.json", "r02_ncu_gemv_grouped_8b_Mle8.json"):
         path = os.path.join(ROOT, "profiles", prof)
         if os.path.exists(path):
             try:
@@ -868,23 +885,19 @@ def main():
                 break
             except Exception:
                 traffic = None
-    if dom:
-        roofline = {"bound": "hbm", "achieved": dom["GBps"], "peak": hbm, "unit": "GB/s",
-                    "frac": round(dom["GBps"] / hbm, 4), "traffic": traffic,
-                    "kernel": "the step's M<=8 grouped launch (28 problems: x pre-pass + gemv_kernel + fix-up), "
-                              f"{dom['us']} us for {dom['bytes']} algorithmic bytes",
-                    "traffic_note": f"dram read+write of that gemv_kernel launch, profiles/{traffic_src}" if traffic
-                    else None, "per_launch": per_launch,
-                    "step_achieved": round(step_ach, 1), "step_frac": round(step_ach / hbm, 4),
-                    "algorithmic_bytes_per_step": step_bytes, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
-    else:
-        roofline = {"bound": "hbm", "achieved": round(step_ach, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(step_ach / hbm, 4), "traffic": None,
-                    "kernel": "whole step (per-rank bytes / step time)" if sharded else "whole step",
-                    "algorithmic_bytes_per_step": step_bytes, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
-        if kernel_us:
-            roofline.update({"kernel_us": round(kernel_us, 2), "collective_and_unpermute_us": round(t_us - kernel_us, 2),
-                             "kernel_frac": round(step_bytes / (kernel_us * 1e-6) / 1e9 / hbm, 4)})
+    roofline = {"bound": "hbm", "achieved": round(step_ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(step_ach / hbm, 4), "traffic": traffic,
+                "kernel": (f"the step's single grouped launch (35 problems: x pre-pass + gemv_kernel + fix-up, "
+                           f"{launches_per_step} kernels), {round(t_us, 2)} us for {step_bytes} algorithmic bytes")
+                if not sharded else "whole step (per-rank bytes / step time)",
+                "traffic_note": f"ncu dram read+write of that gemv_kernel launch, profiles/{traffic_src}" if traffic
+                else None,
+                "algorithmic_bytes_per_step": step_bytes, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({src})"}
+    if per_launch:
+        roofline["split_by_token_class"] = per_launch  # the same problems as two launches, for reference
+    if kernel_us:
+        roofline.update({"kernel_us": round(kernel_us, 2), "collective_and_unpermute_us": round(t_us - kernel_us, 2),
+                         "kernel_frac": round(step_bytes / (kernel_us * 1e-6) / 1e9 / hbm, 4)})
     out = {
         "metric": METRIC, "value": round(t_us, 2), "unit": "us", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 5),
@@ -892,21 +905,22 @@ def main():
         "dtype": "f16", "data": "synthetic",
         "config": {"workload": WORKLOAD, "avg_code_bits": AVG_BITS, "M": MS, "projections": PROJS,
                    "kernel": "K1 decode GEMV (gemv_kernel) + x pre-pass (xprep_rows_kernel) + fix-up",
-                   "launch_grouping": ("the whole step is one call (sfmp_gemm_grouped_v): one pre-pass + one GEMV "
-                                       "launch for the 28 M<=8 problems, one for the 7 M=16 problems"
-                                       if grouped else "one launch per linear") +
+                   "launch_grouping": ("the whole step is one call (sfmp_gemm_grouped_v): ONE pre-pass + ONE GEMV "
+                                       "launch (token counts 1..16 mixed, each linear at its own n-tile count) + "
+                                       "ONE fix-up for all 35 problems" if grouped else "one launch per linear") +
                                       ("; sfmp_gemm_sharded: + ONE NCCL all-gather of all 35 problems' shard rows "
                                        "and ONE un-permute launch" if sharded else ""),
                    "l2": f"inputs larger than L2: {COPIES} rotating device copies of the layer "
                          f"({sum(i['payload_bytes'] for i in infos.values()) * COPIES / 1e6:.0f} MB)",
-                   "cuda_graph": use_graph,
+                   "cuda_graph": (f"{COPIES} consecutive steps per graph replay (+ single-step graphs for the "
+                                  f"remainder of --steps)") if use_graph else False,
                    "parallelism": "single GPU" if not sharded else
                    f"N-sharded x{world} (snake block rows), one NCCL all-gather per step (library communicator)",
                    "parity_max_rel_err_M16": parity},
         "roofline": roofline,
         "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": "us", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
-                "api": ("pinned host x -> H2D per M group on a copy stream, one sfmp_gemm_grouped_v "
+                "api": ("pinned host bf16 x -> H2D per M group on a copy stream, one sfmp_gemm_grouped_v "
                         + ("" if not sharded else "/ sfmp_gemm_sharded ") +
                         "call per group, D2H per group on a second copy stream (copies overlap compute); CUDA "
                         "graph per step, host synchronises on y every step"), "groups": E2E_GROUPS,

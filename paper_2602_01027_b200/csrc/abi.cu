@@ -872,11 +872,9 @@ sfmp_status grouped_impl(const sfmp_dev_model* const* models, const void* const*
         if (Ms[i] <= 16 && ms[i]->gemv_ok) {
             if (!decode_ok(i))
                 return fail(SFMP_ERR_CONFIG, "grouped decode needs a workspace per model (sfmp_workspace_size)");
-            const bool wide = Ms[i] > 8;
-            // same n-tile class, groupable geometry, and a workspace of its own
-            // (the records / partials / counters of one launch must not alias)
-            while (j < count && j - i < 40 && decode_ok(j) && (Ms[j] > 8) == wide &&
-                   sfmpk::gemv_groupable(*ms[i], *ms[j])) {
+            // groupable geometry and a workspace of its own (the records / partials /
+            // counters of one launch must not alias); token counts 1..16 mix freely
+            while (j < count && j - i < 40 && decode_ok(j) && sfmpk::gemv_groupable(*ms[i], *ms[j])) {
                 bool distinct = true;
                 for (int k = i; k < j; ++k) distinct = distinct && workspaces[k] != workspaces[j];
                 if (!distinct) break;

@@ -526,10 +526,12 @@ __device__ __forceinline__ void unit_chunk(const uint8_t* pw, const uint8_t* con
 // One unit (block column) of B bits: the MMA over its chunks, then the
 // block's per-row affine y += s*C + z*Xg (the mirror identity of
 // quantizer.cpp:57-72 without the LUT).
-template <int B, int CH, int NT, bool X2>
-__device__ __forceinline__ void unit_step(const uint8_t* ub, const uint8_t* xr, const uint32_t (&xoff)[NT],
+// NT: n-tiles of this linear (tokens <= 8 or <= 16); NTM: the launch's
+// accumulator width (a launch mixing token classes runs each linear's own NT).
+template <int B, int CH, int NT, int NTM, bool X2>
+__device__ __forceinline__ void unit_step(const uint8_t* ub, const uint8_t* xr, const uint32_t (&xoff)[NTM],
                                           uint32_t chunk_bytes, uint32_t lo_off, uint32_t xg_off, int cw, int lane,
-                                          float (&yacc)[kMT][NT][4]) {
+                                          float (&yacc)[kMT][NTM][4]) {
     float cacc[kMT][NT][4];
 #pragma unroll
     for (int m = 0; m < kMT; ++m)
@@ -582,6 +584,8 @@ struct PendCopy {
     uint32_t dst, bytes;
 };
 
+// NT = the widest linear's n-tile count (M <= 8: 1, M <= 16: 2); linears of
+// both classes may share a launch, each running its own n-tile count.
 // LO = the model's floor bit-width: every unit has LO or LO+1 bits
 // (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
 // two unpack paths and its hot loop stays resident in the instruction cache.
@@ -714,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
         const int r0 = cw * 16 * kMT + g;  // rows r0 + 8*r of the tile
         const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
         // record geometry depends on the linear's M: set when the linear changes
-        int cur_li = -1;
+        int cur_li = -1, cur_nt = NT;
         uint32_t chunk_bytes = 0, lo_off = 0, xg_off = 0, sec = 0;
         uint32_t xoff[NT];  // offset of this lane's B-fragment piece 0 of each n-tile in a record
         float yacc[kMT][NT][4];
@@ -732,6 +736,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
                 const Lin& L = p.lin[li];
                 const RecGeom GL{L.M, X2};
                 chunk_bytes = GL.chunk_bytes();
+                cur_nt = GL.nt_count();
                 lo_off = L.lo_off;
                 sec = L.sec_bytes;
                 xg_off = GL.xg_off(CH);
@@ -771,10 +776,16 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
                 const uint8_t* xr = xs + u * sec;
                 if (SFMP_NOCOMPUTE) {
                     if (bits == 0xF) yacc[0][0][0] += 1.f;  // experiment builds: streaming only
+                } else if (NT == 2 && cur_nt == 1) {
+                    if (bits == LO) {
+                        unit_step<LO, CH, 1, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
+                    } else if constexpr (LO < 8) {
+                        unit_step<LO + 1, CH, 1, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
+                    }
                 } else if (bits == LO) {
-                    unit_step<LO, CH, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
+                    unit_step<LO, CH, NT, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
                 } else if constexpr (LO < 8) {
-                    unit_step<LO + 1, CH, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
+                    unit_step<LO + 1, CH, NT, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
                 }
             }
             __syncwarp();
@@ -1034,9 +1045,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         if (Ms[i] < 1 || Ms[i] > 16) return cudaErrorInvalidValue;
         M = std::max(M, Ms[i]);
     }
-    const int NT = M > 8 ? 2 : 1;
-    for (int i = 0; i < n; ++i)
-        if ((Ms[i] > 8 ? 2 : 1) != NT) return cudaErrorInvalidValue;  // one n-tile count per launch
+    const int NT = M > 8 ? 2 : 1;  // the widest linear's n-tile count
     const bool X2 = dt == SFMP_F32;
     const int CH = static_cast<int>(m0.n_b / 128);
     Params p{};
