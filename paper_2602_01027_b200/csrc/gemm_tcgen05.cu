@@ -682,6 +682,9 @@ uint32_t unit_max_bytes(const DevModel& m) {
 // reduce launch.  Measured constants (tools/mma_bench.cu, round 1): one
 // 128-column chunk = 8 MMAs of K=16, ~130 cycles each for N <= 128 and ~138
 // at N = 256.
+#ifndef SFMP_KSPLIT_MBPS
+#define SFMP_KSPLIT_MBPS 6.0e6
+#endif
 constexpr int kVirtualSMs = 148;
 int k_splits(const DevModel& m, int64_t M) {
     const int64_t N = tile_n(M), TT = (M + N - 1) / N;
@@ -694,7 +697,7 @@ int k_splits(const DevModel& m, int64_t M) {
         const int64_t items = tiles_g * ks;
         const double waves = static_cast<double>((items + kVirtualSMs - 1) / kVirtualSMs);
         double t = waves * (static_cast<double>((KC + ks - 1) / ks) * chunk_us + item_us);
-        if (ks > 1) t += static_cast<double>(items) * N * 128 * 4 * 2 / 6.0e6 + 3.0;  // partials via L2 + reduce
+        if (ks > 1) t += static_cast<double>(items) * N * 128 * 4 * 2 / SFMP_KSPLIT_MBPS + 3.0;  // partials via L2 + reduce
         if (t < best_t * 0.97) {  // prefer fewer splits unless clearly faster
             best_t = t;
             best = static_cast<int>(ks);
