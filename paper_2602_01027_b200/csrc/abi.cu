@@ -241,14 +241,10 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
     d->RT = static_cast<uint32_t>(d->rows / d->TR);
     const uint32_t TR = d->TR, tiles = p.m_b / TR;
     const uint64_t rb = p.n_b / 8, pb_blk = static_cast<uint64_t>(p.m_b) * rb, pb_unit = TR * rb;
-    // unit-major repack: for each block row, each TR-row tile, each block column
-    std::vector<uint8_t> payload;
-    uint64_t total = 0, sum = 0;
-    for (uint64_t br : brows)
-        for (uint64_t bc = 0; bc < BC; ++bc) total += 4ull * p.m_b + p.bits[br * BC + bc] * pb_blk;
-    payload.resize(total);
+    // unit descriptors: units ordered (block row, TR-row tile, block column), each
+    // scales[TR] | zeros[TR] | planes (the bytes of SFMPPKD1, re-ordered)
+    uint64_t pos = 0, sum = 0;
     d->h_unit_desc.reserve(static_cast<size_t>(d->RT) * BC);
-    uint64_t pos = 0;
     for (uint64_t br : brows) {
         for (uint64_t bc = 0; bc < BC; ++bc) {
             sum += p.bits[br * BC + bc];
@@ -256,22 +252,13 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
         }
         for (uint32_t t = 0; t < tiles; ++t)
             for (uint64_t bc = 0; bc < BC; ++bc) {
-                const uint64_t k = br * BC + bc;
-                const uint8_t* blk = bytes + p.off[k];
-                const int bits = p.bits[k];
-                const uint64_t ro = static_cast<uint64_t>(t) * TR;
+                const int bits = p.bits[br * BC + bc];
                 d->h_unit_desc.push_back(pos | (static_cast<uint64_t>(bits) << 48));
-                std::memcpy(&payload[pos], blk + 2 * ro, 2ull * TR);                    // scales
-                std::memcpy(&payload[pos + 2ull * TR], blk + 2ull * p.m_b + 2 * ro, 2ull * TR);  // zeros
-                pos += 4ull * TR;
-                for (int i = 0; i < bits; ++i) {
-                    std::memcpy(&payload[pos], blk + 4ull * p.m_b + i * pb_blk + ro * rb, pb_unit);
-                    pos += pb_unit;
-                }
+                pos += 4ull * TR + bits * pb_unit;
             }
     }
     d->avg_bits = d->K ? static_cast<double>(sum) / d->K : 0.0;
-    d->payload_bytes = payload.size();
+    d->payload_bytes = pos;
     sfmp_status s;
     if ((s = dev_upload(*d, &d->d_unit_desc, d->h_unit_desc.data(), d->h_unit_desc.size() * 8))) return s;
     std::vector<uint32_t> cp(p.cols);
@@ -285,10 +272,9 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
         std::vector<uint8_t> lp;
         std::vector<uint64_t> lo;
         std::vector<uint8_t> lb;
-        const uint64_t BCn = p.cols / p.n_b;
         for (uint64_t br : brows)
-            for (uint64_t bc = 0; bc < BCn; ++bc) {
-                const uint64_t k = br * BCn + bc;
+            for (uint64_t bc = 0; bc < BC; ++bc) {
+                const uint64_t k = br * BC + bc;
                 const uint64_t n = (k + 1 < p.K ? p.off[k + 1] : p.payload_end) - p.off[k];
                 lo.push_back(lp.size());
                 lb.push_back(p.bits[k]);
@@ -299,22 +285,137 @@ sfmp_status build_model(const uint8_t* bytes, const Parsed& p, int device,
         if ((s = dev_upload(*d, &d->d_lut_off, lo.data(), lo.size() * 8))) return s;
         if ((s = dev_upload(*d, &d->d_lut_bits, lb.data(), lb.size()))) return s;
     }
-    if (!(flags & SFMP_MODEL_DECODE_ONLY) || !d->gemv_ok) {  // the prefill GEMM's own layout
-        std::vector<uint8_t> wl;
-        std::vector<uint64_t> woff;
-        if (sfmpk::build_gemm_layout(*d, payload, out_map, wl, woff)) {
-            if ((s = dev_upload(*d, &d->d_gl, wl.data(), wl.size()))) return s;
-            if ((s = dev_upload(*d, &d->d_gl_off, woff.data(), woff.size() * 8))) return s;
-            d->gl_bytes = wl.size();
-            const std::vector<uint32_t> xslot = sfmpk::gemm_slot_table(cp);
-            if ((s = dev_upload(*d, &d->d_xslot, xslot.data(), xslot.size() * 4))) return s;
+    const bool want_gemm = !(flags & SFMP_MODEL_DECODE_ONLY) || !d->gemv_ok;
+    if (d->gemv_ok) {
+        // Device-side ingest (csrc/ingest.cu): the model's blocks are
+        // uploaded as stored (one span per block row) and both layouts are built by
+        // kernels; the host only keeps O(blocks) + O(rows x chunks) bookkeeping.
+        std::vector<uint64_t> raw_off;
+        std::vector<uint8_t> lbits;
+        uint64_t raw_bytes = 0;
+        for (uint64_t br : brows) {
+            const uint64_t k0 = br * BC, k1 = k0 + BC;
+            const uint64_t end = k1 < p.K ? p.off[k1] : p.payload_end;
+            for (uint64_t k = k0; k < k1; ++k) {
+                raw_off.push_back(raw_bytes + (p.off[k] - p.off[k0]));
+                lbits.push_back(p.bits[k]);
+            }
+            raw_bytes += end - p.off[k0];
         }
+        uint8_t* raw = nullptr;
+        uint64_t* d_raw_off = nullptr;
+        uint8_t* d_lbits = nullptr;
+        auto release = [&]() {
+            if (raw) cudaFree(raw);
+            if (d_raw_off) cudaFree(d_raw_off);
+            if (d_lbits) cudaFree(d_lbits);
+        };
+        SFMP_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&raw), raw_bytes));
+        if ((e = cudaMalloc(reinterpret_cast<void**>(&d_raw_off), raw_off.size() * 8)) != cudaSuccess ||
+            (e = cudaMalloc(reinterpret_cast<void**>(&d_lbits), lbits.size())) != cudaSuccess) {
+            release();
+            return cuda_fail(e, "ingest staging");
+        }
+        uint64_t at = 0;
+        for (uint64_t br : brows) {
+            const uint64_t k0 = br * BC, k1 = k0 + BC;
+            const uint64_t n = (k1 < p.K ? p.off[k1] : p.payload_end) - p.off[k0];
+            e = cudaMemcpy(raw + at, bytes + p.off[k0], n, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) break;
+            at += n;
+        }
+        if (e == cudaSuccess) e = cudaMemcpy(d_raw_off, raw_off.data(), raw_off.size() * 8, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(d_lbits, lbits.data(), lbits.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            release();
+            return cuda_fail(e, "ingest upload");
+        }
+        if ((s = dev_upload<uint8_t>(*d, &d->d_payload, nullptr, d->payload_bytes))) {
+            release();
+            return s;
+        }
+        e = sfmpk::device_unit_layout(raw, d_raw_off, d_lbits, p.m_b, p.n_b, static_cast<uint32_t>(BC),
+                                      static_cast<uint32_t>(d->h_unit_desc.size()), d->d_unit_desc, d->d_payload, 0);
+        if (e == cudaSuccess && want_gemm && p.cols % 128 == 0) {
+            // row-tile layout: tile (T, kc) holds output rows 128T.. (inverse of out_map)
+            const uint64_t KC = p.cols / 128, RT2 = (out_rows + 127) / 128;
+            const int F = p.floor_bits;
+            std::vector<uint32_t> inv(RT2 * 128, 0xFFFFFFFFu);
+            for (uint64_t i = 0; i < out_map.size(); ++i)
+                if (out_map[i] < inv.size()) inv[out_map[i]] = static_cast<uint32_t>(i);
+            std::vector<uint64_t> woff(RT2 * KC + 1, 0);
+            uint64_t w = 0;
+            for (uint64_t T = 0; T < RT2; ++T)
+                for (uint64_t kc = 0; kc < KC; ++kc) {
+                    woff[T * KC + kc] = w;
+                    const uint64_t bc = kc * 128 / p.n_b;
+                    uint64_t nh = 0;
+                    for (int r = 0; r < 128; ++r) {
+                        const uint32_t i = inv[T * 128 + r];
+                        if (i != 0xFFFFFFFFu && lbits[(i / p.m_b) * BC + bc] > F) ++nh;
+                    }
+                    w += 528 + static_cast<uint64_t>(F) * 2048 + nh * 16;
+                }
+            woff[RT2 * KC] = w;
+            uint32_t* d_inv = nullptr;
+            if ((s = dev_upload<uint8_t>(*d, &d->d_gl, nullptr, w)) ||
+                (s = dev_upload(*d, &d->d_gl_off, woff.data(), woff.size() * 8))) {
+                release();
+                return s;
+            }
+            e = cudaMalloc(reinterpret_cast<void**>(&d_inv), inv.size() * 4);
+            if (e == cudaSuccess) e = cudaMemcpy(d_inv, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess)
+                e = sfmpk::device_tile_layout(raw, d_raw_off, d_lbits, p.m_b, p.n_b, static_cast<uint32_t>(BC), d_inv,
+                                              d->d_gl_off, RT2 * KC, static_cast<uint32_t>(KC), F, d->d_gl, 0);
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            if (d_inv) cudaFree(d_inv);
+            d->gl_bytes = w;
+            d->gl_row_tiles = RT2;
+            if (e == cudaSuccess) {
+                const std::vector<uint32_t> xslot = sfmpk::gemm_slot_table(cp);
+                if ((s = dev_upload(*d, &d->d_xslot, xslot.data(), xslot.size() * 4))) {
+                    release();
+                    return s;
+                }
+            }
+        }
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        release();
+        if (e != cudaSuccess) return cuda_fail(e, "device ingest");
+    } else {
+        // other geometries: the unit-major layout in plane form, built on the host
+        std::vector<uint8_t> payload(d->payload_bytes);
+        uint64_t at = 0;
+        for (uint64_t br : brows)
+            for (uint32_t t = 0; t < tiles; ++t)
+                for (uint64_t bc = 0; bc < BC; ++bc) {
+                    const uint64_t k = br * BC + bc;
+                    const uint8_t* blk = bytes + p.off[k];
+                    const int bits = p.bits[k];
+                    const uint64_t ro = static_cast<uint64_t>(t) * TR;
+                    std::memcpy(&payload[at], blk + 2 * ro, 2ull * TR);                                // scales
+                    std::memcpy(&payload[at + 2ull * TR], blk + 2ull * p.m_b + 2 * ro, 2ull * TR);   // zeros
+                    at += 4ull * TR;
+                    for (int i = 0; i < bits; ++i) {
+                        std::memcpy(&payload[at], blk + 4ull * p.m_b + i * pb_blk + ro * rb, pb_unit);
+                        at += pb_unit;
+                    }
+                }
+        if (want_gemm) {
+            std::vector<uint8_t> wl;
+            std::vector<uint64_t> woff;
+            if (sfmpk::build_gemm_layout(*d, payload, out_map, wl, woff)) {
+                if ((s = dev_upload(*d, &d->d_gl, wl.data(), wl.size()))) return s;
+                if ((s = dev_upload(*d, &d->d_gl_off, woff.data(), woff.size() * 8))) return s;
+                d->gl_bytes = wl.size();
+                const std::vector<uint32_t> xslot = sfmpk::gemm_slot_table(cp);
+                if ((s = dev_upload(*d, &d->d_xslot, xslot.data(), xslot.size() * 4))) return s;
+            }
+        }
+        if ((s = dev_upload(*d, &d->d_payload, payload.data(), payload.size()))) return s;
     }
     d->gemm_ok = sfmpk::gemm_supported(*d);
-    // The decode layout stores <= 4-bit units repacked for one-LOP3 unpacking
-    // (same bytes, csrc/repack.cuh); the GEMM layout above was built from the planes.
-    sfmpk::repack_units(*d, payload);
-    if ((s = dev_upload(*d, &d->d_payload, payload.data(), payload.size()))) return s;
     const size_t ws = d->gemv_ok ? sfmpk::gemv_workspace_bytes(*d, 16) : 0;
     if (ws) {
         if ((s = dev_upload<float>(*d, &d->d_ws, nullptr, ws))) return s;

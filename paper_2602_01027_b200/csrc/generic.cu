@@ -193,44 +193,6 @@ GenParams make_params(const DevModel& m) {
 
 }  // namespace
 
-// Host: rewrite every unit of the unit-major payload into the decode GEMV's
-// lane-major order (repack.cuh: lm_sz_off / lm_word_off), <= 4-bit groups
-// repacked for one-LOP3 unpacking; in place, byte count unchanged.
-void repack_units(const DevModel& d, std::vector<uint8_t>& payload) {
-    if (!d.gemv_ok) return;  // only the decode GEMV's geometry (TR=128, n_b in {128, 256})
-    const uint32_t TR = d.TR, nb8 = d.n_b / 8, groups = d.n_b / 32;
-    const uint64_t PS = static_cast<uint64_t>(TR) * nb8;
-    std::vector<uint8_t> tmp;
-    for (uint64_t desc : d.h_unit_desc) {
-        const int B = static_cast<int>((desc >> 48) & 0xF);
-        uint8_t* u = payload.data() + (desc & 0xFFFFFFFFFFFFull);
-        const size_t ub = 4ull * TR + B * PS;
-        tmp.assign(u, u + ub);
-        const uint8_t* planes = tmp.data() + 4ull * TR;
-        for (uint32_t r = 0; r < TR; ++r) {
-            const uint32_t so = lm_sz_off(r);
-            std::memcpy(u + so, tmp.data() + 2 * r, 2);           // s
-            std::memcpy(u + so + 2, tmp.data() + 2 * TR + 2 * r, 2);  // z
-            for (uint32_t g = 0; g < groups; ++g) {
-                uint32_t pw[8], codes[32], out[8];
-                for (int i = 0; i < B; ++i) std::memcpy(&pw[i], planes + i * PS + r * nb8 + g * 4, 4);
-                if (B <= 4) {
-                    for (int k = 0; k < 32; ++k) {
-                        uint32_t c = 0;
-                        for (int i = 0; i < B; ++i) c |= ((pw[i] >> k) & 1u) << i;
-                        codes[k] = c;
-                    }
-                    rp_pack(codes, B, out);
-                } else {
-                    for (int i = 0; i < B; ++i) out[i] = pw[i];
-                }
-                for (int i = 0; i < B; ++i)
-                    std::memcpy(u + 512 + lm_word_off(static_cast<uint32_t>(B), g >> 2, r, g & 3, static_cast<uint32_t>(i)), &out[i], 4);
-            }
-        }
-    }
-}
-
 cudaError_t launch_generic(const DevModel& m, const void* x, sfmp_dtype dt, int64_t M, float* y,
                            cudaStream_t st) {
     GenParams p = make_params(m);

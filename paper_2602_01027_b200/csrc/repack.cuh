@@ -57,7 +57,7 @@ __host__ __device__ inline uint32_t rp_code(const uint32_t* w, int B, int k) {
 }
 
 // Host: codes[32] of one group -> B repacked words.
-inline void rp_pack(const uint32_t* codes, int B, uint32_t* out) {
+__host__ __device__ inline void rp_pack(const uint32_t* codes, int B, uint32_t* out) {
     for (int i = 0; i < B; ++i) out[i] = 0u;
     for (int k = 0; k < 32; ++k) {
         const int j = rp_reg_of(k), half = rp_half_of(k);

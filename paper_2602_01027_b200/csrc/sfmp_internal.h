@@ -135,9 +135,17 @@ cudaError_t launch_unpack(const DevModel& m, uint8_t* codes, cudaStream_t st);
 cudaError_t launch_unpermute_gathered(const DevModel& m, const float* gathered, int64_t M,
                                       float* y, cudaStream_t st);
 
+// Device-side ingest (ingest.cu): the unit-major lane-major layout and the
+// row-tile layout built from the blocks as stored.
+cudaError_t device_unit_layout(const uint8_t* raw, const uint64_t* raw_off, const uint8_t* bits, uint32_t m_b,
+                               uint32_t n_b, uint32_t BC, uint32_t units, const uint64_t* unit_desc, uint8_t* dst,
+                               cudaStream_t st);
+cudaError_t device_tile_layout(const uint8_t* raw, const uint64_t* raw_off, const uint8_t* bits, uint32_t m_b,
+                               uint32_t n_b, uint32_t BC, const uint32_t* inv, const uint64_t* woff, uint64_t tiles,
+                               uint32_t KC, int F, uint8_t* dst, cudaStream_t st);
+
 // K2 prefill GEMM (tcgen05)
 bool gemm_supported(const DevModel& m);
-void repack_units(const DevModel& d, std::vector<uint8_t>& payload);
 std::vector<uint32_t> gemm_slot_table(const std::vector<uint32_t>& col_perm);
 bool build_gemm_layout(DevModel& d, const std::vector<uint8_t>& payload, const std::vector<uint32_t>& out_map,
                        std::vector<uint8_t>& wl, std::vector<uint64_t>& woff);
