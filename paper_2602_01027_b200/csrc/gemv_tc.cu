@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kNCW);
+            mbar_init(&empty[s], kNCW * 32);  // every compute lane releases the stage
         }
         fence_mbar_init();
         fence_proxy_async();
@@ -727,7 +727,13 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
         for (;;) {
             if (SFMP_SPIN) mbar_wait_a(full_a + 8 * s, ph);
             else mbar_wait_idle(full_a + 8 * s, ph);
-            const uint4 info = sinfo[s];
+            // lane 0 reads the stage info and is the lane that later frees the stage
+            // (the producer rewrites sinfo[s] after that arrive): broadcast it
+            uint4 info = make_uint4(0u, 0u, 0u, 0u);
+            if (lane == 0) info = sinfo[s];
+            info.x = __shfl_sync(0xffffffffu, info.x, 0);
+            info.y = __shfl_sync(0xffffffffu, info.y, 0);
+            info.z = __shfl_sync(0xffffffffu, info.z, 0);
             const uint32_t fl = info.x >> 20;
             if (fl & kEnd) break;
             const int li = static_cast<int>(info.x & 0xFF);
@@ -788,8 +794,8 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
                     unit_step<LO + 1, CH, NT, NT, X2>(ub, xr, xoff, chunk_bytes, lo_off, xg_off, cw, lane, yacc);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_a(empty_a + 8 * s);
+            // every lane arrives (its own reads of the stage precede its own release)
+            mbar_arrive_a(empty_a + 8 * s);
             if (++s == S) { s = 0; ph ^= 1; }
             if (!(fl & kLast)) continue;
 

@@ -43,3 +43,20 @@ def test_dropin_matches_reference_gemv(gpu, port, tmp_path, bits, mode):
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "format_error=1 shape_error=1" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_sharded_entry_world1(gpu, port, tmp_path):
+    """A C++ caller of sfmp_gemm_sharded (NCCL communicator from sfmp_nccl_comm_init,
+    world 1): bit-identical to sfmp_gemm; a size-mismatched communicator is refused."""
+    exe = tmp_path / "sharded_test"
+    lib_dir = os.path.join(ROOT, "paper_2602_01027_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-o", str(exe), os.path.join(ROOT, "tests", "cpp", "sharded_test.cpp"),
+                        f"-I{os.path.join(ROOT, 'include')}", "-I/usr/local/cuda/include", f"-L{lib_dir}", "-lsfmp_b200",
+                        "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib_dir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    data = model_bytes(port, 1024, 1024, 3.25)
+    (tmp_path / "m.sfmp").write_bytes(data)
+    r = subprocess.run([str(exe), str(tmp_path / "m.sfmp")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "sharded_vs_unsharded_bit_equal=1" in r.stdout
