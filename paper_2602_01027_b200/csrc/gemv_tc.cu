@@ -88,6 +88,17 @@ constexpr int kSmemSM = 225 * 1024;
 #ifndef SFMP_EXP_NOMMA
 #define SFMP_EXP_NOMMA 0
 #endif
+#ifndef SFMP_YTOT_GLOBAL
+#define SFMP_YTOT_GLOBAL 0
+#endif
+
+#ifndef SFMP_FIX_PAIRS
+#define SFMP_FIX_PAIRS 1
+#endif
+constexpr int kFixPairs = SFMP_FIX_PAIRS;  // (tile, token) pairs per fix-up warp
+#ifndef SFMP_EXP_NOFIXUP
+#define SFMP_EXP_NOFIXUP 0
+#endif
 #ifndef SFMP_EXP_EMPTY
 #define SFMP_EXP_EMPTY 0
 #endif
@@ -130,7 +141,8 @@ struct Lin {
     int RT;
     uint32_t sec_bytes;         // one record section (one block column, one bit-width layout)
     uint32_t lo_off;            // offset of the lo fragments inside a 128-column chunk (f32 input)
-    int item0;                  // first work item of this linear
+    int item0;                  // first work item of this linear (queue order)
+    int IP;                     // work items per tile: P (one per segment) or 1 (the whole K, P > 1)
     int fix0;                   // first fix-up (tile, token) pair of this linear
     int lo;                     // floor bits: units at lo use section 0, lo+1 section 1
 };
@@ -139,7 +151,9 @@ struct Params {
     int nlin;
     int n_items;
     int n_fix;           // fix-up (tile, token) pairs
-    int item_start[kMaxLin + 1];  // first work item of each linear (+ total)
+    int item_start[kMaxLin + 1];  // first work item of each queue slot (+ total)
+    int qlin[kMaxLin];            // linear of each queue slot: whole-K linears first
+    int any_whole;                // some linear runs whole-K items (TMEM running sums)
     int fix_start[kMaxLin + 1];   // first fix-up pair of each linear (+ total; none if P == 1)
     unsigned* queue;     // [0] next item, [1] CTAs done (zero between calls)
     int n_b;
@@ -578,7 +592,8 @@ __device__ __forceinline__ void mbar_wait_idle(uint32_t bar, uint32_t parity) {
 // A stage holds SU consecutive units of one work item (SU = 2 for n_b = 128,
 // 1 for n_b = 256: 256 columns either way) and their record sections.
 // Stage info (16 B): x = linear | bits0 << 8 | bits1 << 12 | units << 16 | flags << 20, y = row tile, z = segment.
-constexpr uint32_t kFirst = 1, kLast = 2, kEnd = 4;
+// kFirst / kLast: first / last stage of a segment; kItemLast: last stage of the work item.
+constexpr uint32_t kFirst = 1, kLast = 2, kEnd = 4, kItemLast = 8;
 struct PendCopy {
     const uint8_t* src;
     uint32_t dst, bytes;
@@ -589,7 +604,9 @@ struct PendCopy {
 // LO = the model's floor bit-width: every unit has LO or LO+1 bits
 // (PackedModel::validate, layout.cpp:100-103), so the kernel carries exactly
 // two unpack paths and its hot loop stays resident in the instruction cache.
-template <int NT, int CH, int LO, bool X2>
+// WH = the launch has whole-K items (only n_b = 128 with 16-bit x: the running
+// sums cost registers, so launches without whole-K items use the lean build).
+template <int NT, int CH, int LO, bool X2, bool WH>
 __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel(const Params p) {
     constexpr int SU = CH == 1 ? SFMP_SU : 1;
     constexpr int nb8 = CH * 16;
@@ -649,17 +666,24 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
             unsigned item = atomicAdd(p.queue, 1u);
             while (item < static_cast<unsigned>(p.n_items)) {
                 const unsigned next = atomicAdd(p.queue, 1u);  // claim ahead: latency overlaps this item
-                const int li = owner_of(p.item_start, p.nlin, static_cast<int>(item));
+                const int li = p.qlin[owner_of(p.item_start, p.nlin, static_cast<int>(item))];
                 const Lin& L = p.lin[li];
                 const int rel = static_cast<int>(item) - L.item0;
-                const int rt = rel / L.P, seg = rel - rt * L.P;
-                const int bc0 = seg * L.L, bc1 = min(L.BC, bc0 + L.L);
+                const int rt = rel / L.IP, seg0 = rel - rt * L.IP;
+                // a whole-K item (IP == 1) runs all segments of its tile back to back
+                const int bc0 = seg0 * L.L, bc1 = L.IP == 1 ? L.BC : min(L.BC, bc0 + L.L);
                 const uint64_t* gdesc = L.unit_desc + static_cast<size_t>(rt) * L.BC;
                 const uint32_t sec = L.sec_bytes;
                 uint64_t d0n = ldg_keep_u64(gdesc + bc0, keep);
                 uint64_t d1n = (SU == 2 && bc0 + 1 < bc1) ? ldg_keep_u64(gdesc + bc0 + 1, keep) : 0ull;
+                int seg = seg0, seg_beg = bc0, seg_end = min(bc1, bc0 + L.L);
                 for (int bc = bc0; bc < bc1; bc += SU) {
                     const int nu = min(SU, bc1 - bc);
+                    if (bc == seg_end) {  // a stage never straddles a segment (L % SU == 0)
+                        ++seg;
+                        seg_beg = seg_end;
+                        seg_end = min(bc1, seg_end + L.L);
+                    }
                     const uint64_t d0 = d0n, d1 = d1n;
                     if (bc + SU < bc1) {
                         d0n = ldg_keep_u64(gdesc + bc + SU, keep);
@@ -669,7 +693,8 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
                     mbar_wait_idle(empty_a + 8 * s, ph ^ 1);
                     const int b0 = static_cast<int>((d0 >> 48) & 0xF);
                     const int b1 = nu > 1 ? static_cast<int>((d1 >> 48) & 0xF) : 0;
-                    const uint32_t fl = (bc == bc0 ? kFirst : 0u) | (bc + nu == bc1 ? kLast : 0u);
+                    const uint32_t fl = (bc == seg_beg ? kFirst : 0u) | (bc + nu == seg_end ? kLast : 0u) |
+                                        (bc + nu == bc1 ? kItemLast : 0u);
                     sinfo[s] = make_uint4(static_cast<uint32_t>(li) | (static_cast<uint32_t>(b0) << 8) |
                                               (static_cast<uint32_t>(b1) << 12) | (static_cast<uint32_t>(nu) << 16) |
                                               (fl << 20),
@@ -722,6 +747,9 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
         uint32_t chunk_bytes = 0, lo_off = 0, xg_off = 0, sec = 0;
         uint32_t xoff[NT];  // offset of this lane's B-fragment piece 0 of each n-tile in a record
         float yacc[kMT][NT][4];
+#if !SFMP_YTOT_GLOBAL
+        float ytot[WH ? kMT : 1][WH ? NT : 1][4];  // whole-K item: the segment sums added in segment order
+#endif
         float ysa[NT][2], ysb[NT][2];
         int s = 0, ph = 0;
         for (;;) {
@@ -803,6 +831,45 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
             const Lin& L = p.lin[li];
             const int rt = static_cast<int>(info.y), seg = static_cast<int>(info.z);
             const bool whole = L.P == 1;
+            if (WH && L.IP == 1 && !whole) {
+                // whole-K item: ((0 + s_0) + s_1) + ... -- the same float operations
+                // gemv_fixup_kernel performs on the partials, so the bits do not depend
+                // on how the call was cut into items
+#pragma unroll
+                for (int m = 0; m < kMT; ++m)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float v = (yacc[m][nt][e] * ysa[nt][e & 1]) * ysb[nt][e & 1];  // exact
+#if SFMP_YTOT_GLOBAL
+                            // the running sum in this thread's own slot of the tile's partials
+                            const int t = nt * 8 + 2 * q + (e & 1);
+                            float* slot = L.part + static_cast<size_t>(rt) * L.P * (16 * kTR) + t * kTR + r0 + 16 * m + 8 * (e >> 1);
+                            yacc[m][nt][e] = (seg == 0 ? 0.f : *slot) + v;
+                            if (!(fl & kItemLast)) *slot = yacc[m][nt][e];
+#else
+                            ytot[m][nt][e] = (seg == 0 ? 0.f : ytot[m][nt][e]) + v;
+#endif
+                        }
+                if (!(fl & kItemLast)) continue;
+#pragma unroll
+                for (int m = 0; m < kMT; ++m)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int t = nt * 8 + 2 * q + (e & 1);
+                            if (t >= L.M) continue;
+                            const int row = r0 + 16 * m + 8 * (e >> 1);
+#if SFMP_YTOT_GLOBAL
+                            L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = yacc[m][nt][e];
+#else
+                            L.y[t * L.out_rows + __ldg(L.out_map + rt * kTR + row)] = ytot[m][nt][e];
+#endif
+                        }
+                continue;
+            }
             float* dst = whole ? L.y : L.part + (static_cast<size_t>(rt) * L.P + seg) * (16 * kTR);
 #pragma unroll
             for (int m = 0; m < kMT; ++m)
@@ -840,33 +907,58 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm(NT, LO, X2)) gemv_kernel
 __global__ void __launch_bounds__(256) gemv_fixup_kernel(const Params p) {
     pdl_launch_dependents();  // a later launch of the same grouped call may start its pre-pass
     const int lane = threadIdx.x & 31;
-    const int w = static_cast<int>(blockIdx.x) * 8 + static_cast<int>(threadIdx.x >> 5);
-    if (w >= p.n_fix) return;
-    const Lin& L = p.lin[owner_of(p.fix_start, p.nlin, w)];
-    const int rel = w - L.fix0, rt = rel / L.M, t = rel - rt * L.M;
-    const uint4 om = __ldg(reinterpret_cast<const uint4*>(L.out_map + rt * kTR) + lane);
-    const float4* pp = reinterpret_cast<const float4*>(L.part + static_cast<size_t>(rt) * L.P * (16 * kTR) + t * kTR) + lane;
-    pdl_wait();  // the GEMV grid has completed and its partials are visible
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k0 = 0; k0 < L.P; k0 += 16) {
-        float4 v[16];
+    // kFixPairs (tile, token) pairs per warp, all their partial loads issued before any is used
+    const int w0 = (static_cast<int>(blockIdx.x) * 8 + static_cast<int>(threadIdx.x >> 5)) * kFixPairs;
+    if (w0 >= p.n_fix) return;
+    const float4* pp[kFixPairs];
+    float* yrow[kFixPairs];
+    uint4 om[kFixPairs];
+    int P[kFixPairs];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (k0 + k < L.P) v[k] = __ldg(pp + (k0 + k) * (16 * kTR / 4));  // previous grid's data
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (k0 + k < L.P) {  // segment order
-                acc.x += v[k].x;
-                acc.y += v[k].y;
-                acc.z += v[k].z;
-                acc.w += v[k].w;
-            }
+    for (int h = 0; h < kFixPairs; ++h) {
+        P[h] = 0;
+        const int w = w0 + h;
+        if (w >= p.n_fix) continue;
+        const Lin& L = p.lin[owner_of(p.fix_start, p.nlin, w)];
+        const int rel = w - L.fix0, rt = rel / L.M, t = rel - rt * L.M;
+        P[h] = L.P;
+        om[h] = __ldg(reinterpret_cast<const uint4*>(L.out_map + rt * kTR) + lane);
+        pp[h] = reinterpret_cast<const float4*>(L.part + static_cast<size_t>(rt) * L.P * (16 * kTR) + t * kTR) + lane;
+        yrow[h] = L.y + static_cast<size_t>(t) * L.out_rows;
     }
-    float* yrow = L.y + static_cast<size_t>(t) * L.out_rows;
-    yrow[om.x] = acc.x;
-    yrow[om.y] = acc.y;
-    yrow[om.z] = acc.z;
-    yrow[om.w] = acc.w;
+    pdl_wait();  // the GEMV grid has completed and its partials are visible
+    int Pm = 0;
+#pragma unroll
+    for (int h = 0; h < kFixPairs; ++h) Pm = max(Pm, P[h]);
+    float4 acc[kFixPairs];
+#pragma unroll
+    for (int h = 0; h < kFixPairs; ++h) acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < Pm; k0 += 8) {
+        float4 v[kFixPairs][8];
+#pragma unroll
+        for (int h = 0; h < kFixPairs; ++h)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < P[h]) v[h][k] = __ldg(pp[h] + (k0 + k) * (16 * kTR / 4));  // previous grid's data
+#pragma unroll
+        for (int h = 0; h < kFixPairs; ++h)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (k0 + k < P[h]) {  // segment order
+                    acc[h].x += v[h][k].x;
+                    acc[h].y += v[h][k].y;
+                    acc[h].z += v[h][k].z;
+                    acc[h].w += v[h][k].w;
+                }
+    }
+#pragma unroll
+    for (int h = 0; h < kFixPairs; ++h) {
+        if (!P[h]) continue;
+        yrow[h][om[h].x] = acc[h].x;
+        yrow[h][om[h].y] = acc[h].y;
+        yrow[h][om[h].z] = acc[h].z;
+        yrow[h][om[h].w] = acc[h].w;
+    }
 }
 
 // One-time (per device, thread-safe) function attribute setup.
@@ -878,9 +970,9 @@ void once_per_device(std::once_flag* flags, F&& f) {
     std::call_once(flags[dev], f);
 }
 
-template <int NT, int CH, int LO, bool X2>
-cudaError_t launch_k(cudaLaunchConfig_t& cfg, const Params& p) {
-    auto k = gemv_kernel<NT, CH, LO, X2>;
+template <int NT, int CH, int LO, bool X2, bool WH>
+cudaError_t launch_kw(cudaLaunchConfig_t& cfg, const Params& p) {
+    auto k = gemv_kernel<NT, CH, LO, X2, WH>;
     static std::once_flag fl[64];
     static cudaError_t err[64];
     int dev = 0;
@@ -889,6 +981,13 @@ cudaError_t launch_k(cudaLaunchConfig_t& cfg, const Params& p) {
     if (err[dev & 63] != cudaSuccess) return err[dev & 63];
     note_launch();
     return cudaLaunchKernelEx(&cfg, k, p);
+}
+template <int NT, int CH, int LO, bool X2>
+cudaError_t launch_k(cudaLaunchConfig_t& cfg, const Params& p) {
+    if constexpr (CH == 1 && !X2) {
+        if (p.any_whole) return launch_kw<NT, CH, LO, X2, true>(cfg, p);
+    }
+    return launch_kw<NT, CH, LO, X2, false>(cfg, p);
 }
 
 template <int NT, int CH, bool X2>
@@ -973,10 +1072,10 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xitems, int max_col
     cudaError_t e;
     if (NT == 1) e = CH == 1 ? launch_nc<1, 1, X2>(cfg, p, lo) : launch_nc<1, 2, X2>(cfg, p, lo);
     else e = CH == 1 ? launch_nc<2, 1, X2>(cfg, p, lo) : launch_nc<2, 2, X2>(cfg, p, lo);
-    if (e != cudaSuccess || p.n_fix == 0) return e;
+    if (e != cudaSuccess || p.n_fix == 0 || SFMP_EXP_NOFIXUP) return e;
     // split tiles: sum the segment partials (programmatic dependent of the GEMV)
     cudaLaunchConfig_t fc{};
-    fc.gridDim = dim3((p.n_fix + 7) / 8);  // one warp per (tile, token) pair
+    fc.gridDim = dim3((p.n_fix + 8 * kFixPairs - 1) / (8 * kFixPairs));  // kFixPairs (tile, token) pairs per warp
     fc.blockDim = dim3(256);
     fc.stream = st;
     fc.attrs = pdl;
@@ -992,6 +1091,60 @@ int units_per_segment(const DevModel& m) { return std::max(1, kSegCols / static_
 int segments_per_tile(const DevModel& m) {
     const int L = units_per_segment(m);
     return (static_cast<int>(m.BC) + L - 1) / L;
+}
+
+// Work items of one launch.  A multi-segment linear runs either one item per
+// (tile, segment) -- partials summed by the fix-up -- or one item per tile
+// that sums its segments in registers: the same float operations, so the
+// choice changes no bit and is made per call for balance.  Whole-K items
+// (fewer claims, no partial traffic, no fix-up) go first in the queue,
+// shortest K first; the small items -- split linears and single-segment
+// ones -- go last, so the dynamic queue still ends evenly: the small-item
+// work per CTA slot must cover kWholeFrac of the longest whole-K item, and
+// the call keeps at least two items per CTA slot.
+#ifndef SFMP_WHOLE_FRAC
+#define SFMP_WHOLE_FRAC 0.5
+#endif
+#ifndef SFMP_WHOLE_MAX
+#define SFMP_WHOLE_MAX 0.35  // longest whole-K item / average units per CTA slot
+#endif
+void plan_items(Params& p, int slots, bool allow) {
+    const int n = p.nlin;
+    double small = 0.0;
+    int items = 0;
+    for (int i = 0; i < n; ++i) {
+        small += static_cast<double>(p.lin[i].RT) * p.lin[i].BC;
+        items += p.lin[i].RT * p.lin[i].P;
+    }
+    const double total = small;
+    p.any_whole = 0;
+    int order[kMaxLin];
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order, order + n, [&](int a, int b) { return p.lin[a].BC < p.lin[b].BC; });
+    int longest = 0;
+    for (int k = 0; k < n; ++k) {
+        Lin& L = p.lin[order[k]];
+        if (L.P < 2 || !allow) continue;
+        const double rest = small - static_cast<double>(L.RT) * L.BC;
+        const int items_after = items - L.RT * (L.P - 1);
+        const int lw = std::max(longest, L.BC);
+        if (rest < SFMP_WHOLE_FRAC * slots * lw || lw > SFMP_WHOLE_MAX * total / slots || items_after < 2 * slots) break;
+        L.IP = 1;
+        p.any_whole = 1;
+        small = rest;
+        items = items_after;
+        longest = std::max(longest, L.BC);
+    }
+    int q = 0, it = 0;
+    for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i < n; ++i) {
+            Lin& L = p.lin[i];
+            if ((L.IP == 1 && L.P > 1) != (pass == 0)) continue;
+            p.qlin[q] = i;
+            p.item_start[q++] = it;
+            L.item0 = it;
+            it += L.RT * L.IP;
+        }
 }
 
 // Shared-memory plan of one launch: stages and resident CTAs per SM (fewer
@@ -1083,12 +1236,7 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
         L.sec_bytes = static_cast<uint32_t>(G.sec_bytes(CH));
         L.lo_off = static_cast<uint32_t>(G.lo_off());
         L.lo = m.floor_bits;
-        L.item0 = items;
-        p.item_start[i] = items;
-        p.fix_start[i] = fix;
-        items += static_cast<int>(m.RT) * L.P;
-        L.fix0 = fix;
-        if (L.P > 1) fix += static_cast<int>(m.RT) * Ms[i];  // (tile, token) fix-up pairs
+        L.IP = L.P;
         XLin& X = xp.lin[i];
         X.x = xs[i];
         X.col_perm = m.d_col_perm;
@@ -1107,14 +1255,22 @@ cudaError_t launch_gemv_group(const DevModel* const* ms, const void* const* xs, 
     // the launch's work queue lives in the first problem's workspace (problems
     // of one launch have distinct workspaces)
     p.queue = reinterpret_cast<unsigned*>(wss[0] + gemv_rec_bytes(m0) + gemv_part_bytes(m0));
-    p.n_items = items;
-    p.n_fix = fix;
-    p.item_start[n] = items;
-    p.fix_start[n] = fix;
     p.stage_w = stage_bytes(m0, ceil_bits);
     const SmemPlan sp = smem_plan(p.stage_w, units_per_stage(m0) * p.sec_bytes, NT, m0.floor_bits, X2);
     if (sp.stages < 2) return cudaErrorInvalidConfiguration;  // excluded at upload (gemv_feasible)
     p.stages = sp.stages;
+    plan_items(p, m0.num_sms * sp.ctas, CH == 1 && !X2);
+    for (int i = 0; i < n; ++i) {
+        Lin& L = p.lin[i];
+        p.fix_start[i] = fix;
+        L.fix0 = fix;
+        if (L.IP > 1) fix += L.RT * L.M;  // (tile, token) fix-up pairs
+        items += L.RT * L.IP;
+    }
+    p.n_items = items;
+    p.n_fix = fix;
+    p.item_start[n] = items;
+    p.fix_start[n] = fix;
     const int grid = std::min(items, m0.num_sms * sp.ctas);
     switch (dt) {
         case SFMP_F32: return launch_t<SFMP_F32>(p, xp, xitems, max_cols, grid, sp.smem, m0.floor_bits, st, overlap_prev);

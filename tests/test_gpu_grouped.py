@@ -68,3 +68,27 @@ def test_grouped_per_problem_token_counts(gpu, port):
         # bit-identical with the single-problem call (canonical segment order)
         y1 = sel[i].gemm(xs[i])
         assert torch.equal(ys[i], y1), (i, M)
+
+
+def test_whole_k_items_bit_identical(gpu, port):
+    """The 8B decode step (7 linears x M in {1, 2, 4, 8, 16}) in one call is
+    large enough for whole-K work items: the K = 4096 linears sum their
+    segments in registers (their partial region stays untouched), down_proj
+    keeps per-segment items and the fix-up.  Either way the bits equal the
+    single-linear calls, which use per-segment items only."""
+    import torch
+    from synth import LLAMA_8B
+    names = list(LLAMA_8B)
+    models = {p: gpu.DeviceModel(model_bytes(port, *LLAMA_8B[p], 3.25, m_b=128 if p in ("k_proj", "v_proj") else 512))
+              for p in names}
+    keys = [(p, M) for M in (1, 2, 4, 8, 16) for p in names]
+    xs = [torch.from_numpy(activations(port, M, LLAMA_8B[p][1], seed=M)).cuda().to(torch.bfloat16) for p, M in keys]
+    ws = [torch.zeros(models[p].workspace_bytes(16), dtype=torch.uint8, device="cuda") for p, M in keys]
+    ys = gpu.gemm_grouped([models[p] for p, M in keys], xs, workspaces=ws)
+    torch.cuda.synchronize()
+    for (p, M), x, y, w in zip(keys, xs, ys, ws):
+        rows, cols = LLAMA_8B[p]
+        part = (rows // 128) * (cols // 1024) * 16 * 128 * 4  # [tiles][segments][16 tokens][128 rows] f32
+        touched = bool(w[-(part + 128):-128].any())
+        assert touched == (p == "down_proj"), (p, M)
+        assert torch.equal(y, models[p].gemm(x)), (p, M)
