@@ -803,10 +803,12 @@ def main():
     gx = {M: (xoff[(PROJS[0], M)], xoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][1]) for M in MS}
     gy = {M: (yoff[(PROJS[0], M)], yoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][0]) for M in MS}
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    # group order: a small group first (short exposed H2D) and last (short exposed D2H);
-    # finer groups overlap the PCIe copies better than fewer, larger launches (round 1)
+    # group order: a small group first (short exposed H2D), then the largest so its
+    # 2.75 MB D2H hides under the later groups' compute, the smallest last (short exposed
+    # D2H); measured over 14 orders (tools/gpu_e2e_orders.sh): 2/16/8/4/1 235 us,
+    # 1/4/8/16/2 259 us, one group 334 us
     E2E_GROUPS = ([[int(v) for v in g.split(",")] for g in args.e2e_order.split("/")] if args.e2e_order
-                  else [[1], [4], [8], [16], [2]])
+                  else [[2], [16], [8], [4], [1]])
     assert sorted(M for g in E2E_GROUPS for M in g) == sorted(MS)
     ebufs = {}
     if sharded:
