@@ -74,6 +74,9 @@ constexpr int kAccCol = 0;                // accumulator: columns [0, N)
 constexpr int kACol = 256;                // A buffer ab at kACol + ab*64 (128 f16 of K per row)
 constexpr int kNA = 4;                    // A buffers
 constexpr int kSmemLimit = 227 * 1024;
+#ifndef SFMP_XPREP_WARP
+#define SFMP_XPREP_WARP 1  // warp-per-token prefill pre-pass (0: CTA-per-token, experiment builds)
+#endif
 
 struct GemmParams {
     const uint8_t* wl;       // row-tile layout payload
@@ -229,6 +232,117 @@ __global__ void __launch_bounds__(512) xprep_gemm_rows_kernel(const void* __rest
                          static_cast<const uint8_t*>(x) + static_cast<size_t>(t2) * row_bytes, row_bytes, &bar[buf],
                          policy_evict_first());
             }
+        }
+    }
+}
+
+// Warp-per-token pre-pass (rows up to ~12K columns): NW warps per CTA share the
+// u16 slot table in shared memory; each warp owns one row buffer, bulk-copies
+// its token's x row into it and does the absmax (and fused norm), scaling,
+// conversion and swizzled gather alone -- no CTA barrier per token, so up to
+// 148 x NW tokens are in flight at once (the CTA-per-token pre-pass above
+// serialises a few tokens per CTA behind two row buffers: 17 us for 2048 x
+// 4096 bf16, ~3x its HBM time).  Tokens M..Mpad-1 are written as zeros.
+template <sfmp_dtype DT>
+__global__ void __launch_bounds__(512) xprep_gemm_warp_kernel(const void* __restrict__ x,
+                                                              const uint32_t* __restrict__ xslot,
+                                                              uint8_t* __restrict__ xs, float* __restrict__ ysc, int M,
+                                                              int N, int KC, int cols, int Mpad, const PreNorm norm) {
+    using T = std::conditional_t<DT == SFMP_F32, float, uint16_t>;
+    constexpr int kPerVec = 16 / sizeof(T);  // x elements per 16-byte shared load
+    extern __shared__ __align__(16) uint8_t xsm[];
+    pdl_launch_dependents();
+    const int NW = static_cast<int>(blockDim.x >> 5), w = static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(xsm);                      // [NW]
+    uint16_t* idx = reinterpret_cast<uint16_t*>(xsm + 8 * 16);             // [cols] slot table (<= 16 warps)
+    const uint32_t row_bytes = static_cast<uint32_t>(cols) * sizeof(T);
+    uint8_t* rowbuf = xsm + 8 * 16 + ((static_cast<size_t>(cols) * 2 + 15) / 16) * 16 + static_cast<size_t>(w) * row_bytes;
+    const T* xr = reinterpret_cast<const T*>(rowbuf);
+    const int stride = static_cast<int>(gridDim.x) * NW;
+    int t = static_cast<int>(blockIdx.x) * NW + w;
+    const uint32_t bar_a = smem_u32(&bar[w]);
+    if (lane == 0) {
+        mbar_init(&bar[w], 1);
+        fence_mbar_init();
+        if (t < M) {
+            mbar_arrive_expect_tx(&bar[w], row_bytes);
+            bulk_g2s(rowbuf, static_cast<const uint8_t*>(x) + static_cast<size_t>(t) * row_bytes, row_bytes, &bar[w],
+                     policy_evict_first());
+        }
+    }
+    for (int i = threadIdx.x; i < cols / 4; i += blockDim.x) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(xslot) + i);
+        reinterpret_cast<uint2*>(idx)[i] = make_uint2(v.x | (v.y << 16), v.z | (v.w << 16));
+    }
+    __syncthreads();  // slot table and barrier init visible
+    (void)bar_a;
+    for (int k = 0; t < Mpad; ++k, t += stride) {
+        const int tt = t / N, r = t - tt * N;
+        uint8_t* dst = xs + static_cast<size_t>(tt) * KC * 2 * N * 128 + r * 128;
+        const bool live = t < M;
+        if (live) mbar_wait(&bar[w], static_cast<uint32_t>(k) & 1u);
+        float sc = 1.f, inv = 1.f;
+        if (live && (DT != SFMP_F16 || norm.on)) {
+            float m = 0.f, ss = 0.f;
+            for (int v = lane; v < cols / kPerVec; v += 32) {
+                const uint4 q = *reinterpret_cast<const uint4*>(rowbuf + 16 * v);
+                const T* e = reinterpret_cast<const T*>(&q);
+#pragma unroll
+                for (int i = 0; i < kPerVec; ++i) {
+                    const float f = x_as_float<DT>(e[i]);
+                    if (norm.on) {
+                        ss = fmaf(f, f, ss);
+                        m = fmaxf(m, fabsf(f * gamma_at(norm, kPerVec * v + i)));
+                    } else {
+                        m = fmaxf(m, fabsf(f));
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                ss += __shfl_xor_sync(0xffffffffu, ss, o);
+            }
+            if (norm.on) {
+                inv = 1.f / sqrtf(ss / static_cast<float>(cols) + norm.eps);
+                m *= inv;
+            }
+            const int e = token_exp(m);
+            sc = ldexpf(1.f, -e);
+            if (lane == 0) ysc[t] = ldexpf(1.f, e);
+        } else if (lane == 0) {
+            ysc[t] = live ? 1.f : 0.f;
+        }
+        for (int c = lane; c < KC * 16; c += 32) {
+            const int kc = c >> 4, a = (c >> 3) & 1, j = c & 7;
+            uint4 out = make_uint4(0u, 0u, 0u, 0u);
+            if (live) {
+                const uint4 ii = *reinterpret_cast<const uint4*>(idx + kc * 128 + 64 * a + 8 * j);
+                const uint32_t iv[4] = {ii.x, ii.y, ii.z, ii.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t clo = iv[e] & 0xFFFFu, chi = iv[e] >> 16;
+                    const T lo = xr[clo], hi = xr[chi];
+                    if (DT == SFMP_F16 && !norm.on) {
+                        o[e] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+                    } else if (norm.on) {
+                        o[e] = h2_as_u32(__floats2half2_rn((x_as_float<DT>(lo) * inv) * gamma_at(norm, clo) * sc,
+                                                           (x_as_float<DT>(hi) * inv) * gamma_at(norm, chi) * sc));
+                    } else {
+                        o[e] = h2_as_u32(__floats2half2_rn(x_as_float<DT>(lo) * sc, x_as_float<DT>(hi) * sc));
+                    }
+                }
+                out = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+            *reinterpret_cast<uint4*>(dst + (static_cast<size_t>(kc) * 2 + a) * N * 128 + ((j ^ (r & 7)) << 4)) = out;
+        }
+        __syncwarp();  // the warp's reads of its row buffer are done
+        if (lane == 0 && t + stride < M) {
+            fence_proxy_async();  // generic-proxy reads before the async-proxy overwrite
+            mbar_arrive_expect_tx(&bar[w], row_bytes);
+            bulk_g2s(rowbuf, static_cast<const uint8_t*>(x) + static_cast<size_t>(t + stride) * row_bytes, row_bytes,
+                     &bar[w], policy_evict_first());
         }
     }
 }
@@ -823,6 +937,14 @@ void launch_xprep_rows(const void* x, const DevModel& m, uint8_t* xs, float* ysc
     xprep_gemm_rows_kernel<DT><<<grid, 512, smem, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad, norm);
 }
 template <sfmp_dtype DT>
+void launch_xprep_warp(const void* x, const DevModel& m, uint8_t* xs, float* ysc, const GemmParams& p, int cols, int Mpad,
+                       int nw, int grid, size_t smem, cudaStream_t st, const PreNorm& norm) {
+    static std::once_flag fl[64];
+    once_per_device(fl, [] { cudaFuncSetAttribute(xprep_gemm_warp_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit); });
+    note_launch();
+    xprep_gemm_warp_kernel<DT><<<grid, 32 * nw, smem, st>>>(x, m.d_xslot, xs, ysc, p.M, p.N, p.KC, cols, Mpad, norm);
+}
+template <sfmp_dtype DT>
 void launch_xprep_tok(const void* x, const DevModel& m, uint8_t* xs, float* ysc, const GemmParams& p, int cols, int Mpad,
                       cudaStream_t st, const PreNorm& norm) {
     static std::once_flag fl[64];
@@ -902,8 +1024,24 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     // shared memory (1..4 CTAs per SM)
     const size_t rsm = 16 + (static_cast<size_t>(cols) * 2 + 15) / 16 * 16 + 2 * static_cast<size_t>(cols) * elem;
     const bool rows_ok = cols < 65536 && rsm <= 200 * 1024 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    // warp-per-token pre-pass when >= 8 row buffers fit next to the slot table
+    const size_t wtab = 8 * 16 + (static_cast<size_t>(cols) * 2 + 15) / 16 * 16, wrow = static_cast<size_t>(cols) * elem;
+    const int nw = static_cast<int>(std::min<size_t>(16, (kSmemLimit - 1024 - wtab) / wrow));
+    const size_t wsm = wtab + static_cast<size_t>(std::max(nw, 1)) * wrow;
+    const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(2048 / (32 * std::max(nw, 1)), (kSmemLimit - 1024) / wsm)));
+    // ... and every token gets its own warp (a second round would wait a whole row
+    // copy again: 70B q at M=2048, 1924 warps for 2048 tokens, measured 6 us slower)
+    const bool warp_ok = rows_ok && cols % 8 == 0 && nw >= 8 && SFMP_XPREP_WARP &&
+                         Mpad <= static_cast<int64_t>(nw) * per_sm * m.num_sms;
     cudaError_t e0 = cudaSuccess;
-    if (rows_ok) {
+    if (warp_ok) {
+        const int wgrid = static_cast<int>(std::min<int64_t>((Mpad + nw - 1) / nw, static_cast<int64_t>(per_sm) * m.num_sms));
+        switch (dt) {
+            case SFMP_F32: launch_xprep_warp<SFMP_F32>(x, m, xs, ysc, p, cols, Mpad, nw, wgrid, wsm, st, norm); break;
+            case SFMP_F16: launch_xprep_warp<SFMP_F16>(x, m, xs, ysc, p, cols, Mpad, nw, wgrid, wsm, st, norm); break;
+            default: launch_xprep_warp<SFMP_BF16>(x, m, xs, ysc, p, cols, Mpad, nw, wgrid, wsm, st, norm); break;
+        }
+    } else if (rows_ok) {
         const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / rsm)));
         const int rgrid = static_cast<int>(std::min<int64_t>(Mpad, static_cast<int64_t>(per_sm) * m.num_sms));
         switch (dt) {
