@@ -939,7 +939,7 @@ def main():
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f16", "data": "synthetic",
         "config": {"workload": WORKLOAD, "avg_code_bits": AVG_BITS, "M": MS, "projections": PROJS,
-                   "kernel": "K1 decode GEMV (gemv_kernel) + x pre-pass (xprep_rows_kernel) + fix-up",
+                   "kernel": "K1 decode GEMV (gemv_kernel) + x pre-pass (xprep_gather_kernel) + fix-up (gemv_fixup_kernel, split linears only)",
                    "launch_grouping": ("the whole step is one call (sfmp_gemm_grouped_v): ONE pre-pass + ONE GEMV "
                                        "launch (token counts 1..16 mixed, each linear at its own n-tile count) + "
                                        "ONE fix-up for all 35 problems" if grouped else "one launch per linear") +
