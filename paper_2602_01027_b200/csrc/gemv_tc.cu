@@ -88,6 +88,12 @@ constexpr int kSmemSM = 225 * 1024;
 #ifndef SFMP_EXP_NOMMA
 #define SFMP_EXP_NOMMA 0
 #endif
+#ifndef SFMP_XPREP_MINB
+#define SFMP_XPREP_MINB 8
+#endif
+#ifndef SFMP_EXP_NOPREPASS
+#define SFMP_EXP_NOPREPASS 0
+#endif
 #ifndef SFMP_YTOT_GLOBAL
 #define SFMP_YTOT_GLOBAL 0
 #endif
@@ -408,7 +414,9 @@ __global__ void __launch_bounds__(256) xprep_rows_kernel(const XParams xp) {
 // CTA reads the whole row.  Column sums X_g (lutgemm.cpp:113-115) use the
 // scaled values.
 template <sfmp_dtype DT>
-__global__ void __launch_bounds__(256) xprep_gather_kernel(const XParams xp) {
+// 8 CTAs per SM (<= 32 registers): the step's ~1200 (linear, token, 8 block
+// columns) CTAs then fit in one wave on 148 SMs
+__global__ void __launch_bounds__(256, SFMP_XPREP_MINB) xprep_gather_kernel(const XParams xp) {
     using T = typename XT<DT>::T;
     constexpr bool X2 = DT == SFMP_F32;
     pdl_launch_dependents();  // let the GEMV start streaming weights right away
@@ -1033,7 +1041,8 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xitems, int max_col
     c.stream = st;
     c.attrs = a;
     c.numAttrs = 1;
-    if (!any_norm) {
+    if (SFMP_EXP_NOPREPASS) {  // experiment builds only: records left as they are
+    } else if (!any_norm) {
         note_launch();
         cudaError_t e = cudaLaunchKernelEx(&c, xprep_gather_kernel<DT>, xq);
         if (e != cudaSuccess) return e;
