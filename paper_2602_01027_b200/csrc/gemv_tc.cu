@@ -88,6 +88,9 @@ constexpr int kSmemSM = 225 * 1024;
 #ifndef SFMP_EXP_NOMMA
 #define SFMP_EXP_NOMMA 0
 #endif
+#ifndef SFMP_XPREP_PDL
+#define SFMP_XPREP_PDL 1
+#endif
 #ifndef SFMP_XPREP_MINB
 #define SFMP_XPREP_MINB 8
 #endif
@@ -193,6 +196,7 @@ struct XParams {
     XLin lin[kMaxLin];
     int nlin, M, n_b;
     int wait_prev;  // launched as a programmatic dependent of the previous GEMV
+    int wait_first; // programmatic dependent of whatever ran before: wait before x and the workspace
 };
 
 // Activation record section of one block column (n_b columns) for M tokens
@@ -419,7 +423,10 @@ template <sfmp_dtype DT>
 __global__ void __launch_bounds__(256, SFMP_XPREP_MINB) xprep_gather_kernel(const XParams xp) {
     using T = typename XT<DT>::T;
     constexpr bool X2 = DT == SFMP_F32;
-    pdl_launch_dependents();  // let the GEMV start streaming weights right away
+    // let the GEMV start streaming weights right away -- unless this grid itself
+    // started early (wait_first): then only once the previous grid is done, so
+    // the GEMV never overlaps the previous call's GEMV (shared work queue)
+    if (!xp.wait_first) pdl_launch_dependents();
     __shared__ __align__(16) uint32_t cp[8 * 256];  // [nbc][n_b] column indices
     __shared__ float red[8];
     const int n_b = xp.n_b, CH = n_b >> 7;
@@ -436,6 +443,13 @@ __global__ void __launch_bounds__(256, SFMP_XPREP_MINB) xprep_gather_kernel(cons
         const uint4* src = reinterpret_cast<const uint4*>(XL.col_perm + static_cast<size_t>(bc0) * n_b);
         const uint64_t keep = policy_evict_last();
         for (int i = threadIdx.x; i < nbc * n_b / 4; i += 256) reinterpret_cast<uint4*>(cp)[i] = ldg_keep_v4(src + i, keep);
+    }
+    // prologue done (col_perm is the model's, constant): from here on x -- maybe
+    // the previous kernel's output -- and the workspace the previous call's
+    // GEMV may still read are touched, so wait for the previous grid
+    if (xp.wait_first) {
+        pdl_wait();
+        pdl_launch_dependents();
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1032,9 +1046,12 @@ cudaError_t launch_t(const Params& p, const XParams& xp, int xitems, int max_col
     // workspaces disjoint from the earlier launches'): the pre-pass may start
     // while the previous GEMV still runs, and this call's GEMV then fills the
     // previous one's tail.
-    a[0].val.programmaticStreamSerializationAllowed = overlap_prev ? 1 : 0;
+    a[0].val.programmaticStreamSerializationAllowed = (overlap_prev || (!any_norm && SFMP_XPREP_PDL)) ? 1 : 0;
     XParams xq = xp;
     xq.wait_prev = overlap_prev ? 1 : 0;
+    // the gather pre-pass is always a programmatic dependent: its launch and the
+    // col_perm load overlap the previous kernel's tail, it waits before x
+    xq.wait_first = (!overlap_prev && !any_norm && SFMP_XPREP_PDL) ? 1 : 0;
     cudaLaunchConfig_t c{};
     c.gridDim = dim3(xitems);
     c.blockDim = dim3(256);
