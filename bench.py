@@ -800,20 +800,30 @@ def main():
     dx = {k: dxb[xoff[k]:xoff[k] + k[1] * SHAPES[k[0]][1]].view(k[1], SHAPES[k[0]][1]) for k in keys}
     dy = {k: dyb[yoff[k]:yoff[k] + k[1] * SHAPES[k[0]][0]].view(k[1], SHAPES[k[0]][0]) for k in keys}
     h2d, d2h = xo * 2, yo * 4
-    gx = {M: (xoff[(PROJS[0], M)], xoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][1]) for M in MS}
-    gy = {M: (yoff[(PROJS[0], M)], yoff[(PROJS[-1], M)] + M * SHAPES[PROJS[-1]][0]) for M in MS}
+
+    # a group element is "M" (all seven linears at M) or "M:i-j" (PROJS[i..j] at M,
+    # contiguous in the x and y buffers)
+    def elem(tok):
+        M, _, rng = tok.partition(":")
+        M = int(M)
+        a, _, b = rng.partition("-")
+        i, j = (int(a), int(b or a)) if rng else (0, len(PROJS) - 1)
+        return M, PROJS[i:j + 1]
+
+    def span(off, M, ps, dim):
+        return off[(ps[0], M)], off[(ps[-1], M)] + M * SHAPES[ps[-1]][dim]
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     # group order: a small group first (short exposed H2D), then the largest so its
     # 2.75 MB D2H hides under the later groups' compute, the smallest last (short exposed
     # D2H); measured over 14 orders (tools/gpu_e2e_orders.sh): 2/16/8/4/1 235 us,
     # 1/4/8/16/2 259 us, one group 334 us
-    E2E_GROUPS = ([[int(v) for v in g.split(",")] for g in args.e2e_order.split("/")] if args.e2e_order
-                  else [[2], [16], [8], [4], [1]])
-    assert sorted(M for g in E2E_GROUPS for M in g) == sorted(MS)
+    E2E_ORDER = args.e2e_order or "2/16/8/4/1"
+    E2E_GROUPS = [[elem(v) for v in g.split(",")] for g in E2E_ORDER.split("/")]
+    assert sorted((p, M) for g in E2E_GROUPS for M, ps in g for p in ps) == sorted(keys_all)
     ebufs = {}
     if sharded:
         for gi_, grp in enumerate(E2E_GROUPS):
-            kk = [(p, M) for M in grp for p in PROJS]
+            kk = [(p, M) for M, ps in grp for p in ps]
             ebufs[gi_] = torch.zeros(sfmp.sharded_gather_bytes([models[0][p] for p, M in kk], [M for p, M in kk]) // 4,
                                      device=dev)
 
@@ -824,15 +834,15 @@ def main():
         ready = []
         for grp in E2E_GROUPS:
             with torch.cuda.stream(h2d_s):
-                for M in grp:
-                    a, b = gx[M]
+                for M, ps in grp:
+                    a, b = span(xoff, M, ps, 1)
                     dxb[a:b].copy_(hxb[a:b], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d_s)
                 ready.append(ev)
         for gi_, grp in enumerate(E2E_GROUPS):
             cur.wait_event(ready[gi_])
-            kk = [(p, M) for M in grp for p in PROJS]
+            kk = [(p, M) for M, ps in grp for p in ps]
             ms = [models[(i * len(MS) + MS.index(M)) % COPIES][p] for p, M in kk]
             if not sharded:
                 sfmp.gemm_grouped(ms, [dx[k] for k in kk], outs=[dy[k] for k in kk], workspaces=[wsm[k] for k in kk])
@@ -842,8 +852,8 @@ def main():
             done.record(cur)
             with torch.cuda.stream(d2h_s):
                 d2h_s.wait_event(done)
-                for M in grp:
-                    a, b = gy[M]
+                for M, ps in grp:
+                    a, b = span(yoff, M, ps, 0)
                     hyb[a:b].copy_(dyb[a:b], non_blocking=True)
         cur.wait_stream(d2h_s)
         cur.wait_stream(h2d_s)
@@ -958,7 +968,7 @@ def main():
                 "api": ("pinned host bf16 x -> H2D per M group on a copy stream, one sfmp_gemm_grouped_v "
                         + ("" if not sharded else "/ sfmp_gemm_sharded ") +
                         "call per group, D2H per group on a second copy stream (copies overlap compute); CUDA "
-                        "graph per step, host synchronises on y every step"), "groups": E2E_GROUPS,
+                        "graph per step, host synchronises on y every step"), "groups": E2E_ORDER,
                 "event_us": round(e2e_event_ms * 1e3, 2), "wall_us": round(e2e_wall_ms * 1e3, 2)},
         "gpu_launches": args.steps * launches_per_step,
         "gpu_launches_note": f"{launches_per_step} kernels per step, counted by sfmp_launch_count() "
