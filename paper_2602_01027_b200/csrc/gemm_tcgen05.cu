@@ -23,10 +23,13 @@
 //    1-D bulk copy (no tensor map).  The epilogue multiplies back by 2^e_t.
 //  * Persistent warp-specialised kernel, one CTA per SM, tile = 128 output
 //    rows (MMA M) x N <= 256 tokens (MMA N):
-//      warp 0       producers: lane 0 weight units, lane 1 X atoms (cp.async.bulk)
+//      warp 0       weight producer (lane 0, cp.async.bulk)
 //      warp 1       TMEM allocator + tcgen05.mma issuer (one elected lane)
-//      warps 2-17   epilogue: tcgen05.ld accumulators -> coalesced y stores
-//      warps 18-25  dequant: bit-planes -> codes -> f16(s*c+z) (one exact
+//      warp 2       X producer (lane 0) -- its own warp: as lane 1 of warp 0 it
+//                   stalled behind the weight producer's ring waits (8192x28672
+//                   M=32/64: 73.6/74.7 -> 65.7/67.6 us)
+//      warps 3-18   epilogue: tcgen05.ld accumulators -> coalesced y stores
+//      warps 19-26  dequant: bit-planes -> codes -> f16(s*c+z) (one exact
 //                   HSUB2 + one HFMA2 per weight pair, fp16 s/z as stored)
 //                   written straight into TMEM as the MMA A operand
 //                   (tcgen05.st), so weights never take a shared-memory trip.
@@ -63,11 +66,32 @@ namespace {
 constexpr int kUnitHdr = 528;             // scales[128] | zeros[128] | highmask[4]
 constexpr int kPlaneBytes = 128 * 16;     // one plane of a unit
 // Tile = 128 output rows (MMA M) x N <= 256 tokens (MMA N).
-constexpr int kDeqWarps = 8;              // dequant warps: 4 TMEM lane quarters x kKS K-splits
+#ifndef SFMP_DEQ_WARPS
+#define SFMP_DEQ_WARPS 8
+#endif
+#ifndef SFMP_EPI_WARPS
+#define SFMP_EPI_WARPS 16
+#endif
+constexpr int kDeqWarps = SFMP_DEQ_WARPS;  // dequant warps: 4 TMEM lane quarters x kKS K-splits
 constexpr int kKS = kDeqWarps / 4;        // K splits of a 128-column unit among dequant warps
 constexpr int kWords = 4 / kKS;           // 32-weight words per dequant thread per unit
-constexpr int kEpiWarps = 16;             // epilogue warps: 4 lane quarters x 4 column groups
-constexpr int kThreads = (2 + kEpiWarps + kDeqWarps) * 32;
+constexpr int kEpiWarps = SFMP_EPI_WARPS;  // epilogue warps: 4 lane quarters x column groups
+// SFMP_XPROD_WARP: the X producer runs in its own warp (warp 2) instead of
+// lane 1 of the weight producer's warp
+#ifndef SFMP_XPROD_WARP
+#define SFMP_XPROD_WARP 1
+#endif
+constexpr int kXW = SFMP_XPROD_WARP;
+// SFMP_PROD_SPIN: the producers and dequant warps poll without a suspend hint
+#ifndef SFMP_PROD_SPIN
+#define SFMP_PROD_SPIN 1
+#endif
+__device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    if (SFMP_PROD_SPIN) mbar_wait(bar, parity);
+    else mbar_wait_sleep(bar, parity, ns);
+}
+constexpr int kEpi0 = 2 + kXW;             // first epilogue warp
+constexpr int kThreads = (kEpi0 + kEpiWarps + kDeqWarps) * 32;
 constexpr int kMaxN = 256;                // tokens per tile
 constexpr int kTmemCols = 512;
 constexpr int kAccCol = 0;                // accumulator: columns [0, N)
@@ -564,13 +588,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
     // partial tile, summed in split order by gemm_reduce_kernel.
     const int KC = p.KC;
 
-    if (warp == 0) {
+    if (warp == 0 || (kXW && warp == 2)) {
         // ---------------- producers ----------------
         // Lane 0 streams the weight units, lane 1 the X atoms, each gated only
         // by its own ring: the weights never wait for X slots (which free only
         // as MMAs complete), so dequantisation can run ahead.
         const uint64_t pol_w = policy_evict_first();
-        if (lane == 0) {
+        if (warp == 0 && lane == 0) {
             int ws = 0, wph = 0;
             GSeg sg;
             for (int k = 0; seg_at(p, k, sg); ++k) {
@@ -582,13 +606,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                     const uint64_t a0 = a_next;
                     a_next = __ldg(off0 + (kc - sg.kc0) + 1);
                     const uint32_t n0 = static_cast<uint32_t>(a_next - a0);
-                    mbar_wait_sleep(&wempty[ws], wph ^ 1, 500);
+                    role_wait(&wempty[ws], wph ^ 1, 500);
                     mbar_arrive_expect_tx(&wfull[ws], n0);
                     bulk_g2s(wbuf + static_cast<size_t>(ws) * p.stage_w, p.wl + a0, n0, &wfull[ws], pol_w);
                     if (++ws == SW) { ws = 0; wph ^= 1; }
                 }
             }
-        } else if (lane == 1) {
+        } else if (kXW ? lane == 0 : lane == 1) {
             int xs = 0, xph = 0;
             pdl_wait();  // X is written by the pre-pass (programmatic dependent launch)
             GSeg sg;
@@ -597,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 tile_coords(p, sg.tile, rt, tt);
                 for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
                     for (int h = 0; h < 2; ++h) {
-                        mbar_wait_sleep(&xempty[xs], xph ^ 1, 200);
+                        role_wait(&xempty[xs], xph ^ 1, 200);
                         mbar_arrive_expect_tx(&xfull[xs], xstage);
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -646,14 +670,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
             __syncwarp();
             accph ^= 1;
         }
-    } else if (warp < 2 + kEpiWarps) {
+    } else if (warp < kEpi0 + kEpiWarps) {
         // ---------------- epilogue: TMEM -> registers -> coalesced y rows ----------------
         // kEpiWarps/4 warps per TMEM lane quarter, each owning 256/(kEpiWarps/4)
         // accumulator columns, loaded 32 at a time; the accumulator is
         // released after the last load, so the last stores overlap the next
         // tile's MMAs.
         constexpr int kCols = 256 / (kEpiWarps / 4);
-        const int ew = warp - 2, q = warp & 3, cg = ew >> 2;
+        const int ew = warp - kEpi0, q = warp & 3, cg = ew >> 2;
         int accph = 0;
         GSeg sg;
         for (int k = 0; seg_at(p, k, sg); ++k) {
@@ -706,14 +730,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         }
     } else {
         // ---------------- dequant: bit-planes -> f16 A operand in TMEM ----------------
-        const int dw = warp - 2 - kEpiWarps, q = warp & 3, kh = dw >> 2;
+        const int dw = warp - kEpi0 - kEpiWarps, q = warp & 3, kh = dw >> 2;
         const int r = q * 32 + lane;  // row within the unit = TMEM lane
         const uint32_t woff = static_cast<uint32_t>(kh * kWords * 4);  // byte offset of this warp's words in a row
         int ws = 0, wph = 0, ab = 0, aph = 0;
         GSeg sg;
         for (int k = 0; seg_at(p, k, sg); ++k) {
             for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
-                mbar_wait_sleep(&wfull[ws], wph, 200);
+                role_wait(&wfull[ws], wph, 200);
                 const uint32_t u = smem_u32(wbuf + static_cast<size_t>(ws) * p.stage_w);
                 const __half2 s2 = __half2half2(__ushort_as_half(lds_u16(u + 2 * r)));
                 const __half2 z2 = __half2half2(__ushort_as_half(lds_u16(u + 256 + 2 * r)));
@@ -793,9 +817,12 @@ uint32_t unit_max_bytes(const DevModel& m) {
 // bits -- are the same on any B200, for any shard count.  Chosen by a cost
 // model over a virtual 148-SM grid: waves x (chunks per item x MMA time per
 // chunk + per-item fill/drain) + the split partials' write/read and the
-// reduce launch.  Measured constants (tools/mma_bench.cu, round 1): one
-// 128-column chunk = 8 MMAs of K=16, ~130 cycles each for N <= 128 and ~138
-// at N = 256.
+// reduce launch.  Chunk-time constants: one 128-column chunk = 8 MMAs of
+// K=16 at ~130 cycles each for N <= 128 and ~138 at N = 256.  That is NOT
+// the MMA cost at small N (tools/mma_bench.cu with an unrolled issue loop:
+// 47 / 74 / 138 cycles at N = 64 / 128 / 256) but matches the kernel's measured
+// chunk time there (8192x28672, M=64: ~0.5 us per chunk, bound by the
+// producer/dequant hand-offs, not the tensor pipe), so the model keeps it.
 #ifndef SFMP_KSPLIT_MBPS
 #define SFMP_KSPLIT_MBPS 6.0e6
 #endif

@@ -57,22 +57,41 @@ __global__ void __launch_bounds__(512, 1) bench(int iters, int n, int ss, int bu
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1 && lane == 0) {
+    if (warp == 1) {  // the whole warp runs the loop, one elected lane issues (no divergent waterfall)
         const uint32_t idesc = tc_idesc_f16(128, n);
         const uint64_t bdesc = tc_desc_sw128(smem_u32(smem));
         const uint64_t adesc = tc_desc_sw128(smem_u32(smem + 32768));
         unsigned long long t0 = clock64();
-        for (int i = 0; i < iters; ++i) {
-            uint64_t b = bdesc + ((i & 3) * 2);  // +32 B per k-step
-            if (mode & 1) b += ((i >> 2) & 1) * ((32768) >> 4);  // alternate two 32 KB atoms
-            if (ss) tc_mma_ss(tb, adesc + ((i & 3) * 2), b, idesc, i > 0);
-            else tc_mma_ts(tb, tb + 256 + (i & 7) * 8, b, idesc, i > 0);
+        // mode bit 4: the issue loop unrolled 8 MMAs per elected block with
+        // compile-time descriptor offsets (as gemm_kernel issues a 128-column chunk)
+        if (mode & 16) {
+            for (int i = 0; i < iters; i += 8) {
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        if (ss) tc_mma_ss(tb, adesc + (kk & 3) * 2, bdesc + (kk & 3) * 2, idesc, (i | kk) != 0);
+                        else tc_mma_ts(tb, tb + 256 + kk * 8, bdesc + (kk & 3) * 2, idesc, (i | kk) != 0);
+                    }
+                }
+                __syncwarp();
+            }
+        } else {
+            for (int i = 0; i < iters; ++i) {
+                uint64_t b = bdesc + ((i & 3) * 2);  // +32 B per k-step
+                if (mode & 1) b += ((i >> 2) & 1) * ((32768) >> 4);  // alternate two 32 KB atoms
+                if (elect_one()) {
+                    if (ss) tc_mma_ss(tb, adesc + ((i & 3) * 2), b, idesc, i > 0);
+                    else tc_mma_ts(tb, tb + 256 + (i & 7) * 8, b, idesc, i > 0);
+                }
+                __syncwarp();
+            }
         }
-        tc_commit(bar);
+        if (elect_one()) tc_commit(bar);
+        __syncwarp();
         mbar_wait(bar, 0);
         unsigned long long t1 = clock64();
-        if (blockIdx.x == 0) out[0] = t1 - t0;
-        if (blockIdx.x == 0) out[1] = 0;
+        if (blockIdx.x == 0 && lane == 0) out[0] = t1 - t0;
+        if (blockIdx.x == 0 && lane == 0) out[1] = 0;
     } else if (warp == 2 && (mode & 2)) {
         // TMA-like traffic: 32 KB bulk copies into smem[131072..) back to back
         if (lane == 0) {
@@ -112,11 +131,11 @@ int main(int argc, char** argv) {
     cudaMalloc(&gsrc, 64 << 20);
     cudaMemset(gsrc, 0, 64 << 20);
     const int iters = 4096;
-    for (int mode : {0, 8, 15})
+    for (int mode : {0, 16})
     for (int ss = 0; ss < 2; ++ss)
-        for (int n : {128, 256})
+        for (int n : {32, 64, 128, 256})
             for (int busy : {0}) {
-                if (ss && mode) continue;
+                if (ss && (mode & 15)) continue;
                 bench<<<148, 512, 200000>>>(iters, n, ss, busy, d, mode, gsrc);
                 cudaEvent_t e0, e1;
                 cudaEventCreate(&e0);
