@@ -82,6 +82,10 @@ constexpr int kEpiWarps = SFMP_EPI_WARPS;  // epilogue warps: 4 lane quarters x 
 #define SFMP_XPROD_WARP 1
 #endif
 constexpr int kXW = SFMP_XPROD_WARP;
+// SFMP_EPI_NAMEDBAR: one epilogue warp polls the accumulator barrier, the rest wait on a named barrier
+#ifndef SFMP_EPI_NAMEDBAR
+#define SFMP_EPI_NAMEDBAR 1
+#endif
 // SFMP_PROD_SPIN: the producers and dequant warps poll without a suspend hint
 #ifndef SFMP_PROD_SPIN
 #define SFMP_PROD_SPIN 1
@@ -97,6 +101,12 @@ constexpr int kTmemCols = 512;
 constexpr int kAccCol = 0;                // accumulator: columns [0, N)
 constexpr int kACol = 256;                // A buffer ab at kACol + ab*64 (128 f16 of K per row)
 constexpr int kNA = 4;                    // A buffers
+#ifndef SFMP_SX_MAX
+#define SFMP_SX_MAX 8                     // X ring stages (64-column atoms), at most
+#endif
+#ifndef SFMP_SW_MAX
+#define SFMP_SW_MAX 8                     // weight ring stages (units), at most
+#endif
 constexpr int kSmemLimit = 227 * 1024;
 #ifndef SFMP_XPREP_WARP
 #define SFMP_XPREP_WARP 1  // warp-per-token prefill pre-pass (0: CTA-per-token, experiment builds)
@@ -683,7 +693,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         for (int k = 0; seg_at(p, k, sg); ++k) {
             int rt, tt;
             tile_coords(p, sg.tile, rt, tt);
-            mbar_wait_sleep(accfull, accph, 200);  // a whole tile of MMAs away: sleep between polls
+            // a whole item of MMAs away: one warp polls, the other epilogue warps
+            // block on a named barrier (16 polling warps took ~45 % of the issue
+            // slots from the dequant warps at small N, ncu 8192x28672 M=64)
+            if (!SFMP_EPI_NAMEDBAR || ew == 0) mbar_wait_sleep(accfull, accph, 200);
+            if (SFMP_EPI_NAMEDBAR) named_bar_sync(1, kEpiWarps * 32);
             accph ^= 1;
             tc_fence_after();
             const int c_begin = cg * kCols;
@@ -1029,17 +1043,17 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
     p.stage_w = (unit_max_bytes(m) + 127) / 128 * 128;
     const uint32_t xstage = static_cast<uint32_t>(p.N) * 128;
     const size_t bar_bytes = 1024;
-    // W ring: up to 8 units; X ring: as many 64-column atoms as the rest holds (<= 8)
+    // W ring: up to SFMP_SW_MAX units; X ring: as many 64-column atoms as the rest holds (<= SFMP_SX_MAX)
     const size_t avail = kSmemLimit - 1024 - bar_bytes;
-    p.SW = 8;
-    p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
+    p.SW = SFMP_SW_MAX;
+    p.SX = static_cast<int>(std::min<size_t>(SFMP_SX_MAX, (avail - p.SW * p.stage_w) / xstage));
     while (p.SX < 4 && p.SW > 4) {
         --p.SW;
-        p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
+        p.SX = static_cast<int>(std::min<size_t>(SFMP_SX_MAX, (avail - p.SW * p.stage_w) / xstage));
     }
     if (p.SX < 2) {
         p.SW = 2;
-        p.SX = static_cast<int>(std::min<size_t>(8, (avail - p.SW * p.stage_w) / xstage));
+        p.SX = static_cast<int>(std::min<size_t>(SFMP_SX_MAX, (avail - p.SW * p.stage_w) / xstage));
     }
     if (p.SX < 2) return cudaErrorInvalidConfiguration;
     const size_t smem = 1024 + p.SX * xstage + p.SW * p.stage_w + bar_bytes;
