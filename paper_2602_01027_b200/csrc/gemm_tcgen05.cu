@@ -82,6 +82,11 @@ constexpr int kEpiWarps = SFMP_EPI_WARPS;  // epilogue warps: 4 lane quarters x 
 #define SFMP_XPROD_WARP 1
 #endif
 constexpr int kXW = SFMP_XPROD_WARP;
+// SFMP_DEQ_PIPE (experiment, off): a dequant warp waits for its previous chunk's tcgen05.st after
+// this chunk's math (measured: M=32 -1.5 us, q_proj M=2048 +1.7 us -- STTM latency is not the limiter)
+#ifndef SFMP_DEQ_PIPE
+#define SFMP_DEQ_PIPE 0
+#endif
 // SFMP_EPI_NAMEDBAR: one epilogue warp polls the accumulator barrier, the rest wait on a named barrier
 #ifndef SFMP_EPI_NAMEDBAR
 #define SFMP_EPI_NAMEDBAR 1
@@ -748,6 +753,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         const int r = q * 32 + lane;  // row within the unit = TMEM lane
         const uint32_t woff = static_cast<uint32_t>(kh * kWords * 4);  // byte offset of this warp's words in a row
         int ws = 0, wph = 0, ab = 0, aph = 0;
+        int pend = -1;  // A buffer whose tcgen05.st are still in flight (SFMP_DEQ_PIPE)
+        (void)pend;
         GSeg sg;
         for (int k = 0; seg_at(p, k, sg); ++k) {
             for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
@@ -792,6 +799,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 mbar_wait_sleep(&aempty[ab], aph ^ 1, 300);
                 tc_fence_after();
                 const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + ab * 64 + kh * kWords * 16;
+#if SFMP_DEQ_PIPE
+                // software-pipelined: this chunk's math overlaps the previous chunk's
+                // tcgen05.st, which is waited for (and its A buffer handed to the MMA)
+                // only now
+                uint32_t H[kWords][16];
+#pragma unroll
+                for (int w = 0; w < kWords; ++w) {
+                    uint32_t pw[NP];
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) pw[i] = pl[i][w];
+                    dequant_word<NP>(pw, s2, z2, H[w]);
+                }
+                if (pend >= 0) {
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&afull[pend]);
+                }
+#pragma unroll
+                for (int w = 0; w < kWords; ++w) tc_st_x16(ta + w * 16, H[w]);
+                pend = ab;
+#else
 #pragma unroll
                 for (int w = 0; w < kWords; ++w) {
                     uint32_t pw[NP];
@@ -805,9 +834,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&afull[ab]);
+#endif
                 if (++ws == SW) { ws = 0; wph ^= 1; }
                 if (++ab == kNA) { ab = 0; aph ^= 1; }
             }
+        }
+        if (SFMP_DEQ_PIPE && pend >= 0) {
+            tc_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afull[pend]);
         }
     }
     tc_fence_before();
