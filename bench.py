@@ -814,10 +814,11 @@ def main():
         return off[(ps[0], M)], off[(ps[-1], M)] + M * SHAPES[ps[-1]][dim]
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     # group order: a small group first (short exposed H2D), then the largest so its
-    # 2.75 MB D2H hides under the later groups' compute, the smallest last (short exposed
-    # D2H); measured over 14 orders (tools/gpu_e2e_orders.sh): 2/16/8/4/1 235 us,
-    # 1/4/8/16/2 259 us, one group 334 us
-    E2E_ORDER = args.e2e_order or "2/16/8/4/1"
+    # 2.75 MB D2H hides under the later groups' compute, M=4 and 8 in one call (one
+    # launch's fixed costs fewer), the smallest last (short exposed D2H); measured
+    # (tools/gpu_e2e_orders.sh, profiles/r02_e2e_orders.txt): 2/16/4,8/1 221-223 us,
+    # 2/16/8/4/1 235-250 us, 1/4/8/16/2 259 us, one group 334 us
+    E2E_ORDER = args.e2e_order or "2/16/4,8/1"
     E2E_GROUPS = [[elem(v) for v in g.split(",")] for g in E2E_ORDER.split("/")]
     assert sorted((p, M) for g in E2E_GROUPS for M, ps in g for p in ps) == sorted(keys_all)
     ebufs = {}
