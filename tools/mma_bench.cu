@@ -131,7 +131,7 @@ int main(int argc, char** argv) {
     cudaMalloc(&gsrc, 64 << 20);
     cudaMemset(gsrc, 0, 64 << 20);
     const int iters = 4096;
-    for (int mode : {0, 16})
+    for (int mode : {0, 16, 20})
     for (int ss = 0; ss < 2; ++ss)
         for (int n : {32, 64, 128, 256})
             for (int busy : {0}) {
