@@ -29,7 +29,8 @@
 //                   stalled behind the weight producer's ring waits (8192x28672
 //                   M=32/64: 73.6/74.7 -> 65.7/67.6 us)
 //      warps 3-18   epilogue: tcgen05.ld accumulators -> coalesced y stores
-//      warps 19-26  dequant: bit-planes -> codes -> f16(s*c+z) (one exact
+//      warps 19-26  dequant (two per TMEM lane quarter, whole chunks in turn):
+//                   bit-planes -> codes -> f16(s*c+z) (one exact
 //                   HSUB2 + one HFMA2 per weight pair, fp16 s/z as stored)
 //                   written straight into TMEM as the MMA A operand
 //                   (tcgen05.st), so weights never take a shared-memory trip.
@@ -74,7 +75,13 @@ constexpr int kPlaneBytes = 128 * 16;     // one plane of a unit
 #endif
 constexpr int kDeqWarps = SFMP_DEQ_WARPS;  // dequant warps: 4 TMEM lane quarters x kKS K-splits
 constexpr int kKS = kDeqWarps / 4;        // K splits of a 128-column unit among dequant warps
-constexpr int kWords = 4 / kKS;           // 32-weight words per dequant thread per unit
+// SFMP_DEQ_IL: the kKS dequant warps of a TMEM lane quarter take whole chunks in turn
+// (chunk i -> group i % kKS) instead of splitting every chunk's K among them
+#ifndef SFMP_DEQ_IL
+#define SFMP_DEQ_IL 1
+#endif
+constexpr int kWords = SFMP_DEQ_IL ? 4 : 4 / kKS;  // 32-weight words per dequant thread per unit
+constexpr int kDeqPerChunk = SFMP_DEQ_IL ? 4 : kDeqWarps;  // dequant warps that handle one chunk
 constexpr int kEpiWarps = SFMP_EPI_WARPS;  // epilogue warps: 4 lane quarters x column groups
 // SFMP_XPROD_WARP: the X producer runs in its own warp (warp 2) instead of
 // lane 1 of the weight producer's warp
@@ -576,10 +583,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         }
         for (int s = 0; s < SW; ++s) {
             mbar_init(&wfull[s], 1);
-            mbar_init(&wempty[s], kDeqWarps);
+            mbar_init(&wempty[s], kDeqPerChunk);
         }
         for (int a = 0; a < kNA; ++a) {
-            mbar_init(&afull[a], kDeqWarps);
+            mbar_init(&afull[a], kDeqPerChunk);
             mbar_init(&aempty[a], 1);
         }
         mbar_init(accfull, 1);
@@ -751,13 +758,19 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
         // ---------------- dequant: bit-planes -> f16 A operand in TMEM ----------------
         const int dw = warp - kEpi0 - kEpiWarps, q = warp & 3, kh = dw >> 2;
         const int r = q * 32 + lane;  // row within the unit = TMEM lane
-        const uint32_t woff = static_cast<uint32_t>(kh * kWords * 4);  // byte offset of this warp's words in a row
+        const uint32_t woff = SFMP_DEQ_IL ? 0u : static_cast<uint32_t>(kh * kWords * 4);  // this warp's words in a row
+        int cc = 0;  // chunk counter (SFMP_DEQ_IL: this warp's chunks are cc % kKS == kh)
         int ws = 0, wph = 0, ab = 0, aph = 0;
         int pend = -1;  // A buffer whose tcgen05.st are still in flight (SFMP_DEQ_PIPE)
         (void)pend;
         GSeg sg;
         for (int k = 0; seg_at(p, k, sg); ++k) {
             for (int kc = sg.kc0; kc < sg.kc1; ++kc) {
+                if (SFMP_DEQ_IL && (cc++ % kKS) != kh) {  // another group's chunk
+                    if (++ws == SW) { ws = 0; wph ^= 1; }
+                    if (++ab == kNA) { ab = 0; aph ^= 1; }
+                    continue;
+                }
                 role_wait(&wfull[ws], wph, 200);
                 const uint32_t u = smem_u32(wbuf + static_cast<size_t>(ws) * p.stage_w);
                 const __half2 s2 = __half2half2(__ushort_as_half(lds_u16(u + 2 * r)));
@@ -798,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const GemmParams p) {
                 // buffer before the math costs little and keeps registers low
                 mbar_wait_sleep(&aempty[ab], aph ^ 1, 300);
                 tc_fence_after();
-                const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + ab * 64 + kh * kWords * 16;
+                const uint32_t ta = tbase + (static_cast<uint32_t>(q * 32) << 16) + kACol + ab * 64 + (SFMP_DEQ_IL ? 0 : kh * kWords * 16);
 #if SFMP_DEQ_PIPE
                 // software-pipelined: this chunk's math overlaps the previous chunk's
                 // tcgen05.st, which is waited for (and its A buffer handed to the MMA)
@@ -1091,7 +1104,8 @@ cudaError_t launch_gemm(const DevModel& m, const void* x, sfmp_dtype dt, int64_t
         p.SW = 2;
         p.SX = static_cast<int>(std::min<size_t>(SFMP_SX_MAX, (avail - p.SW * p.stage_w) / xstage));
     }
-    if (p.SX < 2) return cudaErrorInvalidConfiguration;
+    if (SFMP_DEQ_IL) p.SW -= p.SW % kKS;  // a weight stage always meets the same dequant group
+    if (p.SX < 2 || p.SW < kKS) return cudaErrorInvalidConfiguration;
     const size_t smem = 1024 + p.SX * xstage + p.SW * p.stage_w + bar_bytes;
     // K4 (prefill flavour): gather + scale + convert + swizzle X
     const int cols = static_cast<int>(m.cols);
